@@ -1,0 +1,258 @@
+"""Oracle — TEST INFRASTRUCTURE ONLY.
+
+Plain CPU implementations of what the hot path computes, written from the
+paper (arXiv 2501.01005, /root/reference/PAPER.md) and independent of the CUDA
+path: the two share no code, and neither imports the other. Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and
+``--impl reference``) may import this package.
+
+Contents
+  * ``paged_attention``   float64 C oracle (``bsra_oracle.c``), Eq. 1-2 over the BSR page
+                          table, causal/custom masks, GQA.
+  * ``brute_force``       NumPy: un-page to dense K/V, materialise masked scores, float64
+                          softmax. Pins the C oracle (different code, same definition).
+  * ``merge`` / ``merge_all``   ⊕ of attention states, float64.
+  * ``split_attention``   P contiguous KV shards, each through the oracle, merged in order.
+  * ``scheduler_ref``     Algorithm 1 re-implemented in Python.
+
+Every function that has no independent pin says so ("parity unpinned") in its
+docstring; see DESIGN.md §Oracle.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liborc.so")
+_SRC = os.path.join(_HERE, "bsra_oracle.c")
+_lib = None
+
+DT_CODE = {"f32": 0, "f16": 1, "bf16": 2}
+MASK_CODE = {"none": 0, "causal": 1, "custom": 2}
+
+
+def build(force: bool = False) -> str:
+    """Compile the C oracle (gcc -O2 -fopenmp). Building the checker is not using it."""
+    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-o", _SO,
+                               _SRC, "-lm"])
+    return _SO
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_SO)
+        P = ctypes.c_void_p
+        lib.orc_paged_attention.restype = ctypes.c_int
+        lib.orc_paged_attention.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P,
+                                            ctypes.c_int, P, P, ctypes.c_double, P, ctypes.c_int, P, P,
+                                            ctypes.c_int]
+        lib.orc_merge.restype = None
+        lib.orc_merge.argtypes = [ctypes.c_int64, ctypes.c_int, P, P, P, P, P, P]
+        lib.orc_decode.restype = ctypes.c_double
+        lib.orc_decode.argtypes = [ctypes.c_int, ctypes.c_uint32]
+        _lib = lib
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def decode_scalar(dtype: str, bits: int) -> float:
+    return _load().orc_decode(DT_CODE[dtype], int(bits))
+
+
+def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
+                    k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
+                    mask_bit_indptr=None, sm_scale, req_list: Optional[Sequence[int]] = None,
+                    num_threads: int = 0, out=None):
+    """float64 oracle (C). Array arguments are host numpy arrays; ``q``/pools hold raw
+    element bits (float32, or uint16 bits for f16/bf16). Returns (o, lse) float64 with
+    shapes [sum l_qo, H_qo, D] and [sum l_qo, H_qo]. With ``req_list`` only those requests
+    are computed (other rows stay NaN)."""
+    lib = _load()
+    qo_indptr = np.ascontiguousarray(qo_indptr, np.int32)
+    kv_page_indptr = np.ascontiguousarray(kv_page_indptr, np.int32)
+    kv_last_page_len = np.ascontiguousarray(kv_last_page_len, np.int32)
+    kv_page_indices = np.ascontiguousarray(kv_page_indices, np.int32)
+    batch = len(qo_indptr) - 1
+    nq = int(qo_indptr[-1])
+    if out is None:
+        o = np.full((nq, H_qo, D), np.nan)
+        lse = np.full((nq, H_qo), np.nan)
+    else:
+        o, lse = out
+    ks = np.ascontiguousarray(k_strides, np.int64)
+    vs = np.ascontiguousarray(v_strides, np.int64)
+    rl = None if req_list is None else np.ascontiguousarray(req_list, np.int32)
+    cm = None if custom_mask is None else np.ascontiguousarray(custom_mask, np.uint8)
+    mb = None if mask_bit_indptr is None else np.ascontiguousarray(mask_bit_indptr, np.int64)
+    q = np.ascontiguousarray(q)
+    k_pool = np.asarray(k_pool)
+    v_pool = np.asarray(v_pool)
+    rc = lib.orc_paged_attention(batch, _ptr(qo_indptr), _ptr(kv_page_indptr), _ptr(kv_last_page_len),
+                                 _ptr(kv_page_indices), H_qo, H_kv, D, page_size, DT_CODE[dtype], _ptr(q),
+                                 _ptr(k_pool), _ptr(v_pool), _ptr(ks), _ptr(vs), MASK_CODE[mask], _ptr(cm),
+                                 _ptr(mb), float(sm_scale), _ptr(rl), 0 if rl is None else len(rl), _ptr(o),
+                                 _ptr(lse), int(num_threads))
+    if rc != 0:
+        raise ValueError(f"orc_paged_attention failed with code {rc}")
+    return o, lse
+
+
+def attention_from_inputs(inp, req_list=None, num_threads=0):
+    """Convenience: run the C oracle on a ``synth.Inputs`` (tensors copied to host)."""
+    from synth import raw_bits  # input generator only (no method arithmetic)
+    wl = inp.wl
+    return paged_attention(
+        qo_indptr=inp.qo_indptr, kv_page_indptr=inp.kv_page_indptr, kv_last_page_len=inp.kv_last_page_len,
+        kv_page_indices=inp.kv_page_indices.cpu().numpy(), q=raw_bits(inp.q), k_pool=raw_bits(inp.k_pool),
+        v_pool=raw_bits(inp.v_pool), k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo,
+        H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
+        custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
+        mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, req_list=req_list,
+        num_threads=num_threads)
+
+
+# ------------------------------------------------------------- brute force ---
+def to_float64(bits: np.ndarray, dtype: str) -> np.ndarray:
+    """Exact upcast via numpy's own float types (independent of the C decoders)."""
+    if dtype == "f32":
+        return np.asarray(bits, np.float32).astype(np.float64)
+    if dtype == "f16":
+        return np.asarray(bits, np.uint16).view(np.float16).astype(np.float64)
+    u32 = np.asarray(bits, np.uint16).astype(np.uint32) << 16
+    return u32.view(np.float32).astype(np.float64)
+
+
+def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
+                k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
+                mask_bit_indptr=None, sm_scale):
+    """NumPy brute force (tiny inputs): dense un-paged K/V per request, the full masked
+    score matrix, float64 softmax. Same definition as the C oracle, different code."""
+    qf = to_float64(q, dtype).reshape(-1, H_qo, D)
+    kflat = to_float64(k_pool, dtype).reshape(-1)
+    vflat = to_float64(v_pool, dtype).reshape(-1)
+    g = H_qo // H_kv
+    nq = int(qo_indptr[-1])
+    o = np.zeros((nq, H_qo, D))
+    lse = np.full((nq, H_qo), -np.inf)
+    bits = None
+    if mask == "custom":
+        bits = np.unpackbits(np.asarray(custom_mask, np.uint8), bitorder="little").astype(bool)
+    for i in range(len(qo_indptr) - 1):
+        q0, q1 = int(qo_indptr[i]), int(qo_indptr[i + 1])
+        p0, p1 = int(kv_page_indptr[i]), int(kv_page_indptr[i + 1])
+        lq = q1 - q0
+        lk = 0 if p1 == p0 else (p1 - p0 - 1) * page_size + int(kv_last_page_len[i])
+        if lq == 0:
+            continue
+        t = np.arange(lk)
+        pages = np.asarray(kv_page_indices[p0:p1], np.int64)[t // page_size] if lk else np.zeros(0, np.int64)
+        slot = t % page_size
+        hk = np.arange(H_kv)
+        d = np.arange(D)
+        kidx = (pages[:, None, None] * k_strides[0] + slot[:, None, None] * k_strides[1]
+                + hk[None, :, None] * k_strides[2] + d[None, None, :])
+        vidx = (pages[:, None, None] * v_strides[0] + slot[:, None, None] * v_strides[1]
+                + hk[None, :, None] * v_strides[2] + d[None, None, :])
+        Kd = kflat[kidx]  # [lk, H_kv, D]
+        Vd = vflat[vidx]
+        Kr = np.repeat(Kd, g, axis=1)  # GQA: head h uses kv head h // g
+        Vr = np.repeat(Vd, g, axis=1)
+        S = sm_scale * np.einsum("rhd,thd->hrt", qf[q0:q1], Kr)  # [H, lq, lk]
+        if mask == "none":
+            vis = np.ones((lq, lk), bool)
+        elif mask == "causal":
+            vis = np.arange(lk)[None, :] <= (lk - lq + np.arange(lq))[:, None]
+        else:
+            b0 = int(mask_bit_indptr[i])
+            vis = bits[b0:b0 + lq * lk].reshape(lq, lk)
+        S = np.where(vis[None], S, -np.inf)
+        m = S.max(axis=2, initial=-np.inf, keepdims=True)
+        msafe = np.where(np.isfinite(m), m, 0.0)
+        P = np.where(vis[None], np.exp(S - msafe), 0.0)
+        Z = P.sum(axis=2, keepdims=True)
+        nz = Z[..., 0] > 0
+        l = np.where(nz, (msafe[..., 0] + np.log(np.where(nz, Z[..., 0], 1.0))), -np.inf)
+        O = np.einsum("hrt,thd->rhd", P / np.where(Z > 0, Z, 1.0), Vr)
+        o[q0:q1] = O
+        lse[q0:q1] = l.T
+    return o, lse
+
+
+def brute_force_from_inputs(inp):
+    from synth import raw_bits
+    wl = inp.wl
+    return brute_force(
+        qo_indptr=inp.qo_indptr, kv_page_indptr=inp.kv_page_indptr, kv_last_page_len=inp.kv_last_page_len,
+        kv_page_indices=inp.kv_page_indices.cpu().numpy(), q=raw_bits(inp.q), k_pool=raw_bits(inp.k_pool),
+        v_pool=raw_bits(inp.v_pool), k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo,
+        H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
+        custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
+        mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale)
+
+
+# --------------------------------------------------------------------- ⊕ ---
+def merge(o_a, lse_a, o_b, lse_b):
+    """⊕, float64 C implementation, max-shifted; empty state is the
+    identity (R3). Shapes: o [..., D], lse [...]."""
+    lib = _load()
+    o_a = np.ascontiguousarray(o_a, np.float64)
+    o_b = np.ascontiguousarray(o_b, np.float64)
+    lse_a = np.ascontiguousarray(lse_a, np.float64)
+    lse_b = np.ascontiguousarray(lse_b, np.float64)
+    D = o_a.shape[-1]
+    rows = int(lse_a.size)
+    o = np.empty_like(o_a)
+    lse = np.empty_like(lse_a)
+    lib.orc_merge(rows, D, _ptr(o_a), _ptr(lse_a), _ptr(o_b), _ptr(lse_b), _ptr(o), _ptr(lse))
+    return o, lse
+
+
+def merge_all(states):
+    """Left fold of ⊕ in the given order ("composed in any order")."""
+    o, lse = states[0]
+    for ob, lb in states[1:]:
+        o, lse = merge(o, lse, ob, lb)
+    return o, lse
+
+
+def split_attention(inp, P: int, num_threads=0):
+    """Sequence split (Ring-Attention/Flash-Decoding use of ⊕): every
+    request's pages are cut into P contiguous page ranges (rank r owns pages
+    [r*n/P, (r+1)*n/P)); each shard goes through the oracle; states merged in rank order.
+    Only meaningful for mask 'none'."""
+    from synth import raw_bits
+    wl = inp.wl
+    assert wl.mask == "none"
+    idx = inp.kv_page_indices.cpu().numpy()
+    states = []
+    for r in range(P):
+        indptr = [0]
+        sel = []
+        last = []
+        for i in range(wl.batch):
+            p0, p1 = int(inp.kv_page_indptr[i]), int(inp.kv_page_indptr[i + 1])
+            n = p1 - p0
+            a, b = p0 + (r * n) // P, p0 + ((r + 1) * n) // P
+            sel.append(idx[a:b])
+            indptr.append(indptr[-1] + (b - a))
+            last.append(int(inp.kv_last_page_len[i]) if (b == p1 and b > a) else wl.page_size)
+        o, lse = paged_attention(
+            qo_indptr=inp.qo_indptr, kv_page_indptr=np.array(indptr, np.int32),
+            kv_last_page_len=np.array(last, np.int32), kv_page_indices=np.concatenate(sel).astype(np.int32),
+            q=raw_bits(inp.q), k_pool=raw_bits(inp.k_pool), v_pool=raw_bits(inp.v_pool),
+            k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D,
+            page_size=wl.page_size, dtype=wl.dtype, sm_scale=inp.sm_scale, num_threads=num_threads)
+        states.append((o, lse))
+    return merge_all(states)

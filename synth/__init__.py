@@ -1,0 +1,223 @@
+"""Seeded synthetic inputs shared by the oracle side and the CUDA side.
+
+This module holds NO arithmetic of the method (no softmax, no scheduling, no
+merge). It only draws lengths and values and lays them out in the paged (BSR)
+storage format the paper describes (§3.1.1): a ragged query
+tensor indexed by ``qo_indptr`` and a KV pool of pages indexed by
+``kv_page_indptr`` / ``kv_page_indices`` / ``kv_last_page_len``.
+
+Recipe:
+  * numpy ``Generator(PCG64)`` for lengths, torch generators for values;
+    seeds: lengths 0, q 1, k 2, v 3, page permutation 4, custom mask 5
+    (each offset by ``seed_base``);
+  * q, k ~ N(0, 1); v ~ U(-1, 1) (needed for the 1e-2 o tolerance);
+    a "peaked" variant scales q by ``q_scale``;
+  * physical page placement is a random permutation of the pool (seed 4), so
+    the gather is truly scattered; ``permute=False`` gives contiguous placement;
+  * pool layout NHD ``[num_pages, page_size, H_kv, D]`` by default, ``HND``
+    (``[num_pages, H_kv, page_size, D]``) available; strides are reported in
+    elements as (page, token, head).
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Optional
+
+import numpy as np
+import torch
+
+DTYPES = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+MASKS = ("none", "causal", "custom")
+
+SEED_LEN, SEED_Q, SEED_K, SEED_V, SEED_PERM, SEED_MASK = 0, 1, 2, 3, 4, 5
+
+
+@dataclasses.dataclass
+class Workload:
+    name: str
+    H_qo: int
+    H_kv: int
+    D: int
+    page_size: int
+    dtype: str
+    mask: str
+    qo_lens: np.ndarray  # int32 [B]
+    kv_lens: np.ndarray  # int32 [B]
+
+    @property
+    def batch(self) -> int:
+        return int(len(self.qo_lens))
+
+    @property
+    def g(self) -> int:
+        return self.H_qo // self.H_kv
+
+    def num_pages(self) -> np.ndarray:
+        ps = self.page_size
+        return ((self.kv_lens.astype(np.int64) + ps - 1) // ps).astype(np.int64)
+
+
+# ---------------------------------------------------------------- configs ---
+def c1_tiny_decode() -> Workload:
+    """BASELINE.json configs[0]: batch 2, 4/1 heads, d 64, page 4, kv {5, 37}, fp32."""
+    return Workload("c1_tiny_decode", 4, 1, 64, 4, "f32", "none",
+                    np.array([1, 1], np.int32), np.array([5, 37], np.int32))
+
+
+def sharegpt_like_kv_lens(batch: int = 128, seed: int = SEED_LEN) -> np.ndarray:
+    """Log-normal, ShareGPT-like decode lengths clipped to [128, 4096]."""
+    r = np.random.default_rng(seed)
+    return np.clip(np.round(np.exp(r.normal(np.log(800), 0.9, batch))), 128, 4096).astype(np.int32)
+
+
+def c2_decode_llama8b(batch: int = 128, seed: int = SEED_LEN) -> Workload:
+    """BASELINE.json configs[1]: batched paged decode, 32/8 heads, d 128, page 16, bf16."""
+    kv = sharegpt_like_kv_lens(batch, seed)
+    return Workload("c2_decode_llama8b", 32, 8, 128, 16, "bf16", "none", np.ones(batch, np.int32), kv)
+
+
+def c3_prefill_llama70b(batch: int = 16, seed: int = SEED_LEN, mask: str = "causal") -> Workload:
+    """BASELINE.json configs[2]: ragged causal prefill, 64/8 heads, d 128, page 16, qo 64..2048."""
+    qo = np.random.default_rng(seed).integers(64, 2049, batch).astype(np.int32)
+    return Workload("c3_prefill_llama70b", 64, 8, 128, 16, "bf16", mask, qo, qo.copy())
+
+
+def c5_long_decode(batch: int = 4, kv_len: int = 524288) -> Workload:
+    """BASELINE.json configs[4]: long-context decode, 32/8 heads, d 128, page 16, kv 512K."""
+    return Workload("c5_long_decode", 32, 8, 128, 16, "bf16", "none",
+                    np.ones(batch, np.int32), np.full(batch, kv_len, np.int32))
+
+
+def random_workload(rng: np.random.Generator, *, max_batch=6, max_qo=40, max_kv=90,
+                    heads=((4, 1), (4, 4), (8, 1), (8, 2)), dims=(64, 128),
+                    page_sizes=(1, 2, 4, 16), dtype="f32", mask=None) -> Workload:
+    """Small random workload (ragged, with empty requests) for parity sweeps."""
+    B = int(rng.integers(1, max_batch + 1))
+    H_qo, H_kv = heads[int(rng.integers(len(heads)))]
+    D = int(dims[int(rng.integers(len(dims)))])
+    ps = int(page_sizes[int(rng.integers(len(page_sizes)))])
+    m = mask or MASKS[int(rng.integers(3))]
+    qo = rng.integers(0, max_qo + 1, B).astype(np.int32)
+    kv = rng.integers(0, max_kv + 1, B).astype(np.int32)
+    if m == "causal":
+        kv = np.maximum(kv, qo)  # incremental prefill: l_qo <= l_kv
+    return Workload("random", H_qo, H_kv, D, ps, dtype, m, qo, kv)
+
+
+# ------------------------------------------------------------ materialise ---
+@dataclasses.dataclass
+class Inputs:
+    wl: Workload
+    qo_indptr: np.ndarray       # int32 [B+1]
+    kv_page_indptr: np.ndarray  # int32 [B+1]
+    kv_last_page_len: np.ndarray  # int32 [B]
+    kv_page_indices: torch.Tensor  # int32 [nnz]
+    q: torch.Tensor             # [sum l_qo, H_qo, D]
+    k_pool: torch.Tensor        # NHD [P, ps, H_kv, D] or HND [P, H_kv, ps, D]
+    v_pool: torch.Tensor
+    k_strides: tuple            # elements (page, token, head)
+    v_strides: tuple
+    custom_mask: Optional[torch.Tensor]  # uint8 packed bits, LSB first
+    mask_bit_indptr: Optional[np.ndarray]  # int64 [B+1]
+    sm_scale: float
+
+    @property
+    def device(self):
+        return self.q.device
+
+
+def _gen(device, seed):
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    return g
+
+
+def page_table(wl: Workload, *, permute=True, seed_base=0, extra_pages=0):
+    """Page table in BSR form: kv_page_indptr, kv_page_indices, kv_last_page_len."""
+    n = wl.num_pages()
+    indptr = np.zeros(wl.batch + 1, np.int64)
+    indptr[1:] = np.cumsum(n)
+    nnz = int(indptr[-1])
+    total_pages = nnz + extra_pages
+    if permute:
+        perm = np.random.default_rng(SEED_PERM + seed_base).permutation(total_pages)[:nnz]
+    else:
+        perm = np.arange(nnz)
+    last = np.where(n > 0, wl.kv_lens - (n - 1) * wl.page_size, 0).astype(np.int32)
+    # requests with pages have last_page_len in [1, page_size]
+    return indptr.astype(np.int32), perm.astype(np.int32), last, total_pages
+
+
+def custom_mask_bits(wl: Workload, *, seed_base=0, density=0.5, causal_and=True):
+    """Per request, row-major l_qo x l_kv bits (R9), packed LSB-first.
+
+    Bernoulli(density) AND (optionally) right-aligned lower-triangular, with the
+    diagonal t = l_kv - l_qo + r forced visible when it exists."""
+    r = np.random.default_rng(SEED_MASK + seed_base)
+    bit_indptr = np.zeros(wl.batch + 1, np.int64)
+    chunks = []
+    for i in range(wl.batch):
+        lq, lk = int(wl.qo_lens[i]), int(wl.kv_lens[i])
+        bits = r.random((lq, lk)) < density
+        if causal_and and lq > 0 and lk > 0:
+            rows = np.arange(lq)[:, None]
+            cols = np.arange(lk)[None, :]
+            lim = lk - lq + rows
+            bits &= cols <= lim
+            diag_ok = (lim >= 0) & (lim < lk)
+            rr = np.nonzero(diag_ok[:, 0])[0]
+            bits[rr, (lk - lq + rr)] = True
+        chunks.append(bits.reshape(-1))
+        bit_indptr[i + 1] = bit_indptr[i] + lq * lk
+    flat = np.concatenate(chunks) if chunks else np.zeros(0, bool)
+    packed = np.packbits(flat.astype(np.uint8), bitorder="little")
+    if packed.size == 0:
+        packed = np.zeros(1, np.uint8)
+    return packed, bit_indptr
+
+
+def make_inputs(wl: Workload, *, device="cpu", seed_base=0, permute=True, layout="NHD",
+                q_scale=1.0, sm_scale=None, extra_pages=0, mask_bits=None) -> Inputs:
+    dt = DTYPES[wl.dtype]
+    qo_indptr = np.zeros(wl.batch + 1, np.int32)
+    qo_indptr[1:] = np.cumsum(wl.qo_lens)
+    kv_indptr, kv_indices, last, total_pages = page_table(wl, permute=permute, seed_base=seed_base,
+                                                          extra_pages=extra_pages)
+    nq = int(qo_indptr[-1])
+    q = torch.randn((nq, wl.H_qo, wl.D), generator=_gen(device, SEED_Q + seed_base), device=device,
+                    dtype=torch.float32)
+    if q_scale != 1.0:
+        q.mul_(q_scale)
+    q = q.to(dt)
+    if layout == "NHD":
+        shape = (total_pages, wl.page_size, wl.H_kv, wl.D)
+        strides = (wl.page_size * wl.H_kv * wl.D, wl.H_kv * wl.D, wl.D)
+    elif layout == "HND":
+        shape = (total_pages, wl.H_kv, wl.page_size, wl.D)
+        strides = (wl.page_size * wl.H_kv * wl.D, wl.D, wl.page_size * wl.D)
+    else:
+        raise ValueError(layout)
+    k = torch.empty(shape, device=device, dtype=dt)
+    v = torch.empty(shape, device=device, dtype=dt)
+    # generate in slabs to bound fp32 temporaries on large pools
+    slab = max(1, (1 << 26) // max(1, int(np.prod(shape[1:]))))
+    gk, gv = _gen(device, SEED_K + seed_base), _gen(device, SEED_V + seed_base)
+    for s in range(0, total_pages, slab):
+        e = min(total_pages, s + slab)
+        k[s:e] = torch.randn((e - s,) + shape[1:], generator=gk, device=device).to(dt)
+        v[s:e] = (torch.rand((e - s,) + shape[1:], generator=gv, device=device) * 2 - 1).to(dt)
+    cm, mbi = None, None
+    if wl.mask == "custom":
+        packed, mbi = mask_bits if mask_bits is not None else custom_mask_bits(wl, seed_base=seed_base)
+        cm = torch.from_numpy(packed).to(device)
+    return Inputs(wl, qo_indptr, kv_indptr, last, torch.from_numpy(kv_indices).to(device), q, k, v,
+                  strides, strides, cm, mbi,
+                  float(sm_scale) if sm_scale is not None else 1.0 / float(np.sqrt(wl.D)))
+
+
+def raw_bits(t: torch.Tensor) -> np.ndarray:
+    """Host numpy view of a tensor's storage: float32 stays float32, 16-bit types as uint16 bits."""
+    t = t.detach().cpu().contiguous()
+    if t.dtype == torch.float32:
+        return t.numpy()
+    return t.view(torch.int16).numpy().view(np.uint16)
