@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""bench.py — paged decode HBM TB/s (BASELINE.json configs[1]) on B200, plus the prefill
+TFLOP/s of configs[2] as a secondary figure, through the libbsra C ABI.
+
+A step = one decode generation step of the hot path for a
+Llama-3-8B-shaped model: plan() once (host Algorithm 1 + H2D of the plan image) and
+run() for every one of `--layers` layers (distinct q / KV pools / o per layer, the same plan,
+replayed from one CUDA graph). value = KV bytes (+ q, o, lse, indices) per step /
+device time. Every layer's KV pool is 621 MB >> 126 MB L2, so no layer is L2-resident when
+it is read (no flush needed; stated in config).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 (torchrun): every rank runs its own configs[1] batch (requests sharded, no collective
+on the data path) -> "scaling": "weak"; the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(PEAKS_PATH) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------ clocks ---
+class ClockSampler:
+    """nvidia-smi clock / throttle sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+            time.sleep(0.05)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[5 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- workloads ---
+def decode_bytes(wl) -> dict:
+    """Algorithmic bytes of one decode layer: every KV byte once per kv head,
+    plus q, o (dtype), lse (fp32) and the BSR arrays (int32)."""
+    es = 2 if wl.dtype in ("bf16", "f16") else 4
+    kv = int(wl.kv_lens.astype(np.int64).sum()) * wl.H_kv * wl.D * 2 * es
+    nq = int(wl.qo_lens.sum())
+    qo = 2 * nq * wl.H_qo * wl.D * es + nq * wl.H_qo * 4
+    idx = int(wl.num_pages().sum()) * 4 + 3 * (wl.batch + 1) * 4
+    return {"kv": kv, "total": kv + qo + idx}
+
+
+def causal_flops(wl) -> float:
+    """4*D flops per visible (query, key, qo head) pair."""
+    pairs = 0
+    for lq, lk in zip(wl.qo_lens.astype(np.int64), wl.kv_lens.astype(np.int64)):
+        # right-aligned causal: row r sees min(lk, lk - lq + r + 1) keys
+        r = np.arange(lq)
+        pairs += int(np.clip(lk - lq + r + 1, 0, lk).sum())
+    return 4.0 * wl.D * wl.H_qo * pairs
+
+
+class Layered:
+    """R layers of one workload: per-layer q / K / V pools / o, one shared page table."""
+
+    def __init__(self, wl, layers, device, seed_base=0):
+        import paper_2501_01005_b200 as bsra
+        self.wl = wl
+        self.layers = []
+        for r in range(layers):
+            inp = synth.make_inputs(wl, device=device, seed_base=seed_base + 100 * r)
+            nq = int(inp.qo_indptr[-1])
+            o = torch.empty((nq, wl.H_qo, wl.D), device=device, dtype=inp.q.dtype)
+            lse = torch.empty((nq, wl.H_qo), device=device)
+            if r > 0:  # one page table per model (shared by all layers)
+                inp.kv_page_indices = self.layers[0][0].kv_page_indices
+            self.layers.append((inp, o, lse))
+        self.inp0 = self.layers[0][0]
+        self.bsra = bsra
+
+    def engine(self, **kw):
+        wl = self.wl
+        cfg = self.bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
+                                    mask=wl.mask, max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()), **kw)
+        return self.bsra.Engine(cfg, torch.cuda.current_device())
+
+    def plan(self, eng, stream=None):
+        i = self.inp0
+        eng.plan(i.qo_indptr, i.kv_page_indptr, i.kv_last_page_len, i.sm_scale, stream=stream)
+
+    def run_layer(self, eng, r, stream=None):
+        inp, o, lse = self.layers[r]
+        eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse,
+                stream=stream)
+
+
+def time_device_steps(L: Layered, eng, steps, warmup, use_graph=True):
+    """K timed steps; each = plan() + all layers (one graph replay). Returns per-step ms list."""
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        L.plan(eng, s)
+        for r in range(len(L.layers)):
+            L.run_layer(eng, r, s)
+    torch.cuda.synchronize()
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            for r in range(len(L.layers)):
+                L.run_layer(eng, r, s)
+    launches_per_step = eng.last_launches() * len(L.layers)
+
+    def one_step():
+        L.plan(eng, s)
+        if graph is not None:
+            graph.replay()
+        else:
+            for r in range(len(L.layers)):
+                L.run_layer(eng, r, s)
+
+    with torch.cuda.stream(s):
+        for _ in range(warmup):
+            one_step()
+    torch.cuda.synchronize()
+    return s, one_step, launches_per_step
+
+
+def per_launch_ms(L: Layered, eng, reps=3):
+    """CUDA events around each run() on its stream (attention + contraction kernels)."""
+    s = torch.cuda.Stream()
+    evs = []
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        L.plan(eng, s)
+        for _ in range(reps):
+            for r in range(len(L.layers)):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                L.run_layer(eng, r, s)
+                b.record(s)
+                evs.append((a, b))
+    torch.cuda.synchronize()
+    return float(np.mean([a.elapsed_time(b) for a, b in evs]))
+
+
+def e2e_steps(L: Layered, eng, steps, warmup):
+    """End to end through the public API with HOST buffers: per step, H2D of every layer's q and
+    the page table from pinned memory, plan(), run() per layer, D2H of o and lse. KV pools are
+    the resident cache (model state), not per-step input."""
+    s = torch.cuda.Stream()
+    host_q = [inp.q.cpu().pin_memory() for inp, _, _ in L.layers]
+    host_idx = L.inp0.kv_page_indices.cpu().pin_memory()
+    host_o = [o.cpu().pin_memory() for _, o, _ in L.layers]
+    host_l = [l.cpu().pin_memory() for _, _, l in L.layers]
+    h2d = sum(q.numel() * q.element_size() for q in host_q) + host_idx.numel() * 4
+    d2h = sum(o.numel() * o.element_size() for o in host_o) + sum(l.numel() * 4 for l in host_l)
+
+    def step():
+        with torch.cuda.stream(s):
+            L.inp0.kv_page_indices.copy_(host_idx, non_blocking=True)
+            L.plan(eng, s)
+            for r, (inp, o, lse) in enumerate(L.layers):
+                inp.q.copy_(host_q[r], non_blocking=True)
+                L.run_layer(eng, r, s)
+                host_o[r].copy_(o, non_blocking=True)
+                host_l[r].copy_(lse, non_blocking=True)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(steps):
+        step()
+    b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps, h2d, d2h
+
+
+def oracle_cpu_baseline(wl, inp_host, budget_s=12.0):
+    """The float64 C oracle, as it stands, on this host's cores: whole configs[1] layers
+    repeated until ~budget_s of CPU work. Returns (TB/s of KV, threads, sample text)."""
+    import oracle
+    threads = len(os.sched_getaffinity(0))
+    by = decode_bytes(wl)["total"]
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        oracle.paged_attention(**inp_host, num_threads=threads)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or n >= 200:
+            break
+    return by * n / el / 1e12, threads, f"{n} full configs[1] layer(s) (batch 128, one layer each) in {el:.1f} s"
+
+
+def host_inputs(inp):
+    from synth import raw_bits
+    wl = inp.wl
+    return dict(qo_indptr=inp.qo_indptr, kv_page_indptr=inp.kv_page_indptr, kv_last_page_len=inp.kv_last_page_len,
+                kv_page_indices=inp.kv_page_indices.cpu().numpy(), q=raw_bits(inp.q), k_pool=raw_bits(inp.k_pool),
+                v_pool=raw_bits(inp.v_pool), k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo,
+                H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
+                sm_scale=inp.sm_scale)
+
+
+# -------------------------------------------------------------------- main ---
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle (the CPU baseline program) on this host, same metric/config."""
+    if rank != 0:
+        return
+    wl = synth.c2_decode_llama8b()
+    inp = synth.make_inputs(wl, device="cpu")
+    hin = host_inputs(inp)
+    import oracle
+    threads = len(os.sched_getaffinity(0))
+    # each step = a bounded sample: the 16 longest... use a fixed request subset so K steps stay short
+    reqs = list(range(0, wl.batch, 4))  # 32 of 128 requests
+    sub = synth.Workload(wl.name, wl.H_qo, wl.H_kv, wl.D, wl.page_size, wl.dtype, wl.mask, wl.qo_lens[reqs],
+                         wl.kv_lens[reqs])
+    by = decode_bytes(sub)["total"]
+    for _ in range(args.warmup):
+        oracle.paged_attention(**hin, req_list=reqs, num_threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.paged_attention(**hin, req_list=reqs, num_threads=threads)
+    el = (time.perf_counter() - t0) / args.steps
+    val = by / el / 1e12
+    sample = f"requests 0,4,...,124 (32 of 128) of configs[1], one layer per step"
+    print(json.dumps({
+        "impl": "reference", "metric": "paged decode HBM TB/s (configs[1], Llama-3-8B shape, batch 128)",
+        "value": val, "unit": "TB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "c2_decode_llama8b (sampled)", "global_batch": 32},
+        "cpu_baseline": {"value": val, "unit": "TB/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "TB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="bsra", choices=["bsra", "reference"])
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--num-ctas", type=int, default=296)
+    ap.add_argument("--kernel", default="auto")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import paper_2501_01005_b200 as bsra
+    bsra.lib()  # fail loudly if the extension is missing
+    dev = torch.device(f"cuda:{torch.cuda.current_device()}")
+    pk, pk_kind = peaks()
+
+    # ---- configs[1]: batched paged decode, Llama-3-8B heads, batch 128 per rank
+    wl = synth.c2_decode_llama8b()
+    L = Layered(wl, args.layers, dev, seed_base=1000 * rank)
+    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel)
+    by = decode_bytes(wl)
+    s, one_step, launches_per_step = time_device_steps(L, eng, args.steps, args.warmup, not args.no_graph)
+    clk = ClockSampler(local)
+    clk.start()
+    barrier(world)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        a.record(s)
+        for _ in range(args.steps):
+            one_step()
+        b.record(s)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = clk.stop()
+    ms = max_over_ranks(a.elapsed_time(b) / args.steps, world)
+    step_bytes = by["total"] * args.layers
+    value = world * step_bytes / (ms * 1e-3) / 1e12
+
+    # ---- roofline of the dominant launch (run(): attention + contraction), CUDA events per launch
+    launch_ms = per_launch_ms(L, eng)
+    achieved = by["total"] / (launch_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_kind": pk_kind,
+            "kernel": f"bsra attention ({eng.selected_kernel()}) + contraction, per run() launch pair",
+            "algorithmic_bytes_per_launch": by["total"], "launch_ms": launch_ms}
+
+    # ---- e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e_ms, h2d, d2h = e2e_steps(L, eng, max(3, args.steps // 4), 2)
+        e2e_ms = max_over_ranks(e2e_ms, world)
+        e2e = {"value": world * step_bytes / (e2e_ms * 1e-3) / 1e12, "unit": "TB/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+
+    # ---- secondary: configs[2] ragged causal prefill TFLOP/s (one layer, per-launch events)
+    prefill = None
+    if not args.no_prefill:
+        del L
+        torch.cuda.empty_cache()
+        wl3 = synth.c3_prefill_llama70b()
+        L3 = Layered(wl3, 2, dev, seed_base=1000 * rank)
+        e3 = L3.engine(num_ctas=148, kernel=args.kernel)
+        p_ms = per_launch_ms(L3, e3, reps=3)
+        fl = causal_flops(wl3)
+        tf = fl / (p_ms * 1e-3) / 1e12
+        prefill = {"value": tf, "unit": "TFLOP/s", "workload": "c3_prefill_llama70b (configs[2])",
+                   "ms_per_layer": p_ms, "frac": tf / pk["bf16_tflops"], "peak": pk["bf16_tflops"],
+                   "kernel": e3.selected_kernel(), "flops_per_layer": fl}
+        del L3
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        inp_cpu = synth.make_inputs(wl, device="cpu")
+        v, th, sample = oracle_cpu_baseline(wl, host_inputs(inp_cpu))
+        cpu = {"value": v, "unit": "TB/s", "cores": th, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        out = {
+            "metric": "paged decode HBM TB/s (configs[1], Llama-3-8B shape, batch 128) & prefill TFLOP/s (configs[2])",
+            "value": value, "unit": "TB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": "c2_decode_llama8b (BASELINE configs[1])", "global_batch": wl.batch * world,
+                       "layers_per_step": args.layers, "kv_tokens_per_layer": int(wl.kv_lens.sum()),
+                       "num_ctas": eng.cfg.num_ctas, "parallelism": f"requests sharded x{world}",
+                       "l2": "inputs larger than L2 (621 MB KV per layer > 126 MB L2); no flush",
+                       "graph": not args.no_graph},
+            "frac_of_hbm_peak": value / world * 1e3 / pk["hbm_gbs"],
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "prefill": prefill,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,166 @@
+/*
+ * bsra.h — C ABI of libbsra.so: block-sparse-row (paged) attention for B200 (sm_100a).
+ *
+ * The hot path of FlashInfer (arXiv 2501.01005; /root/reference/PAPER.md, cited "P:<line>"):
+ * attention of ragged query batches over a KV cache stored as a block-sparse-row matrix
+ * (§3.1.1), scheduled by the load-balanced Algorithm 1 (§3.3.1), with
+ * split-KV partial states combined by the attention-state operator ⊕ (§2.2).
+ * The plan()/run() split follows the paper's inspector-executor interface (§3.4).
+ *
+ * Conventions (all functions):
+ *   - every call returns bsra_status (0 = OK); no C++ exception crosses the ABI; on error a
+ *     message is available from bsra_last_error() (thread-local, valid until the next call).
+ *   - "host" pointers are ordinary CPU memory; "device" pointers are CUDA device memory on the
+ *     engine's device. The caller owns every buffer it passes and every stream; nothing the
+ *     caller passed is freed by the library. Streams are cudaStream_t passed as void*.
+ *   - asynchronous CUDA failures surface as BSRA_ECUDA on a later call.
+ *   - determinism: the same plan inputs give bitwise-identical outputs run to run.
+ *   - one host thread per engine; engines are independent.
+ */
+#ifndef BSRA_H_
+#define BSRA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BSRA_OK = 0,
+  BSRA_EINVAL = 1,       /* malformed argument (NULL, bad indptr, unsupported combination) */
+  BSRA_EBOUNDS = 2,      /* workload exceeds the bounds declared at engine creation */
+  BSRA_EUNSUPPORTED = 3, /* valid but not implemented (e.g. head_dim not in {64,128}) */
+  BSRA_ECUDA = 4,        /* CUDA runtime/driver error */
+  BSRA_ENOMEM = 5,       /* host allocation failed or workspace too small */
+  BSRA_ENCCL = 6         /* NCCL error (bsra_dist.h) */
+} bsra_status;
+
+typedef enum { BSRA_F32 = 0, BSRA_F16 = 1, BSRA_BF16 = 2 } bsra_dtype;
+
+/* LogitsMask. CAUSAL is right-aligned: query row r of a request with lengths
+ * (l_qo, l_kv) sees token t iff t <= l_kv - l_qo + r (R4). CUSTOM: per request a
+ * row-major l_qo x l_kv bit matrix, LSB-first within bytes, starting at bit offset
+ * mask_bit_indptr[i] (R9). Masked pairs are skipped; a row that sees nothing gets
+ * o = 0, lse = -inf (R3, R10). */
+typedef enum { BSRA_MASK_NONE = 0, BSRA_MASK_CAUSAL = 1, BSRA_MASK_CUSTOM = 2 } bsra_mask;
+
+/* Kernel family selection; AUTO picks the tcgen05 kernels where they apply (bf16/f16,
+ * head_dim 128) and the CUDA-core kernel otherwise. SIMT forces the CUDA-core kernel
+ * (cross-kernel tests). */
+typedef enum { BSRA_KERNEL_AUTO = 0, BSRA_KERNEL_SIMT = 1, BSRA_KERNEL_TC = 2 } bsra_kernel;
+
+typedef struct {
+  int32_t num_qo_heads;      /* H_qo; H_qo % H_kv == 0; g = H_qo / H_kv                 */
+  int32_t num_kv_heads;      /* H_kv                                                            */
+  int32_t head_dim;          /* D in {64, 128}                                                  */
+  int32_t page_size;         /* B_c >= 1 ("B_c is specified by KV-Cache management")   */
+  bsra_dtype dtype;          /* dtype of q, k_pool, v_pool                                      */
+  bsra_dtype o_dtype;        /* = dtype, or BSRA_F32 (raw attention state for a later ⊕)      */
+  bsra_mask mask;            /* fixed per engine                                                */
+  int32_t max_batch;         /* scheduler-metadata bounds supplied up front (App. D.3) */
+  int32_t max_total_qo_rows; /* bound on sum_i l_qo(i)                                          */
+  int32_t num_ctas;          /* persistent grid size; 0 => 2 x #SM when T_q = 16, else #SM     */
+  int32_t tile_set_mask;     /* allowed query tiles T_q: bit0=16, bit1=64, bit2=128; 0 => all */
+  int32_t tile_q;            /* 0 => heuristic of §3.2.2; else forced T_q in {16,64,128} */
+  int64_t cost_alpha;        /* Algorithm 1 cost(l_q, l_kv) = alpha*l_q + beta*l_kv     */
+  int64_t cost_beta;         /*   0 => 1                                                        */
+  int32_t kv_chunk_align;    /* chunk boundaries aligned to this many tokens; 0 => page_size  */
+  int32_t kv_chunk_min;      /* floor for the chunk size L_kv; 0 => none                        */
+  int32_t kernel;            /* bsra_kernel                                                     */
+  int32_t reserved[7];       /* must be zero                                                    */
+} bsra_config;
+
+typedef struct bsra_engine bsra_engine;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int32_t bsra_version(void);
+
+/* Number of SMs of a device (148 on B200); used for the num_ctas default (App. D.3). */
+bsra_status bsra_num_sms(int32_t device, int32_t* out);
+
+/* Bytes of device workspace an engine with this config needs (App. D.3):
+ * a plan section sized from max_batch / max_total_qo_rows / num_ctas, and a partial-output
+ * section of 2 x num_ctas tiles x T_q_max x (D + 1) fp32 words (the paper's bound taken per
+ * KV-head tile, R19), plus arrival counters. Offsets are fixed for the engine's
+ * lifetime so a CUDA graph can capture run() (App. D.1). Host-only, no CUDA calls if
+ * cfg->num_ctas > 0. */
+bsra_status bsra_workspace_bytes(const bsra_config* cfg, int32_t device, size_t* device_bytes);
+
+/* Create an engine on `device` over a caller-allocated device workspace of ws_bytes
+ * (>= bsra_workspace_bytes, 256-byte aligned). The engine owns a pinned host staging buffer
+ * (App. D) and a host copy of the current plan. No device launches. */
+bsra_status bsra_engine_create(const bsra_config* cfg, int32_t device, void* d_workspace, size_t ws_bytes,
+                               bsra_engine** out);
+void bsra_engine_destroy(bsra_engine* e);
+
+/* Inspector: builds the load-balanced plan (Algorithm 1) from HOST arrays and
+ * enqueues its upload (pinned staging -> fixed workspace section) on `stream`. Not CUDA-graph
+ * capturable. One plan serves any number of run() calls with the same lengths.
+ *   qo_indptr        [batch+1] host int32; qo_indptr[0] = 0; nondecreasing (ragged q/o)
+ *   kv_page_indptr   [batch+1] host int32; kv_page_indptr[0] = 0; nondecreasing (BSR indptr)
+ *   kv_last_page_len [batch]   host int32; in [1, page_size] when request i has pages
+ *   sm_scale         logits scale (R1); <= 0 => 1/sqrt(head_dim)
+ * Errors: EINVAL (malformed arrays), EBOUNDS (batch / rows beyond the declared bounds). */
+bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, const int32_t* kv_page_indptr,
+                      const int32_t* kv_last_page_len, float sm_scale, void* stream);
+
+/* Executor: device pointers only; no allocation and no host synchronisation, so it is
+ * CUDA-graph capturable. Uses the most recent plan of `e` in stream order.
+ *   q                [sum l_qo, H_qo, D] device, contiguous, cfg->dtype
+ *   k_pool, v_pool   device pools; element (page p, slot s, kv head h, dim d) lives at
+ *                    p*strides[0] + s*strides[1] + h*strides[2] + d  (strides in ELEMENTS, host
+ *                    int64[3]; dim stride 1). Default NHD: [pages, page_size, H_kv, D].
+ *                    Base addresses and strides must be 16-byte aligned.
+ *   kv_page_indices  [nnz] device int32: BSR `indices` (page ids); not validated (caller contract)
+ *   custom_mask      MASK_CUSTOM: device uint8 bits (see bsra_mask); else NULL
+ *   mask_bit_indptr  MASK_CUSTOM: device int64 [batch+1] bit offsets; else NULL
+ *   o                [sum l_qo, H_qo, D] device, cfg->o_dtype
+ *   lse              [sum l_qo, H_qo] device fp32, natural log (R2); NULL => not written
+ * batch = 0 (or no rows) is a no-op that still launches the fixed kernels (graph stability). */
+bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const void* v_pool,
+                     const int64_t* k_strides, const int64_t* v_strides, const int32_t* kv_page_indices,
+                     const uint8_t* custom_mask, const int64_t* mask_bit_indptr, void* o, float* lse,
+                     void* stream);
+
+/* ⊕ of two attention-state tensors, max-shifted, fp32 arithmetic; the empty state
+ * (o = 0, lse = -inf) is the identity. rows x heads states of head_dim values each.
+ *   o_a, o_b [rows, heads, D] device in in_dtype; lse_a, lse_b [rows, heads] device fp32
+ *   o_out [rows, heads, D] device in out_dtype; lse_out fp32 or NULL. In place allowed. */
+bsra_status bsra_merge_states(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b,
+                              bsra_dtype in_dtype, int64_t rows, int32_t heads, int32_t head_dim, void* o_out,
+                              bsra_dtype out_dtype, float* lse_out, void* stream);
+
+/* Left fold of ⊕ over P parts in part order: o_parts fp32 [P, rows, heads, D] and
+ * lse_parts fp32 [P, rows, heads] (device) -> o_out (out_dtype), lse_out (fp32 or NULL). */
+bsra_status bsra_merge_many(const float* o_parts, const float* lse_parts, int32_t P, int64_t rows,
+                            int32_t heads, int32_t head_dim, void* o_out, bsra_dtype out_dtype, float* lse_out,
+                            void* stream);
+
+/* Host-only Algorithm 1: the plan image bsra_plan would build for this config and lengths with
+ * `num_ctas` CTAs (no engine, no CUDA). Used for the bit-exact scheduler tests. */
+bsra_status bsra_plan_host(const bsra_config* cfg, int32_t num_ctas, int32_t batch, const int32_t* qo_indptr,
+                           const int32_t* kv_page_indptr, const int32_t* kv_last_page_len, int32_t* image,
+                           size_t cap_words, size_t* n_words);
+
+/* Copy of the engine's current plan image: host copy (from_device = 0) or read back from the
+ * device workspace section after synchronising `stream` (from_device = 1). */
+bsra_status bsra_plan_export(const bsra_engine* e, int32_t from_device, int32_t* host_buf, size_t cap_words,
+                             size_t* n_words, void* stream);
+
+/* Per-CTA cost of the current plan under the Algorithm-1 cost model, and its makespan. */
+bsra_status bsra_plan_stats(const bsra_engine* e, int64_t* cta_cost, int32_t cap, int64_t* makespan);
+
+/* Kernels launched by the most recent bsra_run (for launch-count reporting). */
+int32_t bsra_last_run_launches(const bsra_engine* e);
+
+/* Name of the attention kernel family the current plan selected ("simt", "tc_decode", "tc_prefill"). */
+const char* bsra_selected_kernel(const bsra_engine* e);
+
+const char* bsra_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSRA_H_ */

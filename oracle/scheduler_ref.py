@@ -66,7 +66,7 @@ def plan_ref(qo_lens, kv_lens, *, g, H_kv, mask=MASK_NONE, num_ctas, tile_set=(1
     if num_ctas < 1:
         raise ValueError("num_ctas >= 1")
     if T_q is None:
-        T_q = select_tile(qo_lens, g, tile_set) if B > 0 else min(tile_set)
+        T_q = select_tile(qo_lens, g, tile_set)
     # --- rows (request, kv head, q tile) and their effective kv length
     rows = []  # (i, h, t, e)
     for i in range(B):

@@ -1,0 +1,226 @@
+"""bsra — block-sparse-row (paged) attention for B200: thin Python binding of libbsra.so.
+
+Argument marshalling only (ctypes over the C ABI in include/bsra.h): every step of the hot
+path runs in libbsra.so (host scheduler + sm_100a kernels). There is no CPU or PyTorch
+fallback: if libbsra.so is missing or a call fails, an exception is raised.
+
+PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbsra.so")
+
+F32, F16, BF16 = 0, 1, 2
+MASK = {"none": 0, "causal": 1, "custom": 2}
+DTYPE = {"f32": F32, "f16": F16, "bf16": BF16}
+TORCH_DTYPE = {F32: torch.float32, F16: torch.float16, BF16: torch.bfloat16}
+KERNEL = {"auto": 0, "simt": 1, "tc": 2}
+TILE_BIT = {16: 1, 64: 2, 128: 4}
+
+
+class BsraError(RuntimeError):
+    pass
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("num_qo_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32), ("head_dim", ctypes.c_int32),
+                ("page_size", ctypes.c_int32), ("dtype", ctypes.c_int32), ("o_dtype", ctypes.c_int32),
+                ("mask", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("max_total_qo_rows", ctypes.c_int32),
+                ("num_ctas", ctypes.c_int32), ("tile_set_mask", ctypes.c_int32), ("tile_q", ctypes.c_int32),
+                ("cost_alpha", ctypes.c_int64), ("cost_beta", ctypes.c_int64), ("kv_chunk_align", ctypes.c_int32),
+                ("kv_chunk_min", ctypes.c_int32), ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+
+
+_lib = None
+EXPORTS = ["bsra_version", "bsra_num_sms", "bsra_workspace_bytes", "bsra_engine_create", "bsra_engine_destroy",
+           "bsra_plan", "bsra_run", "bsra_merge_states", "bsra_merge_many", "bsra_plan_host", "bsra_plan_export",
+           "bsra_plan_stats", "bsra_last_run_launches", "bsra_selected_kernel", "bsra_last_error"]
+
+
+def lib():
+    """Load libbsra.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise BsraError(f"{LIB_PATH} not built: run `make` (or __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        CP = ctypes.POINTER(Config)
+        sig = {
+            "bsra_version": (I32, []),
+            "bsra_num_sms": (I32, [I32, P]),
+            "bsra_workspace_bytes": (I32, [CP, I32, ctypes.POINTER(SZ)]),
+            "bsra_engine_create": (I32, [CP, I32, P, SZ, ctypes.POINTER(P)]),
+            "bsra_engine_destroy": (None, [P]),
+            "bsra_plan": (I32, [P, I32, P, P, P, ctypes.c_float, P]),
+            "bsra_run": (I32, [P, P, P, P, P, P, P, P, P, P, P, P]),
+            "bsra_merge_states": (I32, [P, P, P, P, I32, I64, I32, I32, P, I32, P, P]),
+            "bsra_merge_many": (I32, [P, P, I32, I64, I32, I32, P, I32, P, P]),
+            "bsra_plan_host": (I32, [CP, I32, I32, P, P, P, P, SZ, ctypes.POINTER(SZ)]),
+            "bsra_plan_export": (I32, [P, I32, P, SZ, ctypes.POINTER(SZ), P]),
+            "bsra_plan_stats": (I32, [P, P, I32, P]),
+            "bsra_last_run_launches": (I32, [P]),
+            "bsra_selected_kernel": (ctypes.c_char_p, [P]),
+            "bsra_last_error": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise BsraError(f"bsra status {rc}: {lib().bsra_last_error().decode()}")
+
+
+def _p(a) -> Optional[int]:
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return a.data_ptr()
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return int(a)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="none", max_batch=1,
+                max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128), tile_q=0, alpha=1, beta=1,
+                kv_chunk_align=0, kv_chunk_min=0, kernel="auto") -> Config:
+    c = Config()
+    c.num_qo_heads, c.num_kv_heads, c.head_dim, c.page_size = H_qo, H_kv, D, page_size
+    c.dtype = DTYPE[dtype] if isinstance(dtype, str) else dtype
+    od = o_dtype if o_dtype is not None else dtype
+    c.o_dtype = DTYPE[od] if isinstance(od, str) else od
+    c.mask = MASK[mask] if isinstance(mask, str) else mask
+    c.max_batch, c.max_total_qo_rows, c.num_ctas = max_batch, max_total_qo_rows, num_ctas
+    c.tile_set_mask = sum(TILE_BIT[t] for t in tile_set)
+    c.tile_q, c.cost_alpha, c.cost_beta = tile_q, alpha, beta
+    c.kv_chunk_align, c.kv_chunk_min = kv_chunk_align, kv_chunk_min
+    c.kernel = KERNEL[kernel] if isinstance(kernel, str) else kernel
+    return c
+
+
+def num_sms(device: int = 0) -> int:
+    out = ctypes.c_int32()
+    _check(lib().bsra_num_sms(device, ctypes.byref(out)))
+    return out.value
+
+
+def plan_host(cfg: Config, num_ctas: int, qo_indptr, kv_page_indptr, kv_last_page_len) -> np.ndarray:
+    """Algorithm-1 plan image computed by the C++ scheduler (host only, no CUDA)."""
+    qi, ki, kl = _i32(qo_indptr), _i32(kv_page_indptr), _i32(kv_last_page_len)
+    n = ctypes.c_size_t()
+    L = lib()
+    _check(L.bsra_plan_host(ctypes.byref(cfg), num_ctas, len(qi) - 1, _p(qi), _p(ki), _p(kl), None, 0,
+                            ctypes.byref(n)))
+    out = np.zeros(n.value, np.int32)
+    _check(L.bsra_plan_host(ctypes.byref(cfg), num_ctas, len(qi) - 1, _p(qi), _p(ki), _p(kl), _p(out), n.value,
+                            ctypes.byref(n)))
+    return out
+
+
+class Engine:
+    """One attention wrapper: fixed variant/task info + a device workspace it sizes."""
+
+    def __init__(self, cfg: Config, device: int = 0):
+        self.cfg = cfg
+        self.device = device
+        L = lib()
+        nbytes = ctypes.c_size_t()
+        _check(L.bsra_workspace_bytes(ctypes.byref(cfg), device, ctypes.byref(nbytes)))
+        self.workspace = torch.empty(max(256, nbytes.value), dtype=torch.uint8, device=f"cuda:{device}")
+        h = ctypes.c_void_p()
+        _check(L.bsra_engine_create(ctypes.byref(cfg), device, self.workspace.data_ptr(), self.workspace.numel(),
+                                    ctypes.byref(h)))
+        self._h = h
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().bsra_engine_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _stream(stream):
+        if stream is None:
+            return torch.cuda.current_stream().cuda_stream
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+    def plan(self, qo_indptr, kv_page_indptr, kv_last_page_len, sm_scale: float = 0.0, stream=None):
+        qi, ki, kl = _i32(qo_indptr), _i32(kv_page_indptr), _i32(kv_last_page_len)
+        self._keep = [qi, ki, kl]
+        _check(lib().bsra_plan(self._h, len(qi) - 1, _p(qi), _p(ki), _p(kl), float(sm_scale), self._stream(stream)))
+
+    def run(self, q, k_pool, v_pool, k_strides, v_strides, kv_page_indices, o, lse=None, custom_mask=None,
+            mask_bit_indptr=None, stream=None):
+        ks = (ctypes.c_int64 * 3)(*[int(x) for x in k_strides])
+        vs = (ctypes.c_int64 * 3)(*[int(x) for x in v_strides])
+        _check(lib().bsra_run(self._h, _p(q), _p(k_pool), _p(v_pool), ctypes.cast(ks, ctypes.c_void_p),
+                              ctypes.cast(vs, ctypes.c_void_p), _p(kv_page_indices), _p(custom_mask),
+                              _p(mask_bit_indptr), _p(o), _p(lse), self._stream(stream)))
+
+    def export_plan(self, from_device=False, stream=None) -> np.ndarray:
+        L = lib()
+        n = ctypes.c_size_t()
+        _check(L.bsra_plan_export(self._h, 0, None, 0, ctypes.byref(n), None))
+        out = np.zeros(n.value, np.int32)
+        _check(L.bsra_plan_export(self._h, int(from_device), _p(out), n.value, ctypes.byref(n),
+                                  self._stream(stream) if from_device else None))
+        return out
+
+    def plan_stats(self):
+        nc = int(self.export_plan()[2]) if self.export_plan().size else 0
+        costs = np.zeros(max(nc, 1), np.int64)
+        mk = ctypes.c_int64()
+        _check(lib().bsra_plan_stats(self._h, _p(costs), nc, ctypes.byref(mk)))
+        return costs[:nc], mk.value
+
+    def last_launches(self) -> int:
+        return lib().bsra_last_run_launches(self._h)
+
+    def selected_kernel(self) -> str:
+        return lib().bsra_selected_kernel(self._h).decode()
+
+
+def merge_states(o_a, lse_a, o_b, lse_b, o_out=None, lse_out=None, stream=None):
+    """⊕ of two state tensors: o [rows, heads, D], lse [rows, heads] fp32."""
+    rows, heads, D = o_a.shape
+    out_dtype = o_out.dtype if o_out is not None else o_a.dtype
+    if o_out is None:
+        o_out = torch.empty_like(o_a)
+    if lse_out is None:
+        lse_out = torch.empty_like(lse_a)
+    inv = {v: k for k, v in TORCH_DTYPE.items()}
+    _check(lib().bsra_merge_states(_p(o_a), _p(lse_a), _p(o_b), _p(lse_b), inv[o_a.dtype], rows, heads, D,
+                                   _p(o_out), inv[out_dtype], _p(lse_out), Engine._stream(stream)))
+    return o_out, lse_out
+
+
+def merge_many(o_parts, lse_parts, o_out, lse_out=None, stream=None):
+    """Left fold of ⊕ over parts (fp32 [P, rows, heads, D] / [P, rows, heads])."""
+    P, rows, heads, D = o_parts.shape
+    inv = {v: k for k, v in TORCH_DTYPE.items()}
+    _check(lib().bsra_merge_many(_p(o_parts), _p(lse_parts), P, rows, heads, D, _p(o_out), inv[o_out.dtype],
+                                 _p(lse_out), Engine._stream(stream)))
+    return o_out, lse_out

@@ -1,0 +1,185 @@
+// common.cuh — kernel parameter block and device-side view of the plan image.
+//
+// The plan image (scheduler.cpp) lives in a fixed workspace section (App. D.1); kernels
+// read its header at run time, so one captured CUDA graph stays valid across re-plans.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+namespace bsra {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct AttnParams {
+  const int32_t* plan;  // device plan image
+  const void* q;
+  const void* k;
+  const void* v;
+  int64_t ks0, ks1, ks2;  // k_pool strides (elements): page, token, head
+  int64_t vs0, vs1, vs2;
+  const int32_t* page_indices;
+  const uint8_t* mask;
+  const int64_t* mask_indptr;
+  void* o;
+  float* lse;
+  float* part_o;    // [slots][T_slot][D] fp32
+  float* part_lse;  // [slots][T_slot]
+  int32_t* counters;  // per-merge-list arrival counters (fused contraction)
+  int32_t H_qo, H_kv, g, page_size, mask_mode, o_f32, T_slot, D;
+  float scale_log2;  // sm_scale * log2(e)
+};
+
+struct PlanView {
+  int32_t num_ctas, T_q, L, n_items, n_lists, n_slots, batch, g, H_kv, mask;
+  const int32_t* cta_indptr;
+  const int32_t* item_req;
+  const int32_t* item_kvh;
+  const int32_t* item_qtile;
+  const int32_t* item_kb;
+  const int32_t* item_ke;
+  const int32_t* item_slot;
+  const int32_t* list_indptr;
+  const int32_t* list_slot;
+  const int32_t* list_req;
+  const int32_t* list_kvh;
+  const int32_t* list_qtile;
+  const int32_t* req_qo_begin;
+  const int32_t* req_qo_len;
+  const int32_t* req_kv_len;
+  const int32_t* req_page_begin;
+};
+
+__device__ __forceinline__ PlanView load_plan(const int32_t* __restrict__ p) {
+  PlanView v;
+  v.num_ctas = p[2];
+  v.T_q = p[3];
+  v.L = p[4];
+  v.n_items = p[5];
+  v.n_lists = p[6];
+  v.n_slots = p[7];
+  v.batch = p[8];
+  v.g = p[9];
+  v.H_kv = p[10];
+  v.mask = p[11];
+  const int32_t* c = p + 16;
+  v.cta_indptr = c;
+  c += v.num_ctas + 1;
+  v.item_req = c;
+  c += v.n_items;
+  v.item_kvh = c;
+  c += v.n_items;
+  v.item_qtile = c;
+  c += v.n_items;
+  v.item_kb = c;
+  c += v.n_items;
+  v.item_ke = c;
+  c += v.n_items;
+  v.item_slot = c;
+  c += v.n_items;
+  v.list_indptr = c;
+  c += v.n_lists + 1;
+  v.list_slot = c;
+  c += v.n_slots;
+  v.list_req = c;
+  c += v.n_lists;
+  v.list_kvh = c;
+  c += v.n_lists;
+  v.list_qtile = c;
+  c += v.n_lists;
+  v.req_qo_begin = c;
+  c += v.batch;
+  v.req_qo_len = c;
+  c += v.batch;
+  v.req_kv_len = c;
+  c += v.batch;
+  v.req_page_begin = c;
+  return v;
+}
+
+// ---- element conversions (16-byte vectors)
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  __device__ __forceinline__ static void to_float(const uint4& u, float* f) {
+    f[0] = __uint_as_float(u.x);
+    f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z);
+    f[3] = __uint_as_float(u.w);
+  }
+};
+template <>
+struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static void to_float(const uint4& u, float* f) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+template <>
+struct Vec<__half> {
+  static constexpr int N = 8;
+  __device__ __forceinline__ static void to_float(const uint4& u, float* f) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      float2 x = __half22float2(h);
+      f[2 * i] = x.x;
+      f[2 * i + 1] = x.y;
+    }
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ T from_float(float x);
+template <>
+__device__ __forceinline__ float from_float<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_float<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <>
+__device__ __forceinline__ __half from_float<__half>(float x) { return __float2half_rn(x); }
+
+template <typename T>
+__device__ __forceinline__ float to_f(T x);
+template <>
+__device__ __forceinline__ float to_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <>
+__device__ __forceinline__ float to_f<__half>(__half x) { return __half2float(x); }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ float warp_max(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// custom-mask bit (R9): row-major l_qo x l_kv per request, LSB first
+__device__ __forceinline__ bool mask_bit(const uint8_t* __restrict__ m, int64_t j) {
+  return (__ldg(m + (j >> 3)) >> (j & 7)) & 1;
+}
+
+}  // namespace bsra

@@ -1,0 +1,493 @@
+// engine.cu — libbsra.so: the C ABI of include/bsra.h.
+//
+// Engine = the paper's attention wrapper (§3.4): created once with the variant /
+// task information (dtype, heads, head_dim, page size, mask) and a caller-owned workspace; plan()
+// is the inspector (host Algorithm 1 + H2D of the plan image through pinned staging, App. D
+// P:463); run() is the executor (persistent attention kernel + contraction, graph-capturable).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bsra.h"
+#include "attn_simt.cuh"
+#include "merge.cuh"
+#include "scheduler.hpp"
+#include "tc_kernels.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+bsra_status fail(bsra_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      return fail(BSRA_ECUDA, std::string(#expr " failed: ") + cudaGetErrorString(_e));       \
+  } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int dtype_size(bsra_dtype t) { return t == BSRA_F32 ? 4 : 2; }
+
+struct Layout {
+  int32_t num_ctas = 0, T_max = 0, T_min = 0;
+  size_t plan_words = 0;
+  size_t off_plan = 0, off_part_o = 0, off_part_lse = 0, off_counters = 0, total = 0;
+};
+
+int tile_mask_of(const bsra_config& c) { return c.tile_set_mask ? c.tile_set_mask : 7; }
+
+bsra_status validate_config(const bsra_config& c) {
+  if (c.num_qo_heads <= 0 || c.num_kv_heads <= 0 || c.num_qo_heads % c.num_kv_heads)
+    return fail(BSRA_EINVAL, "num_qo_heads must be a positive multiple of num_kv_heads");
+  if (c.head_dim != 64 && c.head_dim != 128) return fail(BSRA_EUNSUPPORTED, "head_dim must be 64 or 128");
+  if (c.page_size < 1) return fail(BSRA_EINVAL, "page_size < 1");
+  if (c.dtype < BSRA_F32 || c.dtype > BSRA_BF16) return fail(BSRA_EINVAL, "bad dtype");
+  if (c.o_dtype != c.dtype && c.o_dtype != BSRA_F32) return fail(BSRA_EINVAL, "o_dtype must equal dtype or be F32");
+  if (c.mask < BSRA_MASK_NONE || c.mask > BSRA_MASK_CUSTOM) return fail(BSRA_EINVAL, "bad mask");
+  if (c.max_batch < 0 || c.max_total_qo_rows < 0) return fail(BSRA_EINVAL, "negative bounds");
+  if (c.num_ctas < 0) return fail(BSRA_EINVAL, "num_ctas < 0");
+  const int tm = tile_mask_of(c);
+  if (tm & ~7) return fail(BSRA_EINVAL, "tile_set_mask has unknown bits");
+  if (c.tile_q && c.tile_q != 16 && c.tile_q != 64 && c.tile_q != 128) return fail(BSRA_EINVAL, "tile_q not in {16,64,128}");
+  if (c.cost_alpha < 0 || c.cost_beta < 0) return fail(BSRA_EINVAL, "negative cost parameters");
+  if (c.kv_chunk_align < 0 || c.kv_chunk_min < 0) return fail(BSRA_EINVAL, "negative chunk parameters");
+  if (c.kernel < BSRA_KERNEL_AUTO || c.kernel > BSRA_KERNEL_TC) return fail(BSRA_EINVAL, "bad kernel selector");
+  for (int i = 0; i < 7; ++i)
+    if (c.reserved[i]) return fail(BSRA_EINVAL, "reserved fields must be zero");
+  return BSRA_OK;
+}
+
+int32_t default_num_ctas(const bsra_config& c, int32_t sms) {
+  const bool decode = c.tile_q == 16 || (c.tile_q == 0 && tile_mask_of(c) == 1);
+  return decode ? 2 * sms : sms;
+}
+
+Layout make_layout(const bsra_config& c, int32_t num_ctas) {
+  Layout L;
+  L.num_ctas = num_ctas;
+  const int tm = c.tile_q ? (c.tile_q == 16 ? 1 : c.tile_q == 64 ? 2 : 4) : tile_mask_of(c);
+  L.T_min = (tm & 1) ? 16 : (tm & 2) ? 64 : 128;
+  L.T_max = (tm & 4) ? 128 : (tm & 2) ? 64 : 16;
+  const int32_t g = c.num_qo_heads / c.num_kv_heads;
+  L.plan_words = bsra::plan_capacity_words(num_ctas, c.num_kv_heads, g, c.max_batch, c.max_total_qo_rows, L.T_min);
+  size_t off = 0;
+  L.off_plan = off;
+  off = align_up(off + L.plan_words * 4, 256);
+  const size_t slots = 2 * (size_t)num_ctas;
+  L.off_part_o = off;
+  off = align_up(off + slots * L.T_max * c.head_dim * 4, 256);
+  L.off_part_lse = off;
+  off = align_up(off + slots * L.T_max * 4, 256);
+  L.off_counters = off;
+  off = align_up(off + (size_t)(num_ctas + 1) * 4, 256);
+  L.total = off;
+  return L;
+}
+
+bsra_status query_sms(int32_t device, int32_t* sms) {
+  CUDA_TRY(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, device));
+  return BSRA_OK;
+}
+
+}  // namespace
+
+struct bsra_engine {
+  bsra_config cfg;
+  int32_t device = 0;
+  Layout lay;
+  uint8_t* ws = nullptr;
+  int32_t* staging = nullptr;  // pinned host buffer (App. D)
+  cudaEvent_t staged = nullptr;  // guards staging reuse
+  bool have_event_pending = false;
+  std::vector<int32_t> image;  // host copy of the current plan
+  bsra::PlanSummary summary;
+  bool planned = false;
+  float sm_scale = 0.f;
+  int32_t last_launches = 0;
+  const char* selected = "none";
+};
+
+// Definitions below take C linkage from their declarations in bsra.h.
+
+int32_t bsra_version(void) { return 100; }
+
+const char* bsra_last_error(void) { return g_err.c_str(); }
+
+bsra_status bsra_num_sms(int32_t device, int32_t* out) {
+  if (!out) return fail(BSRA_EINVAL, "NULL out");
+  return query_sms(device, out);
+}
+
+bsra_status bsra_workspace_bytes(const bsra_config* cfg, int32_t device, size_t* device_bytes) {
+  if (!cfg || !device_bytes) return fail(BSRA_EINVAL, "NULL argument");
+  bsra_status s = validate_config(*cfg);
+  if (s) return s;
+  int32_t nc = cfg->num_ctas;
+  if (!nc) {
+    int32_t sms = 0;
+    s = query_sms(device, &sms);
+    if (s) return s;
+    nc = default_num_ctas(*cfg, sms);
+  }
+  *device_bytes = make_layout(*cfg, nc).total;
+  return BSRA_OK;
+}
+
+bsra_status bsra_engine_create(const bsra_config* cfg, int32_t device, void* d_workspace, size_t ws_bytes,
+                               bsra_engine** out) {
+  if (!cfg || !out) return fail(BSRA_EINVAL, "NULL argument");
+  *out = nullptr;
+  bsra_status s = validate_config(*cfg);
+  if (s) return s;
+  if (!d_workspace) return fail(BSRA_EINVAL, "NULL workspace");
+  if (reinterpret_cast<uintptr_t>(d_workspace) % 256) return fail(BSRA_EINVAL, "workspace must be 256-byte aligned");
+  int32_t nc = cfg->num_ctas;
+  if (!nc) {
+    int32_t sms = 0;
+    s = query_sms(device, &sms);
+    if (s) return s;
+    nc = default_num_ctas(*cfg, sms);
+  }
+  Layout lay = make_layout(*cfg, nc);
+  if (ws_bytes < lay.total)
+    return fail(BSRA_ENOMEM, "workspace too small: need " + std::to_string(lay.total) + " bytes");
+  auto* e = new (std::nothrow) bsra_engine();
+  if (!e) return fail(BSRA_ENOMEM, "host allocation failed");
+  e->cfg = *cfg;
+  e->cfg.num_ctas = nc;
+  e->device = device;
+  e->lay = lay;
+  e->ws = static_cast<uint8_t*>(d_workspace);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  cudaError_t ce = cudaMallocHost(&e->staging, lay.plan_words * 4);
+  if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->staged, cudaEventDisableTiming);
+  cudaSetDevice(prev);
+  if (ce != cudaSuccess) {
+    if (e->staging) cudaFreeHost(e->staging);
+    delete e;
+    return fail(BSRA_ECUDA, std::string("pinned staging: ") + cudaGetErrorString(ce));
+  }
+  *out = e;
+  return BSRA_OK;
+}
+
+void bsra_engine_destroy(bsra_engine* e) {
+  if (!e) return;
+  if (e->staged) {
+    cudaEventSynchronize(e->staged);
+    cudaEventDestroy(e->staged);
+  }
+  if (e->staging) cudaFreeHost(e->staging);
+  delete e;
+}
+
+static bsra::SchedParams sched_params(const bsra_config& c, int32_t num_ctas) {
+  bsra::SchedParams sp;
+  sp.H_qo = c.num_qo_heads;
+  sp.H_kv = c.num_kv_heads;
+  sp.page_size = c.page_size;
+  sp.mask = c.mask;
+  sp.num_ctas = num_ctas;
+  sp.tile_set_mask = tile_mask_of(c);
+  sp.tile_q = c.tile_q;
+  sp.alpha = c.cost_alpha ? c.cost_alpha : 1;
+  sp.beta = c.cost_beta ? c.cost_beta : 1;
+  sp.align = c.kv_chunk_align ? c.kv_chunk_align : c.page_size;
+  sp.L_min = c.kv_chunk_min;
+  return sp;
+}
+
+bsra_status bsra_plan_host(const bsra_config* cfg, int32_t num_ctas, int32_t batch, const int32_t* qo_indptr,
+                           const int32_t* kv_page_indptr, const int32_t* kv_last_page_len, int32_t* image,
+                           size_t cap_words, size_t* n_words) {
+  if (!cfg || !n_words) return fail(BSRA_EINVAL, "NULL argument");
+  bsra_status s = validate_config(*cfg);
+  if (s) return s;
+  if (num_ctas < 1) return fail(BSRA_EINVAL, "num_ctas < 1");
+  std::vector<int32_t> qo, kv, im;
+  std::string err = bsra::lengths_from_bsr(batch, qo_indptr, kv_page_indptr, kv_last_page_len, cfg->page_size, qo, kv);
+  if (!err.empty()) return fail(BSRA_EINVAL, err);
+  bsra::PlanSummary sum;
+  err = bsra::build_plan(sched_params(*cfg, num_ctas), qo, kv, qo_indptr, kv_page_indptr, im, sum);
+  if (!err.empty()) return fail(BSRA_EINVAL, err);
+  *n_words = im.size();
+  if (image) {
+    if (cap_words < im.size()) return fail(BSRA_ENOMEM, "image buffer too small");
+    std::memcpy(image, im.data(), im.size() * 4);
+  }
+  return BSRA_OK;
+}
+
+bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, const int32_t* kv_page_indptr,
+                      const int32_t* kv_last_page_len, float sm_scale, void* stream) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  const bsra_config& c = e->cfg;
+  if (batch > c.max_batch) return fail(BSRA_EBOUNDS, "batch exceeds max_batch");
+  std::vector<int32_t> qo, kv;
+  std::string err = bsra::lengths_from_bsr(batch, qo_indptr, kv_page_indptr, kv_last_page_len, c.page_size, qo, kv);
+  if (!err.empty()) return fail(BSRA_EINVAL, err);
+  int64_t rows = 0;
+  for (int32_t x : qo) rows += x;
+  if (rows > c.max_total_qo_rows) return fail(BSRA_EBOUNDS, "sum of qo lengths exceeds max_total_qo_rows");
+  std::vector<int32_t> im;
+  bsra::PlanSummary sum;
+  err = bsra::build_plan(sched_params(c, c.num_ctas), qo, kv, qo_indptr, kv_page_indptr, im, sum);
+  if (!err.empty()) return fail(BSRA_EINVAL, err);
+  if (im.size() > e->lay.plan_words) return fail(BSRA_EBOUNDS, "plan image exceeds the workspace plan section");
+  if (sum.T_q > e->lay.T_max) return fail(BSRA_EBOUNDS, "tile larger than the workspace partial slots");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // the previous upload must have left the pinned buffer before it is overwritten
+  if (e->have_event_pending) CUDA_TRY(cudaEventSynchronize(e->staged));
+  std::memcpy(e->staging, im.data(), im.size() * 4);
+  CUDA_TRY(cudaMemcpyAsync(e->ws + e->lay.off_plan, e->staging, im.size() * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(e->staged, st));
+  e->have_event_pending = true;
+  e->image.swap(im);
+  e->summary = sum;
+  e->planned = true;
+  e->sm_scale = sm_scale > 0.f ? sm_scale : 1.f / std::sqrt((float)c.head_dim);
+  return BSRA_OK;
+}
+
+namespace {
+
+template <typename T, int D>
+bsra_status launch_simt(const bsra::AttnParams& p, int grid, cudaStream_t st) {
+  using S = bsra::SimtSmem<T, D>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(bsra::attn_simt_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes));
+    attr = true;
+  }
+  bsra::attn_simt_kernel<T, D><<<grid, bsra::kSimtWarps * 32, S::kBytes, st>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  return BSRA_OK;
+}
+
+template <typename T>
+bsra_status launch_simt_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st) {
+  return D == 64 ? launch_simt<T, 64>(p, grid, st) : launch_simt<T, 128>(p, grid, st);
+}
+
+template <typename TO, int D>
+bsra_status launch_contraction_t(const bsra::AttnParams& p, int grid, cudaStream_t st) {
+  bsra::contraction_kernel<TO, D><<<grid, 256, 0, st>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  return BSRA_OK;
+}
+
+template <typename TO>
+bsra_status launch_contraction_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st) {
+  return D == 64 ? launch_contraction_t<TO, 64>(p, grid, st) : launch_contraction_t<TO, 128>(p, grid, st);
+}
+
+}  // namespace
+
+bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const void* v_pool, const int64_t* k_strides,
+                     const int64_t* v_strides, const int32_t* kv_page_indices, const uint8_t* custom_mask,
+                     const int64_t* mask_bit_indptr, void* o, float* lse, void* stream) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  if (!e->planned) return fail(BSRA_EINVAL, "run() before plan()");
+  const bsra_config& c = e->cfg;
+  e->last_launches = 0;
+  if (!k_strides || !v_strides) return fail(BSRA_EINVAL, "NULL strides");
+  const bool has_rows = e->summary.n_items > 0;
+  if (has_rows && (!q || !k_pool || !v_pool || !kv_page_indices || !o))
+    return fail(BSRA_EINVAL, "NULL tensor pointer");
+  if (c.mask == BSRA_MASK_CUSTOM && has_rows && (!custom_mask || !mask_bit_indptr))
+    return fail(BSRA_EINVAL, "MASK_CUSTOM needs custom_mask and mask_bit_indptr");
+  const int es = dtype_size(c.dtype);
+  for (int i = 0; i < 3; ++i)
+    if ((k_strides[i] * es) % 16 || (v_strides[i] * es) % 16 || k_strides[i] < 0 || v_strides[i] < 0)
+      return fail(BSRA_EINVAL, "pool strides must be non-negative and 16-byte multiples");
+  if (has_rows && ((reinterpret_cast<uintptr_t>(k_pool) | reinterpret_cast<uintptr_t>(v_pool) |
+                    reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(o)) % 16))
+    return fail(BSRA_EINVAL, "q, pools and o must be 16-byte aligned");
+
+  bsra::AttnParams p{};
+  p.plan = reinterpret_cast<const int32_t*>(e->ws + e->lay.off_plan);
+  p.q = q;
+  p.k = k_pool;
+  p.v = v_pool;
+  p.ks0 = k_strides[0];
+  p.ks1 = k_strides[1];
+  p.ks2 = k_strides[2];
+  p.vs0 = v_strides[0];
+  p.vs1 = v_strides[1];
+  p.vs2 = v_strides[2];
+  p.page_indices = kv_page_indices;
+  p.mask = custom_mask;
+  p.mask_indptr = mask_bit_indptr;
+  p.o = o;
+  p.lse = lse;
+  p.part_o = reinterpret_cast<float*>(e->ws + e->lay.off_part_o);
+  p.part_lse = reinterpret_cast<float*>(e->ws + e->lay.off_part_lse);
+  p.counters = reinterpret_cast<int32_t*>(e->ws + e->lay.off_counters);
+  p.H_qo = c.num_qo_heads;
+  p.H_kv = c.num_kv_heads;
+  p.g = c.num_qo_heads / c.num_kv_heads;
+  p.page_size = c.page_size;
+  p.mask_mode = c.mask;
+  p.o_f32 = c.o_dtype == BSRA_F32;
+  p.T_slot = e->lay.T_max;
+  p.D = c.head_dim;
+  p.scale_log2 = e->sm_scale * bsra::kLog2e;
+
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = c.num_ctas;
+  bsra_status s = BSRA_OK;
+  const int T_q = e->summary.T_q;
+  bool used_tc = false;
+  if (c.kernel != BSRA_KERNEL_SIMT && c.dtype != BSRA_F32 && c.head_dim == 128) {
+    int rc = bsra::tc_launch(p, c.dtype == BSRA_BF16, T_q, grid, st, &e->selected);
+    if (rc < 0) return fail(BSRA_ECUDA, std::string("tcgen05 kernel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+    used_tc = rc > 0;
+    if (!used_tc && c.kernel == BSRA_KERNEL_TC) return fail(BSRA_EUNSUPPORTED, "no tcgen05 kernel for this tile");
+  }
+  if (!used_tc) {
+    e->selected = "simt";
+    switch (c.dtype) {
+      case BSRA_F32: s = launch_simt_d<float>(p, c.head_dim, grid, st); break;
+      case BSRA_F16: s = launch_simt_d<__half>(p, c.head_dim, grid, st); break;
+      default: s = launch_simt_d<__nv_bfloat16>(p, c.head_dim, grid, st); break;
+    }
+    if (s) return s;
+  }
+  // contraction stage: fixed grid, exits immediately when nothing was split
+  const int cgrid = std::max(1, std::min(grid, 2 * 148));
+  if (c.o_dtype == BSRA_F32 || c.dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
+  else if (c.dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
+  else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
+  if (s) return s;
+  e->last_launches = 2;
+  return BSRA_OK;
+}
+
+int32_t bsra_last_run_launches(const bsra_engine* e) { return e ? e->last_launches : 0; }
+
+const char* bsra_selected_kernel(const bsra_engine* e) { return e ? e->selected : "none"; }
+
+namespace {
+template <typename TI, typename TO, int D>
+bsra_status merge_states_t(const void* oa, const float* la, const void* ob, const float* lb, int64_t n, void* out,
+                           float* lo, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 7) / 8, 148 * 16);
+  if (n == 0) return BSRA_OK;
+  bsra::merge_states_kernel<TI, TO, D><<<grid, 256, 0, st>>>(static_cast<const TI*>(oa), la, static_cast<const TI*>(ob),
+                                                              lb, n, static_cast<TO*>(out), lo);
+  CUDA_TRY(cudaGetLastError());
+  return BSRA_OK;
+}
+template <typename TI, typename TO>
+bsra_status merge_states_d(int D, const void* oa, const float* la, const void* ob, const float* lb, int64_t n,
+                           void* out, float* lo, cudaStream_t st) {
+  return D == 64 ? merge_states_t<TI, TO, 64>(oa, la, ob, lb, n, out, lo, st)
+                 : merge_states_t<TI, TO, 128>(oa, la, ob, lb, n, out, lo, st);
+}
+template <typename TI>
+bsra_status merge_states_o(bsra_dtype to, int D, const void* oa, const float* la, const void* ob, const float* lb,
+                           int64_t n, void* out, float* lo, cudaStream_t st) {
+  switch (to) {
+    case BSRA_F32: return merge_states_d<TI, float>(D, oa, la, ob, lb, n, out, lo, st);
+    case BSRA_F16: return merge_states_d<TI, __half>(D, oa, la, ob, lb, n, out, lo, st);
+    default: return merge_states_d<TI, __nv_bfloat16>(D, oa, la, ob, lb, n, out, lo, st);
+  }
+}
+template <typename TO, int D>
+bsra_status merge_many_t(const float* op, const float* lp, int P, int64_t n, void* out, float* lo, cudaStream_t st) {
+  if (n == 0) return BSRA_OK;
+  const int grid = (int)std::min<int64_t>((n + 7) / 8, 148 * 16);
+  bsra::merge_many_kernel<TO, D><<<grid, 256, 0, st>>>(op, lp, P, n, static_cast<TO*>(out), lo);
+  CUDA_TRY(cudaGetLastError());
+  return BSRA_OK;
+}
+}  // namespace
+
+bsra_status bsra_merge_states(const void* o_a, const float* lse_a, const void* o_b, const float* lse_b,
+                              bsra_dtype in_dtype, int64_t rows, int32_t heads, int32_t head_dim, void* o_out,
+                              bsra_dtype out_dtype, float* lse_out, void* stream) {
+  if (head_dim != 64 && head_dim != 128) return fail(BSRA_EUNSUPPORTED, "head_dim must be 64 or 128");
+  if (rows < 0 || heads < 0) return fail(BSRA_EINVAL, "negative size");
+  const int64_t n = rows * heads;
+  if (n && (!o_a || !lse_a || !o_b || !lse_b || !o_out)) return fail(BSRA_EINVAL, "NULL pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (in_dtype) {
+    case BSRA_F32: return merge_states_o<float>(out_dtype, head_dim, o_a, lse_a, o_b, lse_b, n, o_out, lse_out, st);
+    case BSRA_F16: return merge_states_o<__half>(out_dtype, head_dim, o_a, lse_a, o_b, lse_b, n, o_out, lse_out, st);
+    case BSRA_BF16:
+      return merge_states_o<__nv_bfloat16>(out_dtype, head_dim, o_a, lse_a, o_b, lse_b, n, o_out, lse_out, st);
+  }
+  return fail(BSRA_EINVAL, "bad dtype");
+}
+
+bsra_status bsra_merge_many(const float* o_parts, const float* lse_parts, int32_t P, int64_t rows, int32_t heads,
+                            int32_t head_dim, void* o_out, bsra_dtype out_dtype, float* lse_out, void* stream) {
+  if (head_dim != 64 && head_dim != 128) return fail(BSRA_EUNSUPPORTED, "head_dim must be 64 or 128");
+  if (P < 1 || rows < 0 || heads < 0) return fail(BSRA_EINVAL, "bad sizes");
+  const int64_t n = rows * heads;
+  if (n && (!o_parts || !lse_parts || !o_out)) return fail(BSRA_EINVAL, "NULL pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool d64 = head_dim == 64;
+  switch (out_dtype) {
+    case BSRA_F32:
+      return d64 ? merge_many_t<float, 64>(o_parts, lse_parts, P, n, o_out, lse_out, st)
+                 : merge_many_t<float, 128>(o_parts, lse_parts, P, n, o_out, lse_out, st);
+    case BSRA_F16:
+      return d64 ? merge_many_t<__half, 64>(o_parts, lse_parts, P, n, o_out, lse_out, st)
+                 : merge_many_t<__half, 128>(o_parts, lse_parts, P, n, o_out, lse_out, st);
+    case BSRA_BF16:
+      return d64 ? merge_many_t<__nv_bfloat16, 64>(o_parts, lse_parts, P, n, o_out, lse_out, st)
+                 : merge_many_t<__nv_bfloat16, 128>(o_parts, lse_parts, P, n, o_out, lse_out, st);
+  }
+  return fail(BSRA_EINVAL, "bad dtype");
+}
+
+bsra_status bsra_plan_export(const bsra_engine* e, int32_t from_device, int32_t* host_buf, size_t cap_words,
+                             size_t* n_words, void* stream) {
+  if (!e || !n_words) return fail(BSRA_EINVAL, "NULL argument");
+  *n_words = e->image.size();
+  if (!host_buf) return BSRA_OK;
+  if (cap_words < e->image.size()) return fail(BSRA_ENOMEM, "buffer too small");
+  if (!from_device) {
+    std::memcpy(host_buf, e->image.data(), e->image.size() * 4);
+    return BSRA_OK;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(cudaMemcpyAsync(host_buf, e->ws + e->lay.off_plan, e->image.size() * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return BSRA_OK;
+}
+
+bsra_status bsra_plan_stats(const bsra_engine* e, int64_t* cta_cost, int32_t cap, int64_t* makespan) {
+  if (!e || !e->planned) return fail(BSRA_EINVAL, "no plan");
+  const int32_t* im = e->image.data();
+  const int nc = im[2], T_q = im[3], n_items = im[5];
+  const int64_t alpha = e->cfg.cost_alpha ? e->cfg.cost_alpha : 1, beta = e->cfg.cost_beta ? e->cfg.cost_beta : 1;
+  const int32_t* ind = im + bsra::kHeaderWords;
+  const int32_t* kb = ind + nc + 1 + 3 * n_items;
+  const int32_t* ke = kb + n_items;
+  int64_t mx = 0;
+  for (int c = 0; c < nc; ++c) {
+    int64_t s = 0;
+    for (int it = ind[c]; it < ind[c + 1]; ++it) s += alpha * T_q + beta * (int64_t)(ke[it] - kb[it]);
+    if (cta_cost && c < cap) cta_cost[c] = s;
+    mx = std::max(mx, s);
+  }
+  if (makespan) *makespan = mx;
+  return BSRA_OK;
+}
+
