@@ -70,8 +70,11 @@ bsra_status validate_config(const bsra_config& c) {
 }
 
 int32_t default_num_ctas(const bsra_config& c, int32_t sms) {
+  // one persistent CTA per SM (App. D.3: k = 1 "persistent kernel"); the SIMT decode
+  // path fits two per SM, the tcgen05 kernels one.
   const bool decode = c.tile_q == 16 || (c.tile_q == 0 && tile_mask_of(c) == 1);
-  return decode ? 2 * sms : sms;
+  const bool simt = c.kernel == BSRA_KERNEL_SIMT || c.dtype == BSRA_F32;
+  return decode && simt ? 2 * sms : sms;
 }
 
 Layout make_layout(const bsra_config& c, int32_t num_ctas) {
@@ -115,6 +118,7 @@ struct bsra_engine {
   bsra::PlanSummary summary;
   bool planned = false;
   float sm_scale = 0.f;
+  int64_t total_qo = 0;
   int32_t last_launches = 0;
   const char* selected = "none";
 };
@@ -260,6 +264,7 @@ bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, c
   e->summary = sum;
   e->planned = true;
   e->sm_scale = sm_scale > 0.f ? sm_scale : 1.f / std::sqrt((float)c.head_dim);
+  e->total_qo = rows;
   return BSRA_OK;
 }
 
@@ -352,11 +357,21 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
   bsra_status s = BSRA_OK;
   const int T_q = e->summary.T_q;
   bool used_tc = false;
-  if (c.kernel != BSRA_KERNEL_SIMT && c.dtype != BSRA_F32 && c.head_dim == 128) {
-    int rc = bsra::tc_launch(p, c.dtype == BSRA_BF16, T_q, grid, st, &e->selected);
-    if (rc < 0) return fail(BSRA_ECUDA, std::string("tcgen05 kernel launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+  if (c.kernel != BSRA_KERNEL_SIMT && c.dtype != BSRA_F32) {
+    bsra::TcLaunch tl;
+    tl.f16 = c.dtype == BSRA_F16;
+    tl.T_q = T_q;
+    tl.grid = grid;
+    tl.total_qo = e->total_qo;
+    tl.align = c.kv_chunk_align ? c.kv_chunk_align : c.page_size;
+    tl.page_size = c.page_size;
+    const char* why = "";
+    int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
+    if (rc < 0)
+      return fail(BSRA_ECUDA, std::string("tcgen05 kernel launch failed: ") + why + " / " +
+                                  cudaGetErrorString(cudaGetLastError()));
     used_tc = rc > 0;
-    if (!used_tc && c.kernel == BSRA_KERNEL_TC) return fail(BSRA_EUNSUPPORTED, "no tcgen05 kernel for this tile");
+    if (!used_tc && c.kernel == BSRA_KERNEL_TC) return fail(BSRA_EUNSUPPORTED, std::string("no tcgen05 kernel: ") + why);
   }
   if (!used_tc) {
     e->selected = "simt";

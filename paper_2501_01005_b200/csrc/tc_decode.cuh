@@ -1,0 +1,371 @@
+// tc_decode.cuh — paged decode attention on tcgen05 tensor cores (T_q = 16 head-fused rows).
+//
+// Head-group fusion (App. A): the <= 16 fused rows of one (request, kv head, q tile)
+// share every K/V byte. With so few rows the contraction is turned around ("swap-AB") so that
+// the 128 KV tokens of a tile fill the MMA's M dimension:
+//     S^T[128 tok x 16] = K[128 x D] . Q^T[D x 16]           (tcgen05, fp32 accumulate in TMEM)
+//     O^T[D x 16]      += V^T[D x 128] . P^T[128 x 16]       (V^T is an MN-major view of V in smem)
+// so one KV load serves all fused rows and the tensor core does the arithmetic while the kernel
+// streams HBM (decode is HBM-bound, fig:varlen).
+//
+// Warp roles (one CTA per SM, persistent over the CTA's plan queue):
+//   warp 0      TMA producer: per page and 64-column half, one 2-D box {64 d, B_c tokens} of the
+//               4-D pool view (d, kv head, slot, page) — the BSR `indices` give the page coordinate
+//               (the sparse gather of §3.2.1, done by TMA). Runs ahead across items
+//               through a kStages-deep smem ring.
+//   warps 1..4  128 threads: thread = TMEM lane = token (softmax) = head-dim row d (output).
+//               One elected thread issues the MMAs; online softmax in the log2 domain.
+// Epilogue: unsplit rows write o / lse (writethrough, App. D.2), split rows fp32 partials.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace bsra {
+
+struct TcParams {
+  AttnParams p;
+  CUtensorMap tq;  // q  [N, H_qo, D]: dims (D, H_qo, N), box (64, q_hb, q_tb), SW128
+  CUtensorMap tk;  // K pool: dims (D, H_kv, page_size, pages), box (64, 1, box_tok, 1), SW128
+  CUtensorMap tv;  // V pool: same
+  int32_t box_tok;  // min(page_size, 128)
+  int32_t q_hb, q_tb;
+  int32_t f16;      // 1 = fp16 inputs, 0 = bf16
+};
+
+namespace dec {
+constexpr int kTile = 128;         // tokens per KV tile (= MMA M)
+constexpr int kN = 16;             // fused rows per tile (= MMA N)
+constexpr int kStages = 3;
+constexpr int kHalfBytes = kTile * 128;      // 128 tokens x 64 d x 2 B = 16 KB
+constexpr int kKVBytes = 2 * kHalfBytes;     // one of K or V: 32 KB
+constexpr int kStageBytes = 2 * kKVBytes;    // K + V: 64 KB
+constexpr int kQBytes = 2 * kN * 128;        // 2 halves x 16 rows x 128 B = 4 KB
+constexpr int kPBytes = 2 * kN * 128;        // P^T: 2 token-halves x 16 rows x 128 B
+constexpr int kOffQ = kStages * kStageBytes;
+constexpr int kOffP = kOffQ + 2 * kQBytes;
+constexpr int kOffBar = kOffP + kPBytes;
+constexpr int kOffRed = kOffBar + 256;
+constexpr int kSmemBytes = kOffRed + 2 * 4 * kN * 4 + 1024;  // + alignment slack
+constexpr int kThreads = 160;
+constexpr uint32_t kTmemCols = 32;  // S^T at col 0, O^T at col 16
+}  // namespace dec
+
+struct DecItem {
+  int req, kvh, row0, nrows, slot, lq;
+  int64_t kb, ke, lk, qo_begin, page_begin;
+  int ntiles;
+};
+
+__device__ __forceinline__ DecItem dec_item(const PlanView& pv, int it, int g) {
+  DecItem d;
+  d.req = pv.item_req[it];
+  d.kvh = pv.item_kvh[it];
+  const int qt = pv.item_qtile[it];
+  d.kb = pv.item_kb[it];
+  d.ke = pv.item_ke[it];
+  d.slot = pv.item_slot[it];
+  d.lq = pv.req_qo_len[d.req];
+  d.lk = pv.req_kv_len[d.req];
+  d.qo_begin = pv.req_qo_begin[d.req];
+  d.page_begin = pv.req_page_begin[d.req];
+  d.row0 = qt * pv.T_q;
+  d.nrows = min(pv.T_q, d.lq * g - d.row0);
+  d.ntiles = (int)((d.ke - d.kb + dec::kTile - 1) / dec::kTile);
+  return d;
+}
+
+__global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
+  using namespace dec;
+  const AttnParams& p = tp.p;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* full = bar;                 // [kStages]
+  uint64_t* empty = bar + kStages;      // [kStages]
+  uint64_t* full_q = bar + 2 * kStages;  // [2]
+  uint64_t* empty_q = full_q + 2;       // [2]
+  uint64_t* bar_s = empty_q + 2;
+  uint64_t* bar_o = bar_s + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_o + 1);
+  float* red = reinterpret_cast<float*>(smem + kOffRed);  // [4 warps][kN]
+  float* red2 = red + 4 * kN;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const PlanView pv = load_plan(p.plan);
+  const int g = p.g;
+  const int it0 = pv.cta_indptr[blockIdx.x], it1 = pv.cta_indptr[blockIdx.x + 1];
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&full_q[b], 1);
+      ptx::mbar_init(&empty_q[b], 1);
+    }
+    ptx::mbar_init(bar_s, 1);
+    ptx::mbar_init(bar_o, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tp.tq);
+      ptx::tma_prefetch_desc(&tp.tk);
+      ptx::tma_prefetch_desc(&tp.tv);
+    }
+    const int B = tp.box_tok;
+    int stage = 0;
+    uint32_t ephase = 1;  // fresh barriers: waiting on parity 1 passes
+    uint32_t qphase[2] = {1, 1};
+    int qb = 0;
+    for (int it = it0; it < it1; ++it) {
+      const DecItem d = dec_item(pv, it, g);
+      // ---- Q tile: 16 fused rows = q_tb tokens x q_hb heads, two 64-column halves
+      if (lane == 0) {
+        ptx::mbar_wait(&empty_q[qb], qphase[qb]);
+        ptx::mbar_arrive_expect_tx(&full_q[qb], kQBytes);
+        const int head0 = d.kvh * g + (g > kN ? d.row0 % g : 0);
+        const int tok0 = (int)d.qo_begin + d.row0 / g;
+        uint8_t* qdst = smem + kOffQ + qb * kQBytes;
+        ptx::tma_load_3d(qdst, &tp.tq, &full_q[qb], 0, head0, tok0);
+        ptx::tma_load_3d(qdst + kN * 128, &tp.tq, &full_q[qb], 64, head0, tok0);
+      }
+      qphase[qb] ^= 1;
+      qb ^= 1;
+      // ---- K/V tiles: lane j handles sub-block j (one page, or 128 tokens of a big page)
+      for (int ti = 0; ti < d.ntiles; ++ti) {
+        const int64_t t0 = d.kb + (int64_t)ti * kTile;
+        const int n = (int)imin64(kTile, d.ke - t0);
+        const int nsub = (n + B - 1) / B;
+        int page = 0, off = 0;
+        if (lane < nsub) {
+          const int64_t tok = t0 + (int64_t)lane * B;
+          page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
+          off = (int)(tok % p.page_size);
+        }
+        if (lane == 0) {
+          ptx::mbar_wait(&empty[stage], ephase);
+          ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * 512);
+        }
+        __syncwarp();
+        if (lane < nsub) {
+          uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
+          uint8_t* vd = kd + kKVBytes;
+          ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
+          ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
+          ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
+          ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
+        }
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          ephase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===================== softmax / MMA / epilogue warps =====================
+    const int ct = threadIdx.x - 32;         // 0..127
+    const int q4 = warp & 3;                 // TMEM lane quarter this warp may access
+    const int row = q4 * 32 + lane;          // TMEM lane: token (softmax) / head-dim d (output)
+    const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tmem + lane_addr + 0, tO = tmem + lane_addr + 16;
+    const uint32_t fmt = tp.f16 ? 0u : 1u;
+    const uint32_t idS = ptx::idesc_f16(fmt, 128, kN, 0, 0);  // A = K (K-major), B = Q (K-major)
+    const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
+    const uint32_t sbase = ptx::smem_u32(smem);
+    uint8_t* Pbuf = smem + kOffP;
+    int stage = 0;
+    uint32_t fphase = 0, sphase = 0, ophase = 0;
+    uint32_t qphase[2] = {0, 0};
+    int qb = 0;
+
+    for (int it = it0; it < it1; ++it) {
+      const DecItem d = dec_item(pv, it, g);
+      const uint32_t qaddr = sbase + kOffQ + qb * kQBytes;
+      ptx::mbar_wait(&full_q[qb], qphase[qb]);
+      qphase[qb] ^= 1;
+      // per-column running state (identical in every thread) and per-thread partial sums
+      float m[kN], lp[kN], oacc[kN];
+#pragma unroll
+      for (int c = 0; c < kN; ++c) {
+        m[c] = -INFINITY;
+        lp[c] = 0.f;
+        oacc[c] = 0.f;
+      }
+      // causal limit / mask base per column
+      int64_t lim[kN];
+#pragma unroll
+      for (int c = 0; c < kN; ++c) {
+        const int tok = (d.row0 + c) / g;
+        lim[c] = p.mask_mode == 1 ? d.lk - d.lq + tok : (p.mask_mode == 2 ? p.mask_indptr[d.req] + (int64_t)tok * d.lk : 0);
+      }
+
+      for (int ti = 0; ti < d.ntiles; ++ti) {
+        const int64_t t0 = d.kb + (int64_t)ti * kTile;
+        const int n = (int)imin64(kTile, d.ke - t0);
+        uint8_t* kS = smem + stage * kStageBytes;
+        uint8_t* vS = kS + kKVBytes;
+        ptx::mbar_wait(&full[stage], fphase);
+        if (n < kTile && row >= n) {  // rows past the chunk: zero V so 0 * garbage cannot poison O
+          uint4 z = make_uint4(0, 0, 0, 0);
+          uint4* v0 = reinterpret_cast<uint4*>(vS + row * 128);
+          uint4* v1 = reinterpret_cast<uint4*>(vS + kHalfBytes + row * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            v0[j] = z;
+            v1[j] = z;
+          }
+          ptx::fence_proxy_async();
+        }
+        // ---- S^T = K Q^T
+        if (ct == 0) {
+          ptx::tc_fence_after();
+          const uint32_t ka = sbase + stage * kStageBytes;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t a = ptx::smem_desc_sw128(ka + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024);
+            const uint64_t b = ptx::smem_desc_sw128(qaddr + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
+            ptx::mma_f16_ss(tmem + 0, a, b, idS, kk > 0);
+          }
+          ptx::mma_commit(bar_s);
+        }
+        ptx::mbar_wait(bar_s, sphase);
+        sphase ^= 1;
+        ptx::tc_fence_after();
+        float s[kN];
+        ptx::tmem_ld16(tS, s);
+        ptx::tmem_ld_wait();
+        // ---- mask + scale, column max over the 128 tokens
+        const int64_t t = t0 + row;
+        const bool tok_ok = row < n;
+#pragma unroll
+        for (int c = 0; c < kN; ++c) {
+          bool vis = tok_ok && c < d.nrows;
+          if (p.mask_mode == 1) vis = vis && t <= lim[c];
+          else if (p.mask_mode == 2) vis = vis && mask_bit(p.mask, lim[c] + t);
+          s[c] = vis ? s[c] * p.scale_log2 : -INFINITY;
+        }
+#pragma unroll
+        for (int c = 0; c < kN; ++c) {
+          if (c < d.nrows) {
+            const float x = warp_max(s[c]);
+            if (lane == 0) red[q4 * kN + c] = x;
+          }
+        }
+        ptx::tc_fence_before();
+        ptx::named_bar_sync(1, 128);
+        float alpha[kN];
+#pragma unroll
+        for (int c = 0; c < kN; ++c) {
+          float pr = 0.f;
+          alpha[c] = 1.f;
+          if (c < d.nrows) {
+            const float mt = fmaxf(fmaxf(red[c], red[kN + c]), fmaxf(red[2 * kN + c], red[3 * kN + c]));
+            const float mn = fmaxf(m[c], mt);
+            if (mn != -INFINITY) {
+              alpha[c] = exp2f(m[c] - mn);
+              pr = s[c] == -INFINITY ? 0.f : exp2f(s[c] - mn);
+              m[c] = mn;
+            }
+            lp[c] = lp[c] * alpha[c] + pr;
+          }
+          s[c] = pr;
+        }
+        // ---- P^T (K-major, SW128): row c, token `row`
+        {
+          const int a = row >> 6, tt = row & 63;
+          uint8_t* pa = Pbuf + a * (kN * 128);
+#pragma unroll
+          for (int c = 0; c < kN; ++c) {
+            const uint32_t off = (c >> 3) * 1024 + (c & 7) * 128 + ((((tt >> 3) ^ (c & 7)) << 4) | ((tt & 7) << 1));
+            if (tp.f16) {
+              *reinterpret_cast<__half*>(pa + off) = __float2half_rn(s[c]);
+            } else {
+              *reinterpret_cast<__nv_bfloat16*>(pa + off) = __float2bfloat16_rn(s[c]);
+            }
+          }
+        }
+        ptx::fence_proxy_async();
+        ptx::named_bar_sync(1, 128);
+        // ---- O^T_tile = V^T P^T
+        if (ct == 0) {
+          ptx::tc_fence_after();
+          const uint32_t va = sbase + stage * kStageBytes + kKVBytes;
+          const uint32_t pa = sbase + kOffP;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t a = ptx::smem_desc_sw128(va + kk * 2048, kHalfBytes, 1024);
+            const uint64_t b = ptx::smem_desc_sw128(pa + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
+            ptx::mma_f16_ss(tmem + 16, a, b, idO, kk > 0);
+          }
+          ptx::mma_commit(&empty[stage]);  // K/V stage free once these MMAs complete
+          ptx::mma_commit(bar_o);
+        }
+        ptx::mbar_wait(bar_o, ophase);
+        ophase ^= 1;
+        ptx::tc_fence_after();
+        float ot[kN];
+        ptx::tmem_ld16(tO, ot);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < kN; ++c) oacc[c] = oacc[c] * alpha[c] + ot[c];
+        ptx::tc_fence_before();
+        if (++stage == kStages) {
+          stage = 0;
+          fphase ^= 1;
+        }
+      }
+      // Q buffer no longer read by the tensor core (all MMAs of this item have completed)
+      if (ct == 0) ptx::mbar_arrive(&empty_q[qb]);
+      qb ^= 1;
+      // ---- epilogue: denominators (sum over the 128 token lanes), normalise, write
+#pragma unroll
+      for (int c = 0; c < kN; ++c) {
+        if (c < d.nrows) {
+          const float x = warp_sum(lp[c]);
+          if (lane == 0) red2[q4 * kN + c] = x;
+        }
+      }
+      ptx::named_bar_sync(1, 128);
+#pragma unroll
+      for (int c = 0; c < kN; ++c) {
+        if (c < d.nrows) {
+          const float l = (red2[c] + red2[kN + c]) + (red2[2 * kN + c] + red2[3 * kN + c]);
+          const bool empty_row = !(l > 0.f);
+          const float val = empty_row ? 0.f : oacc[c] / l;
+          const float lse = empty_row ? -INFINITY : (m[c] + __log2f(l)) * kLn2;
+          const int f = d.row0 + c;
+          const int tok = f / g, head = d.kvh * g + f % g;
+          if (d.slot < 0) {
+            const int64_t orow = (d.qo_begin + tok) * p.H_qo + head;
+            if (p.o_f32) reinterpret_cast<float*>(p.o)[orow * 128 + row] = val;
+            else if (tp.f16) reinterpret_cast<__half*>(p.o)[orow * 128 + row] = __float2half_rn(val);
+            else reinterpret_cast<__nv_bfloat16*>(p.o)[orow * 128 + row] = __float2bfloat16_rn(val);
+            if (p.lse && row == 0) p.lse[orow] = lse;
+          } else {
+            const int64_t prow = (int64_t)d.slot * p.T_slot + c;
+            p.part_o[prow * 128 + row] = val;
+            if (row == 0) p.part_lse[prow] = lse;
+          }
+        }
+      }
+      ptx::named_bar_sync(1, 128);  // red2 reuse
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+}
+
+}  // namespace bsra

@@ -1,5 +1,103 @@
+// tc_kernels.cu — host side of the tcgen05 kernels: TMA tensor maps over q and the paged K/V
+// pools (built per run(); a captured graph bakes them) and the launch.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "tc_decode.cuh"
 #include "tc_kernels.hpp"
+#include "tc_prefill.cuh"
 
 namespace bsra {
-int tc_launch(const AttnParams&, bool, int, int, cudaStream_t, const char**) { return 0; }
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// q [N, H_qo, 128] contiguous: dims (d, head, token), box (64, hb, tb), 128B swizzle
+bool make_q_map(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, int hb, int tb) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {128, (cuuint64_t)H_qo, (cuuint64_t)std::max<int64_t>(N, 1)};
+  cuuint64_t strides[2] = {128 * 2, (cuuint64_t)H_qo * 128 * 2};
+  cuuint32_t box[3] = {64, (cuuint32_t)hb, (cuuint32_t)tb};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// paged pool: element (page, slot, head, d) at page*s0 + slot*s1 + head*s2 + d (elements).
+// 4-D view ordered (d, head, slot, page) — coordinates in that order — box (64, 1, B, 1).
+bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int page_size, int64_t s0, int64_t s1,
+                   int64_t s2, int B) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {128, (cuuint64_t)H_kv, (cuuint64_t)page_size, (cuuint64_t)0x7fffffff};
+  cuuint64_t strides[3] = {(cuuint64_t)s2 * 2, (cuuint64_t)s1 * 2, (cuuint64_t)s0 * 2};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)B, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pool),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const char** name, const char** why) {
+  *why = "";
+  if (p.D != 128) { *why = "head_dim != 128"; return 0; }
+  const int g = p.g;
+  if (!is_pow2(g)) { *why = "group size not a power of two"; return 0; }
+  const int ps = L.page_size;
+  const int B = std::min(ps, 128);
+  if (!(ps >= 8 && (128 % ps == 0 || ps % 128 == 0))) { *why = "page size must divide 128 (>= 8) or be a multiple of 128"; return 0; }
+  if (L.align % B) { *why = "chunk alignment not a multiple of the page box"; return 0; }
+  if (L.T_q == 16) {
+    TcParams tp;
+    std::memset(&tp, 0, sizeof(tp));
+    tp.p = p;
+    tp.box_tok = B;
+    tp.q_hb = g <= 16 ? g : 16;
+    tp.q_tb = g <= 16 ? 16 / g : 1;
+    tp.f16 = L.f16;
+    if (!make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) ||
+        !make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, ps, p.ks0, p.ks1, p.ks2, B) ||
+        !make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, ps, p.vs0, p.vs1, p.vs2, B)) {
+      *why = "cuTensorMapEncodeTiled failed";
+      return -1;
+    }
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(tc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes) !=
+          cudaSuccess)
+        return -1;
+      attr = true;
+    }
+    tc_decode_kernel<<<L.grid, dec::kThreads, dec::kSmemBytes, st>>>(tp);
+    if (cudaGetLastError() != cudaSuccess) return -1;
+    *name = "tc_decode";
+    return 1;
+  }
+  if (L.T_q == 64 || L.T_q == 128) {
+    return tc_prefill_launch(p, L, st, name, why, B);
+  }
+  *why = "no tcgen05 kernel for this tile";
+  return 0;
+}
+
 }  // namespace bsra

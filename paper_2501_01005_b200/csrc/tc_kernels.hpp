@@ -5,7 +5,20 @@
 #include "common.cuh"
 
 namespace bsra {
-// Launches the tcgen05 kernel for this tile size if one applies (bf16/f16, D = 128).
-// Returns 1 if launched, 0 if no tcgen05 kernel handles this configuration, -1 on launch error.
-int tc_launch(const AttnParams& p, bool bf16, int T_q, int grid, cudaStream_t st, const char** name);
+
+struct TcLaunch {
+  bool f16 = false;        // fp16 inputs (else bf16)
+  int T_q = 0;             // plan tile
+  int grid = 0;            // persistent grid (= plan num_ctas)
+  int64_t total_qo = 0;    // sum of l_qo of the current plan (q tensor extent)
+  int align = 0;           // chunk alignment in tokens
+  int page_size = 0;
+  int64_t max_page_ok = 0; // unused
+};
+
+// Launches the tcgen05 kernel for this plan if one applies (bf16/f16, D = 128, supported page
+// size / group size). Returns 1 if launched, 0 if no tcgen05 kernel handles this configuration
+// (*why says which condition failed), -1 on a CUDA error.
+int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const char** name, const char** why);
+
 }  // namespace bsra
