@@ -119,6 +119,7 @@ struct bsra_engine {
   bool planned = false;
   float sm_scale = 0.f;
   int64_t total_qo = 0;
+  int32_t max_qo = 0;
   int32_t last_launches = 0;
   const char* selected = "none";
 };
@@ -265,6 +266,8 @@ bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, c
   e->planned = true;
   e->sm_scale = sm_scale > 0.f ? sm_scale : 1.f / std::sqrt((float)c.head_dim);
   e->total_qo = rows;
+  e->max_qo = 0;
+  for (int32_t x : qo) e->max_qo = std::max(e->max_qo, x);
   return BSRA_OK;
 }
 
@@ -365,6 +368,8 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
     tl.total_qo = e->total_qo;
     tl.align = c.kv_chunk_align ? c.kv_chunk_align : c.page_size;
     tl.page_size = c.page_size;
+    tl.max_qo = e->max_qo;
+    tl.mask = c.mask;
     const char* why = "";
     int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
     if (rc < 0)

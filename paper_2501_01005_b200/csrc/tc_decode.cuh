@@ -9,12 +9,17 @@
 // streams HBM (decode is HBM-bound, fig:varlen).
 //
 // Warp roles (one CTA per SM, persistent over the CTA's plan queue):
-//   warp 0      TMA producer: per page and 64-column half, one 2-D box {64 d, B_c tokens} of the
+//   warp 0      TMA producer: per page and 64-column half, one box {64 d, B_c tokens} of the
 //               4-D pool view (d, kv head, slot, page) — the BSR `indices` give the page coordinate
 //               (the sparse gather of §3.2.1, done by TMA). Runs ahead across items
 //               through a kStages-deep smem ring.
 //   warps 1..4  128 threads: thread = TMEM lane = token (softmax) = head-dim row d (output).
-//               One elected thread issues the MMAs; online softmax in the log2 domain.
+//               One elected thread issues the MMAs. Online softmax in the log2 domain with
+//               lazy rescaling: O^T accumulates in TMEM across tiles and is rescaled only when a
+//               row max grows by more than 2^8 (the final o = O/l and lse use the same max, so the
+//               result is exact). S^T and P^T are double-buffered and the next tile's S MMA is
+//               issued before this tile's softmax when its K has landed.
+// kC = live fused columns (4, 8 or 16) — only those run through the softmax; kMask = mask mode.
 // Epilogue: unsplit rows write o / lse (writethrough, App. D.2), split rows fp32 partials.
 #pragma once
 #include <cuda.h>
@@ -44,12 +49,13 @@ constexpr int kStageBytes = 2 * kKVBytes;    // K + V: 64 KB
 constexpr int kQBytes = 2 * kN * 128;        // 2 halves x 16 rows x 128 B = 4 KB
 constexpr int kPBytes = 2 * kN * 128;        // P^T: 2 token-halves x 16 rows x 128 B
 constexpr int kOffQ = kStages * kStageBytes;
-constexpr int kOffP = kOffQ + 2 * kQBytes;
-constexpr int kOffBar = kOffP + kPBytes;
+constexpr int kOffP = kOffQ + 2 * kQBytes;   // two P^T buffers
+constexpr int kOffBar = kOffP + 2 * kPBytes;
 constexpr int kOffRed = kOffBar + 256;
 constexpr int kSmemBytes = kOffRed + 2 * 4 * kN * 4 + 1024;  // + alignment slack
 constexpr int kThreads = 160;
-constexpr uint32_t kTmemCols = 32;  // S^T at col 0, O^T at col 16
+constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T at col 32
+constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
 }  // namespace dec
 
 struct DecItem {
@@ -76,19 +82,20 @@ __device__ __forceinline__ DecItem dec_item(const PlanView& pv, int it, int g) {
   return d;
 }
 
+template <int kC, int kMask>
 __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
   using namespace dec;
   const AttnParams& p = tp.p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  uint64_t* full = bar;                 // [kStages]
-  uint64_t* empty = bar + kStages;      // [kStages]
+  uint64_t* full = bar;                  // [kStages]
+  uint64_t* empty = bar + kStages;       // [kStages]
   uint64_t* full_q = bar + 2 * kStages;  // [2]
-  uint64_t* empty_q = full_q + 2;       // [2]
-  uint64_t* bar_s = empty_q + 2;
-  uint64_t* bar_o = bar_s + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_o + 1);
+  uint64_t* empty_q = full_q + 2;        // [2]
+  uint64_t* bar_s = empty_q + 2;         // [2] S^T buffer ready
+  uint64_t* bar_pv = bar_s + 2;          // [2] PV MMA reading P^T buffer b done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_pv + 2);
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [4 warps][kN]
   float* red2 = red + 4 * kN;
 
@@ -105,10 +112,15 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&full_q[b], 1);
       ptx::mbar_init(&empty_q[b], 1);
+      ptx::mbar_init(&bar_s[b], 1);
+      ptx::mbar_init(&bar_pv[b], 1);
     }
-    ptx::mbar_init(bar_s, 1);
-    ptx::mbar_init(bar_o, 1);
     ptx::fence_barrier_init();
+  }
+  if (warp >= 1) {  // zero both P^T buffers once: rows >= kC stay zero for the kernel's lifetime
+    uint4* pz = reinterpret_cast<uint4*>(smem + kOffP);
+    for (int i = threadIdx.x - 32; i < 2 * kPBytes / 16; i += 128) pz[i] = make_uint4(0, 0, 0, 0);
+    ptx::fence_proxy_async();
   }
   if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
@@ -179,45 +191,77 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     const int q4 = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = q4 * 32 + lane;          // TMEM lane: token (softmax) / head-dim d (output)
     const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
-    const uint32_t tS = tmem + lane_addr + 0, tO = tmem + lane_addr + 16;
+    const uint32_t tO = tmem + lane_addr + 32;
     const uint32_t fmt = tp.f16 ? 0u : 1u;
     const uint32_t idS = ptx::idesc_f16(fmt, 128, kN, 0, 0);  // A = K (K-major), B = Q (K-major)
     const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
     const uint32_t sbase = ptx::smem_u32(smem);
-    uint8_t* Pbuf = smem + kOffP;
-    int stage = 0;
-    uint32_t fphase = 0, sphase = 0, ophase = 0;
+    // pipeline state (identical in every compute thread)
+    int stage = 0;            // ring stage of the tile being processed
+    uint32_t fphase = 0;      // its full-barrier parity
+    uint32_t sph[2] = {0, 0}, pvph[2] = {0, 0};
+    bool pv_pending[2] = {false, false};
+    int sbuf = 0;             // S^T buffer of the tile being processed
+    int pbuf = 0;             // P^T buffer to write next
     uint32_t qphase[2] = {0, 0};
     int qb = 0;
+
+    // elected thread: issue S^T(tile in `st`, buffer `b`) = K Q^T
+    auto issue_S = [&](int st, int b, uint32_t qaddr) {
+      ptx::tc_fence_after();
+      const uint32_t ka = sbase + st * kStageBytes;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t a = ptx::smem_desc_sw128(ka + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = ptx::smem_desc_sw128(qaddr + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
+        ptx::mma_f16_ss(tmem + b * 16, a, bd, idS, kk > 0);
+      }
+      ptx::mma_commit(&bar_s[b]);
+    };
+    auto wait_pv = [&](int b) {
+      if (pv_pending[b]) {
+        ptx::mbar_wait(&bar_pv[b], pvph[b]);
+        pvph[b] ^= 1;
+        pv_pending[b] = false;
+      }
+    };
 
     for (int it = it0; it < it1; ++it) {
       const DecItem d = dec_item(pv, it, g);
       const uint32_t qaddr = sbase + kOffQ + qb * kQBytes;
       ptx::mbar_wait(&full_q[qb], qphase[qb]);
       qphase[qb] ^= 1;
-      // per-column running state (identical in every thread) and per-thread partial sums
-      float m[kN], lp[kN], oacc[kN];
+      float m[kC], lp[kC];
+      int64_t lim[kC];
 #pragma unroll
-      for (int c = 0; c < kN; ++c) {
+      for (int c = 0; c < kC; ++c) {
         m[c] = -INFINITY;
         lp[c] = 0.f;
-        oacc[c] = 0.f;
-      }
-      // causal limit / mask base per column
-      int64_t lim[kN];
-#pragma unroll
-      for (int c = 0; c < kN; ++c) {
         const int tok = (d.row0 + c) / g;
-        lim[c] = p.mask_mode == 1 ? d.lk - d.lq + tok : (p.mask_mode == 2 ? p.mask_indptr[d.req] + (int64_t)tok * d.lk : 0);
+        lim[c] = kMask == 1 ? d.lk - d.lq + tok : (kMask == 2 ? p.mask_indptr[d.req] + (int64_t)tok * d.lk : 0);
       }
-
+      // prologue: S^T of tile 0
+      bool next_issued = false;
+      if (d.ntiles > 0 && ct == 0) {
+        ptx::mbar_wait(&full[stage], fphase);
+        issue_S(stage, sbuf, qaddr);
+      }
       for (int ti = 0; ti < d.ntiles; ++ti) {
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
         const int n = (int)imin64(kTile, d.ke - t0);
-        uint8_t* kS = smem + stage * kStageBytes;
-        uint8_t* vS = kS + kKVBytes;
-        ptx::mbar_wait(&full[stage], fphase);
+        const int nstage = stage + 1 == kStages ? 0 : stage + 1;
+        const uint32_t nfphase = nstage == 0 ? fphase ^ 1 : fphase;
+        // early issue of the next S^T when its K tile has already landed
+        next_issued = false;
+        if (ct == 0 && ti + 1 < d.ntiles && ptx::mbar_test_wait(&full[nstage], nfphase)) {
+          issue_S(nstage, sbuf ^ 1, qaddr);
+          next_issued = true;
+        }
+        ptx::mbar_wait(&bar_s[sbuf], sph[sbuf]);
+        sph[sbuf] ^= 1;
+        uint8_t* vS = smem + stage * kStageBytes + kKVBytes;
         if (n < kTile && row >= n) {  // rows past the chunk: zero V so 0 * garbage cannot poison O
+          ptx::mbar_wait(&full[stage], fphase);  // (already complete) orders the TMA writes before ours
           uint4 z = make_uint4(0, 0, 0, 0);
           uint4* v0 = reinterpret_cast<uint4*>(vS + row * 128);
           uint4* v1 = reinterpret_cast<uint4*>(vS + kHalfBytes + row * 128);
@@ -228,122 +272,129 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           }
           ptx::fence_proxy_async();
         }
-        // ---- S^T = K Q^T
-        if (ct == 0) {
-          ptx::tc_fence_after();
-          const uint32_t ka = sbase + stage * kStageBytes;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t a = ptx::smem_desc_sw128(ka + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024);
-            const uint64_t b = ptx::smem_desc_sw128(qaddr + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
-            ptx::mma_f16_ss(tmem + 0, a, b, idS, kk > 0);
-          }
-          ptx::mma_commit(bar_s);
-        }
-        ptx::mbar_wait(bar_s, sphase);
-        sphase ^= 1;
         ptx::tc_fence_after();
-        float s[kN];
-        ptx::tmem_ld16(tS, s);
+        float s[kC];
+        ptx::tmem_ld<kC>(tmem + lane_addr + sbuf * 16, s);
         ptx::tmem_ld_wait();
         // ---- mask + scale, column max over the 128 tokens
         const int64_t t = t0 + row;
         const bool tok_ok = row < n;
 #pragma unroll
-        for (int c = 0; c < kN; ++c) {
+        for (int c = 0; c < kC; ++c) {
           bool vis = tok_ok && c < d.nrows;
-          if (p.mask_mode == 1) vis = vis && t <= lim[c];
-          else if (p.mask_mode == 2) vis = vis && mask_bit(p.mask, lim[c] + t);
+          if (kMask == 1) vis = vis && t <= lim[c];
+          if (kMask == 2) vis = vis && mask_bit(p.mask, lim[c] + t);
           s[c] = vis ? s[c] * p.scale_log2 : -INFINITY;
         }
+        float mx[kC];
 #pragma unroll
-        for (int c = 0; c < kN; ++c) {
-          if (c < d.nrows) {
-            const float x = warp_max(s[c]);
-            if (lane == 0) red[q4 * kN + c] = x;
-          }
+        for (int c = 0; c < kC; ++c) mx[c] = s[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+          for (int c = 0; c < kC; ++c) mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
         }
+        if (lane == 0) {
+#pragma unroll
+          for (int c = 0; c < kC; ++c) red[q4 * kN + c] = mx[c];
+        }
+        wait_pv(pbuf);  // the PV MMA that read this P^T buffer two tiles ago is done
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, 128);
-        float alpha[kN];
+        // ---- lazy max update (exact: o and lse use the same stale max)
+        float alpha[kC];
+        bool rescale = false;
 #pragma unroll
-        for (int c = 0; c < kN; ++c) {
-          float pr = 0.f;
+        for (int c = 0; c < kC; ++c) {
+          const float mt = fmaxf(fmaxf(red[c], red[kN + c]), fmaxf(red[2 * kN + c], red[3 * kN + c]));
           alpha[c] = 1.f;
-          if (c < d.nrows) {
-            const float mt = fmaxf(fmaxf(red[c], red[kN + c]), fmaxf(red[2 * kN + c], red[3 * kN + c]));
-            const float mn = fmaxf(m[c], mt);
-            if (mn != -INFINITY) {
-              alpha[c] = exp2f(m[c] - mn);
-              pr = s[c] == -INFINITY ? 0.f : exp2f(s[c] - mn);
-              m[c] = mn;
+          if (mt > m[c] + kRescaleThresh) {
+            if (m[c] != -INFINITY) {
+              alpha[c] = exp2f(m[c] - mt);
+              rescale = true;
             }
-            lp[c] = lp[c] * alpha[c] + pr;
+            m[c] = mt;
           }
+          const float pr = s[c] == -INFINITY ? 0.f : exp2f(s[c] - m[c]);
+          lp[c] = lp[c] * alpha[c] + pr;
           s[c] = pr;
+        }
+        if (rescale) {  // rare: bring O^T to the new max (no PV MMA may be in flight)
+          wait_pv(pbuf ^ 1);
+          ptx::tc_fence_after();
+          float ov[kC];
+          ptx::tmem_ld<kC>(tO, ov);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int c = 0; c < kC; ++c) ov[c] *= alpha[c];
+          ptx::tmem_st<kC>(tO, ov);
+          ptx::tmem_st_wait();
         }
         // ---- P^T (K-major, SW128): row c, token `row`
         {
-          const int a = row >> 6, tt = row & 63;
-          uint8_t* pa = Pbuf + a * (kN * 128);
+          uint8_t* pa = smem + kOffP + pbuf * kPBytes + (row >> 6) * (kN * 128);
+          const int tt = row & 63;
 #pragma unroll
-          for (int c = 0; c < kN; ++c) {
+          for (int c = 0; c < kC; ++c) {
             const uint32_t off = (c >> 3) * 1024 + (c & 7) * 128 + ((((tt >> 3) ^ (c & 7)) << 4) | ((tt & 7) << 1));
-            if (tp.f16) {
-              *reinterpret_cast<__half*>(pa + off) = __float2half_rn(s[c]);
-            } else {
-              *reinterpret_cast<__nv_bfloat16*>(pa + off) = __float2bfloat16_rn(s[c]);
-            }
+            if (tp.f16) *reinterpret_cast<__half*>(pa + off) = __float2half_rn(s[c]);
+            else *reinterpret_cast<__nv_bfloat16*>(pa + off) = __float2bfloat16_rn(s[c]);
           }
         }
         ptx::fence_proxy_async();
+        ptx::tc_fence_before();
         ptx::named_bar_sync(1, 128);
-        // ---- O^T_tile = V^T P^T
+        // ---- O^T += V^T P^T ; then the next S^T if it was not issued early
         if (ct == 0) {
           ptx::tc_fence_after();
           const uint32_t va = sbase + stage * kStageBytes + kKVBytes;
-          const uint32_t pa = sbase + kOffP;
+          const uint32_t pa = sbase + kOffP + pbuf * kPBytes;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t a = ptx::smem_desc_sw128(va + kk * 2048, kHalfBytes, 1024);
             const uint64_t b = ptx::smem_desc_sw128(pa + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
-            ptx::mma_f16_ss(tmem + 16, a, b, idO, kk > 0);
+            ptx::mma_f16_ss(tmem + 32, a, b, idO, (ti > 0 || kk > 0) ? 1u : 0u);
           }
           ptx::mma_commit(&empty[stage]);  // K/V stage free once these MMAs complete
-          ptx::mma_commit(bar_o);
+          ptx::mma_commit(&bar_pv[pbuf]);
+          if (!next_issued && ti + 1 < d.ntiles) {
+            ptx::mbar_wait(&full[nstage], nfphase);
+            issue_S(nstage, sbuf ^ 1, qaddr);
+          }
         }
-        ptx::mbar_wait(bar_o, ophase);
-        ophase ^= 1;
-        ptx::tc_fence_after();
-        float ot[kN];
-        ptx::tmem_ld16(tO, ot);
-        ptx::tmem_ld_wait();
-#pragma unroll
-        for (int c = 0; c < kN; ++c) oacc[c] = oacc[c] * alpha[c] + ot[c];
-        ptx::tc_fence_before();
-        if (++stage == kStages) {
-          stage = 0;
-          fphase ^= 1;
-        }
+        pv_pending[pbuf] = true;
+        pbuf ^= 1;
+        sbuf ^= 1;
+        stage = nstage;
+        fphase = nfphase;
       }
-      // Q buffer no longer read by the tensor core (all MMAs of this item have completed)
+      // Q buffer no longer read once every MMA of this item completed (PV waits below cover them)
+      wait_pv(0);
+      wait_pv(1);
       if (ct == 0) ptx::mbar_arrive(&empty_q[qb]);
       qb ^= 1;
       // ---- epilogue: denominators (sum over the 128 token lanes), normalise, write
-#pragma unroll
-      for (int c = 0; c < kN; ++c) {
-        if (c < d.nrows) {
-          const float x = warp_sum(lp[c]);
-          if (lane == 0) red2[q4 * kN + c] = x;
-        }
+      float ov[kC];
+      if (d.ntiles > 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_ld<kC>(tO, ov);
+        ptx::tmem_ld_wait();
       }
+#pragma unroll
+      for (int c = 0; c < kC; ++c) {
+        float x = lp[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) red2[q4 * kN + c] = x;
+      }
+      ptx::tc_fence_before();
       ptx::named_bar_sync(1, 128);
 #pragma unroll
-      for (int c = 0; c < kN; ++c) {
+      for (int c = 0; c < kC; ++c) {
         if (c < d.nrows) {
           const float l = (red2[c] + red2[kN + c]) + (red2[2 * kN + c] + red2[3 * kN + c]);
           const bool empty_row = !(l > 0.f);
-          const float val = empty_row ? 0.f : oacc[c] / l;
+          const float val = empty_row ? 0.f : ov[c] / l;
           const float lse = empty_row ? -INFINITY : (m[c] + __log2f(l)) * kLn2;
           const int f = d.row0 + c;
           const int tok = f / g, head = d.kvh * g + f % g;
@@ -360,7 +411,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           }
         }
       }
-      ptx::named_bar_sync(1, 128);  // red2 reuse
+      ptx::named_bar_sync(1, 128);  // red2 reuse; TMEM reads done before the next item's MMAs
     }
   }
   ptx::tc_fence_before();

@@ -56,6 +56,36 @@ bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int pag
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int kC, int kMask>
+cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         dec::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  tc_decode_kernel<kC, kMask><<<grid, dec::kThreads, dec::kSmemBytes, st>>>(tp);
+  return cudaGetLastError();
+}
+
+template <int kC>
+cudaError_t launch_decode_m(int mask, const TcParams& tp, int grid, cudaStream_t st) {
+  switch (mask) {
+    case 0: return launch_decode_t<kC, 0>(tp, grid, st);
+    case 1: return launch_decode_t<kC, 1>(tp, grid, st);
+    default: return launch_decode_t<kC, 2>(tp, grid, st);
+  }
+}
+
+cudaError_t launch_decode(int kc, int mask, const TcParams& tp, int grid, cudaStream_t st) {
+  switch (kc) {
+    case 4: return launch_decode_m<4>(mask, tp, grid, st);
+    case 8: return launch_decode_m<8>(mask, tp, grid, st);
+    default: return launch_decode_m<16>(mask, tp, grid, st);
+  }
+}
+
 }  // namespace
 
 int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const char** name, const char** why) {
@@ -81,15 +111,9 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
       *why = "cuTensorMapEncodeTiled failed";
       return -1;
     }
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(tc_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes) !=
-          cudaSuccess)
-        return -1;
-      attr = true;
-    }
-    tc_decode_kernel<<<L.grid, dec::kThreads, dec::kSmemBytes, st>>>(tp);
-    if (cudaGetLastError() != cudaSuccess) return -1;
+    const int64_t fused = std::min<int64_t>(16, (int64_t)L.max_qo * g);
+    const int kc = fused <= 4 ? 4 : fused <= 8 ? 8 : 16;
+    if (launch_decode(kc, L.mask, tp, L.grid, st) != cudaSuccess) return -1;
     *name = "tc_decode";
     return 1;
   }

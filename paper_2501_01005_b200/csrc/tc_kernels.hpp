@@ -13,7 +13,8 @@ struct TcLaunch {
   int64_t total_qo = 0;    // sum of l_qo of the current plan (q tensor extent)
   int align = 0;           // chunk alignment in tokens
   int page_size = 0;
-  int64_t max_page_ok = 0; // unused
+  int max_qo = 0;          // max l_qo of the current plan (live fused columns)
+  int mask = 0;
 };
 
 // Launches the tcgen05 kernel for this plan if one applies (bf16/f16, D = 128, supported page
