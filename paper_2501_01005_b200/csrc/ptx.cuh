@@ -40,8 +40,12 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
+// Watchdog: a wait that never completes (a pipeline bug) traps after ~2^26 polls instead of
+// hanging the GPU; the launch then fails with an error.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t spins = 0;
   while (!mbar_try_wait(bar, phase)) {
+    if (++spins > (1u << 26)) __trap();
   }
 }
 
@@ -214,6 +218,16 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t fmt, uint32_t M, uint3
          ((M >> 4) << 24);
 }
 
+}  // namespace ptx
+
+// 2^x on the SFU (MUFU.EX2), flush-to-zero; 2^-inf = 0
+__device__ __forceinline__ float ptx_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
+  return y;
+}
+
+namespace ptx {
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }

@@ -88,6 +88,14 @@ cudaError_t launch_decode(int kc, int mask, const TcParams& tp, int grid, cudaSt
 
 }  // namespace
 
+bool make_q_map_ext(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, int hb, int tb) {
+  return make_q_map(m, q, f16, H_qo, N, hb, tb);
+}
+bool make_pool_map_ext(CUtensorMap* m, const void* pool, bool f16, int H_kv, int page_size, int64_t s0, int64_t s1,
+                       int64_t s2, int B) {
+  return make_pool_map(m, pool, f16, H_kv, page_size, s0, s1, s2, B);
+}
+
 int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const char** name, const char** why) {
   *why = "";
   if (p.D != 128) { *why = "head_dim != 128"; return 0; }

@@ -86,3 +86,91 @@ def test_tc_decode_deterministic(cuda_device):
     a = run_gpu(inp, eng)
     b = run_gpu(inp, eng)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ----------------------------------------------------------------- prefill (T_q = 64 / 128)
+def _prefill_case(cuda_device, *, H_qo=64, H_kv=8, ps=16, dtype="bf16", mask="causal", qo=None, kv=None, nc=148,
+                  tile_q=128, seed=0, layout="NHD", q_scale=1.0):
+    qo = np.array(qo if qo is not None else [70, 129, 1, 300], np.int32)
+    kv = np.array(kv if kv is not None else [70, 200, 50, 300], np.int32)
+    wl = synth.Workload("tcpre", H_qo, H_kv, 128, ps, dtype, mask, qo, kv)
+    inp = synth.make_inputs(wl, device=cuda_device, seed_base=seed, layout=layout, q_scale=q_scale)
+    gpu = run_gpu(inp, num_ctas=nc, tile_q=tile_q, kernel="tc")
+    assert gpu[2].selected_kernel() == "tc_prefill"
+    return assert_close(gpu, oracle.attention_from_inputs(inp), dtype, what=f"tc_prefill {wl} T_q={tile_q}")
+
+
+@pytest.mark.parametrize("mask", ["none", "causal", "custom"])
+@pytest.mark.parametrize("tile_q", [64, 128])
+def test_tc_prefill_masks_tiles(cuda_device, mask, tile_q):
+    _prefill_case(cuda_device, mask=mask, tile_q=tile_q)
+
+
+@pytest.mark.parametrize("nc", [1, 5, 148, 300])
+def test_tc_prefill_num_ctas(cuda_device, nc):
+    _prefill_case(cuda_device, nc=nc, qo=[500, 37, 1000], kv=[700, 37, 1000])
+
+
+@pytest.mark.parametrize("H", [(8, 8), (32, 8), (64, 8), (128, 8), (16, 1)])
+def test_tc_prefill_group_sizes(cuda_device, H):
+    _prefill_case(cuda_device, H_qo=H[0], H_kv=H[1], nc=64)
+
+
+@pytest.mark.parametrize("ps", [8, 32, 128, 256])
+def test_tc_prefill_page_sizes(cuda_device, ps):
+    _prefill_case(cuda_device, ps=ps, nc=40)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("layout", ["NHD", "HND"])
+def test_tc_prefill_dtypes_layouts(cuda_device, dtype, layout):
+    _prefill_case(cuda_device, dtype=dtype, layout=layout, nc=33)
+
+
+def test_tc_prefill_peaked_and_empty(cuda_device):
+    _prefill_case(cuda_device, q_scale=8.0, qo=[3, 0, 200, 9], kv=[1, 10, 200, 2], mask="causal", nc=17)
+
+
+def test_tc_prefill_decode_rows_agree_with_tc_decode(cuda_device):
+    """Cross-kernel invariant: l_qo = 1 rows through the prefill kernel (T_q forced to
+    128) and the decode kernel (T_q = 16) agree within tolerance."""
+    wl = synth.c2_decode_llama8b(batch=16)
+    inp = synth.make_inputs(wl, device=cuda_device)
+    a = run_gpu(inp, num_ctas=148, tile_q=16, kernel="tc")
+    b = run_gpu(inp, num_ctas=148, tile_q=128, kernel="tc")
+    assert a[2].selected_kernel() == "tc_decode" and b[2].selected_kernel() == "tc_prefill"
+    assert np.max(np.abs(a[0] - b[0])) < 1e-2 and np.max(np.abs(a[1] - b[1])) < 1e-3
+
+
+def test_tc_prefill_c3_full_bench_config(cuda_device):
+    """configs[2] at full size, bench launch configuration (148 CTAs); the shortest, a middle and
+    the longest request against the oracle."""
+    wl = synth.c3_prefill_llama70b()
+    inp = synth.make_inputs(wl, device=cuda_device)
+    gpu = run_gpu(inp, num_ctas=148, kernel="tc")
+    assert gpu[2].selected_kernel() == "tc_prefill"
+    order = np.argsort(wl.qo_lens)
+    reqs = sorted({int(order[0]), int(order[8]), int(order[-1])})
+    from tests.helpers import rows_of_requests
+    ref = oracle.attention_from_inputs(inp, req_list=reqs)
+    assert_close(gpu, ref, "bf16", rows=rows_of_requests(inp, reqs), what="c3 sampled")
+
+
+def test_tc_prefill_c3_custom_mask_sampled(cuda_device):
+    wl = synth.c3_prefill_llama70b(mask="custom")
+    inp = synth.make_inputs(wl, device=cuda_device)
+    gpu = run_gpu(inp, num_ctas=148, kernel="tc")
+    order = np.argsort(wl.qo_lens)
+    reqs = sorted({int(order[0]), int(order[5])})
+    from tests.helpers import rows_of_requests
+    ref = oracle.attention_from_inputs(inp, req_list=reqs)
+    assert_close(gpu, ref, "bf16", rows=rows_of_requests(inp, reqs), what="c3 custom sampled")
+
+
+def test_tc_prefill_deterministic(cuda_device):
+    wl = synth.c3_prefill_llama70b(batch=4)
+    inp = synth.make_inputs(wl, device=cuda_device)
+    eng = engine_for(wl, num_ctas=148, kernel="tc")
+    a = run_gpu(inp, eng)
+    b = run_gpu(inp, eng)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
