@@ -5,8 +5,8 @@ NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC,-O3 --expt-relaxed-
 PKG     := paper_2501_01005_b200
 SRC     := $(PKG)/csrc
 BUILD   := build
-OBJS    := $(BUILD)/engine.o $(BUILD)/scheduler.o $(BUILD)/tc_kernels.o
-HDRS    := $(wildcard $(SRC)/*.cuh $(SRC)/*.hpp) include/bsra.h
+OBJS    := $(BUILD)/engine.o $(BUILD)/scheduler.o $(BUILD)/tc_kernels.o $(BUILD)/dist.o
+HDRS    := $(wildcard $(SRC)/*.cuh $(SRC)/*.hpp) include/bsra.h include/bsra_dist.h
 
 all: $(PKG)/libbsra.so oracle/liborc.so
 
@@ -19,8 +19,11 @@ $(BUILD)/%.o: $(SRC)/%.cu $(HDRS) | $(BUILD)
 $(BUILD)/scheduler.o: $(SRC)/scheduler.cpp $(SRC)/scheduler.hpp | $(BUILD)
 	g++ -O2 -std=c++17 -fPIC -Wall -c $< -o $@
 
+$(BUILD)/dist.o: $(SRC)/dist.cpp include/bsra.h include/bsra_dist.h | $(BUILD)
+	g++ -O2 -std=c++17 -fPIC -Wall -I/usr/local/cuda/include -c $< -o $@
+
 $(PKG)/libbsra.so: $(OBJS)
-	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS) -ldl
 
 oracle/liborc.so: oracle/bsra_oracle.c
 	gcc -O2 -fopenmp -fPIC -shared -std=c11 -o $@ $< -lm

@@ -267,6 +267,124 @@ def host_inputs(inp):
                 sm_scale=inp.sm_scale)
 
 
+def time_graph(fn, s, reps, warmup=3):
+    """Capture fn() (a sequence of C-ABI launches on stream s) once; time `reps` replays."""
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fn()
+    with torch.cuda.stream(s):
+        for _ in range(warmup):
+            g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        a.record(s)
+        for _ in range(reps):
+            g.replay()
+        b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def bench_composable(dev, pk, layers=16, reps=20):
+    """configs[3]: 8K shared prefix + 64 branches x 256-token suffixes, one decode step per layer
+    through ComposableDecode (prefix engine on tensor-core tiles + suffix engine + ⊕), every layer
+    its own pool (16 x 101.7 MB >> L2). Also the single-format baseline the paper compares with
+    (64 requests x 528 pages through the decode kernel)."""
+    import paper_2501_01005_b200 as bsra
+    cis = [synth.c4_composable(device=dev, seed_base=100 * r) for r in range(layers)]
+    c0 = cis[0]
+    n = c0.q.shape[0]
+    comp = bsra.ComposableDecode(H_qo=c0.H_qo, H_kv=c0.H_kv, D=c0.D, page_size=c0.page_size, n_branch=n,
+                                 prefix_ctas=148, suffix_ctas=148)
+    comp.plan(c0.prefix, c0.suffix, c0.sm_scale)
+    pi = torch.from_numpy(c0.prefix["kv_page_indices"]).to(dev)
+    si = torch.from_numpy(c0.suffix["kv_page_indices"]).to(dev)
+    outs = [(torch.empty((n, c0.H_qo, c0.D), device=dev, dtype=c0.q.dtype), torch.empty((n, c0.H_qo), device=dev))
+            for _ in cis]
+    s = torch.cuda.Stream()
+
+    def step():
+        for ci, (o, l) in zip(cis, outs):
+            comp.run(ci.q, ci.k_pool, ci.v_pool, ci.strides, pi, si, o, l, stream=s)
+
+    ms = time_graph(step, s, reps) / layers
+    es = 2
+    unique = (8192 + n * 256) * c0.H_kv * c0.D * 2 * es + n * c0.H_qo * c0.D * es * 2 + n * c0.H_qo * 4
+    # single format: 64 requests over prefix + own suffix pages (re-reads the prefix per branch)
+    cfg = bsra.make_config(H_qo=c0.H_qo, H_kv=c0.H_kv, D=c0.D, page_size=c0.page_size, dtype="bf16", max_batch=n,
+                           max_total_qo_rows=n, num_ctas=148, tile_q=16)
+    eng = bsra.Engine(cfg, torch.cuda.current_device())
+    sg = c0.single
+    eng.plan(sg["qo_indptr"], sg["kv_page_indptr"], sg["kv_last_page_len"], c0.sm_scale)
+    sgi = torch.from_numpy(sg["kv_page_indices"]).to(dev)
+
+    def step_single():
+        for ci, (o, l) in zip(cis, outs):
+            eng.run(ci.q, ci.k_pool, ci.v_pool, ci.strides, ci.strides, sgi, o, l, stream=s)
+
+    ms_single = time_graph(step_single, s, max(3, reps // 4)) / layers
+    tbs = unique / (ms * 1e-3) / 1e12
+    return {"workload": "c4_composable (BASELINE configs[3]): 8K prefix + 64 x 256 suffix, 32/8 heads",
+            "us_per_layer": ms * 1e3, "unique_bytes_per_layer": unique, "value": tbs, "unit": "TB/s (unique bytes)",
+            "frac": tbs * 1e3 / pk["hbm_gbs"], "single_format_us_per_layer": ms_single * 1e3,
+            "speedup_vs_single_format": ms_single / ms, "launches_per_layer": comp.launches(),
+            "kernels": [comp.prefix.selected_kernel(), comp.suffix.selected_kernel(), "merge_states"]}
+
+
+def bench_long_context(dev, pk, world, rank, local, layers=2, reps=10):
+    """configs[4]: 4 requests x 512K tokens, Llama-3-8B heads. The sequence is split across the
+    `world` GPUs (rank r owns a contiguous 1/P of every request's pages); each rank runs the
+    paged attention of its shard (fp32 state) and the states are combined by the library's NCCL
+    all-gather + ⊕ (bsra_dist). Total work fixed -> strong scaling of one long-context step."""
+    import paper_2501_01005_b200 as bsra
+    full = synth.c5_long_decode()
+    shard_len = int(full.kv_lens[0]) // world  # pages split evenly (32768 pages / P)
+    wl = synth.Workload("c5_shard", full.H_qo, full.H_kv, full.D, full.page_size, full.dtype, "none",
+                        full.qo_lens.copy(), np.full(full.batch, shard_len, np.int32))
+    Ls = [synth.make_inputs(wl, device=dev, seed_base=1000 * rank + 100 * r) for r in range(layers)]
+    nq = wl.batch
+    cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
+                           o_dtype="f32", max_batch=wl.batch, max_total_qo_rows=nq, num_ctas=148, tile_q=16)
+    eng = bsra.Engine(cfg, local)
+    i0 = Ls[0]
+    eng.plan(i0.qo_indptr, i0.kv_page_indptr, i0.kv_last_page_len, i0.sm_scale)
+    if world > 1:
+        import torch.distributed as tdist
+        obj = [bsra.Dist.unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    else:
+        uid = bsra.Dist.unique_id()
+    d = bsra.Dist(world, rank, uid, local)
+    scratch = d.scratch(nq, wl.H_qo, wl.D, dev)
+    o_loc = torch.empty((nq, wl.H_qo, wl.D), device=dev)
+    l_loc = torch.empty((nq, wl.H_qo), device=dev)
+    o = torch.empty((nq, wl.H_qo, wl.D), device=dev, dtype=torch.bfloat16)
+    l = torch.empty((nq, wl.H_qo), device=dev)
+    s = torch.cuda.Stream()
+
+    def step():
+        for inp in Ls:
+            eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, i0.kv_page_indices, o_loc, l_loc,
+                    stream=s)
+            d.allgather_merge(o_loc, l_loc, scratch, o, l, stream=s)
+
+    barrier(world)
+    ms = max_over_ranks(time_graph(step, s, reps) / layers, world)
+    kv_total = int(full.kv_lens.astype(np.int64).sum()) * full.H_kv * full.D * 2 * 2
+    d.close()
+    tbs = kv_total / (ms * 1e-3) / 1e12
+    return {"workload": f"c5_long_decode (BASELINE configs[4]): 4 x 512K tokens, sequence split over {world} GPU(s)",
+            "us_per_layer": ms * 1e3, "kv_bytes_per_layer": kv_total, "value": tbs, "unit": "TB/s (aggregate)",
+            "frac_per_gpu": tbs * 1e3 / world / pk["hbm_gbs"], "scaling": "strong", "n_gpus": world,
+            "gather_bytes_per_rank": nq * wl.H_qo * (wl.D + 1) * 4, "kernel": eng.selected_kernel()}
+
+
 # -------------------------------------------------------------------- main ---
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -343,6 +461,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-composable", action="store_true")
+    ap.add_argument("--no-long", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
@@ -408,6 +528,27 @@ def main():
                    "ms_per_layer": p_ms, "frac": tf / pk["bf16_tflops"], "peak": pk["bf16_tflops"],
                    "kernel": e3.selected_kernel(), "flops_per_layer": fl}
         del L3
+        torch.cuda.empty_cache()
+
+    composable = None
+    if not args.no_composable:
+        try:
+            del L
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        composable = bench_composable(dev, pk)
+        torch.cuda.empty_cache()
+
+    long_ctx = None
+    if not args.no_long:
+        try:
+            del L
+        except NameError:
+            pass
+        torch.cuda.empty_cache()
+        long_ctx = bench_long_context(dev, pk, world, rank, local)
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -428,6 +569,7 @@ def main():
                        "graph": not args.no_graph},
             "frac_of_hbm_peak": value / world * 1e3 / pk["hbm_gbs"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "prefill": prefill,
+            "composable": composable, "long_context": long_ctx,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         }
         print(json.dumps(out))

@@ -42,7 +42,9 @@ class Config(ctypes.Structure):
 _lib = None
 EXPORTS = ["bsra_version", "bsra_num_sms", "bsra_workspace_bytes", "bsra_engine_create", "bsra_engine_destroy",
            "bsra_plan", "bsra_run", "bsra_merge_states", "bsra_merge_many", "bsra_plan_host", "bsra_plan_export",
-           "bsra_plan_stats", "bsra_last_run_launches", "bsra_selected_kernel", "bsra_last_error"]
+           "bsra_plan_stats", "bsra_last_run_launches", "bsra_selected_kernel", "bsra_last_error",
+           "bsra_dist_unique_id", "bsra_dist_create", "bsra_dist_destroy", "bsra_dist_scratch_bytes",
+           "bsra_dist_allgather_merge", "bsra_dist_last_error"]
 
 
 def lib():
@@ -224,3 +226,116 @@ def merge_many(o_parts, lse_parts, o_out, lse_out=None, stream=None):
     _check(lib().bsra_merge_many(_p(o_parts), _p(lse_parts), P, rows, heads, D, _p(o_out), inv[o_out.dtype],
                                  _p(lse_out), Engine._stream(stream)))
     return o_out, lse_out
+
+
+def sequence_shard(kv_page_indptr, kv_page_indices, kv_last_page_len, page_size, nranks, rank):
+    """Sequence split of a BSR page table for long-context decode (BASELINE configs[4]): rank r
+    owns the contiguous page range [r*n/P, (r+1)*n/P) of every request (n = its page count). The
+    last page length is the request's own only on the rank holding its final page. Host-only
+    index arithmetic; returns (kv_page_indptr, kv_page_indices, kv_last_page_len) of the shard."""
+    kp = np.asarray(kv_page_indptr, np.int64)
+    idx = np.asarray(kv_page_indices)
+    last = np.asarray(kv_last_page_len, np.int32)
+    indptr = [0]
+    sel = []
+    lasts = []
+    for i in range(len(kp) - 1):
+        n = int(kp[i + 1] - kp[i])
+        a, b = (rank * n) // nranks, ((rank + 1) * n) // nranks
+        sel.append(idx[kp[i] + a:kp[i] + b])
+        indptr.append(indptr[-1] + (b - a))
+        lasts.append(int(last[i]) if (b == n and b > a) else page_size)
+    ind = np.concatenate(sel).astype(np.int32) if sel else np.zeros(0, np.int32)
+    return np.array(indptr, np.int32), ind, np.array(lasts, np.int32)
+
+
+class Dist:
+    """NCCL communicator owned by libbsra (include/bsra_dist.h); the unique id travels through
+    the caller's process group (torch.distributed is plumbing only)."""
+
+    def __init__(self, nranks: int, rank: int, uid: bytes, device: int = 0):
+        L = lib()
+        L.bsra_dist_create.restype = ctypes.c_int32
+        L.bsra_dist_create.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p, ctypes.c_int32,
+                                       ctypes.POINTER(ctypes.c_void_p)]
+        h = ctypes.c_void_p()
+        rc = L.bsra_dist_create(nranks, rank, uid, device, ctypes.byref(h))
+        if rc:
+            raise BsraError(f"bsra_dist_create: {rc}: {Dist.last_error()}")
+        self._h, self.nranks, self.rank = h, nranks, rank
+
+    @staticmethod
+    def last_error() -> str:
+        f = lib().bsra_dist_last_error
+        f.restype = ctypes.c_char_p
+        return f().decode()
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        rc = lib().bsra_dist_unique_id(buf)
+        if rc:
+            raise BsraError(f"bsra_dist_unique_id: {rc}: {Dist.last_error()}")
+        return buf.raw
+
+    def scratch(self, rows, heads, D, device):
+        n = ctypes.c_size_t()
+        L = lib()
+        L.bsra_dist_scratch_bytes.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.POINTER(ctypes.c_size_t)]
+        _check(L.bsra_dist_scratch_bytes(self._h, rows, heads, D, ctypes.byref(n)))
+        return torch.empty(n.value, dtype=torch.uint8, device=device)
+
+    def allgather_merge(self, o_local, lse_local, scratch, o_out, lse_out=None, stream=None):
+        rows, heads, D = o_local.shape
+        inv = {v: k for k, v in TORCH_DTYPE.items()}
+        L = lib()
+        P = ctypes.c_void_p
+        L.bsra_dist_allgather_merge.argtypes = [P, P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P, P,
+                                                ctypes.c_int32, P, P]
+        rc = L.bsra_dist_allgather_merge(self._h, _p(o_local), _p(lse_local), rows, heads, D, _p(scratch), _p(o_out),
+                                         inv[o_out.dtype], _p(lse_out), Engine._stream(stream))
+        if rc:
+            raise BsraError(f"bsra_dist_allgather_merge: {rc}: {Dist.last_error()} {L.bsra_last_error().decode()}")
+        return o_out, lse_out
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().bsra_dist_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+
+class ComposableDecode:
+    """Composable formats: the KV of n branches that share a prefix is
+    described as two BSR matrices over one pool — a shared-prefix block read once for all n
+    query rows (large B_r: one "request" with l_qo = n, tensor-core tile) and per-branch suffix
+    blocks (B_r = 1) — one engine ("wrapper") each; the two attention states are combined with
+    ⊕ (bsra_merge_states). Three C-ABI launches per layer, all graph-capturable."""
+
+    def __init__(self, *, H_qo, H_kv, D, page_size, n_branch, dtype="bf16", device=0, prefix_ctas=0,
+                 suffix_ctas=0, kernel="auto"):
+        self.n, self.H_qo, self.D = n_branch, H_qo, D
+        self.prefix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
+                                         max_batch=1, max_total_qo_rows=n_branch, num_ctas=prefix_ctas,
+                                         tile_set=(64, 128), kernel=kernel), device)
+        self.suffix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
+                                         max_batch=n_branch, max_total_qo_rows=n_branch, num_ctas=suffix_ctas,
+                                         tile_q=16, kernel=kernel), device)
+        dev = f"cuda:{device}"
+        self.o_p = torch.empty((n_branch, H_qo, D), device=dev)
+        self.l_p = torch.empty((n_branch, H_qo), device=dev)
+        self.o_s = torch.empty((n_branch, H_qo, D), device=dev)
+        self.l_s = torch.empty((n_branch, H_qo), device=dev)
+
+    def plan(self, prefix: dict, suffix: dict, sm_scale=0.0, stream=None):
+        self.prefix.plan(prefix["qo_indptr"], prefix["kv_page_indptr"], prefix["kv_last_page_len"], sm_scale, stream)
+        self.suffix.plan(suffix["qo_indptr"], suffix["kv_page_indptr"], suffix["kv_last_page_len"], sm_scale, stream)
+
+    def run(self, q, k_pool, v_pool, strides, prefix_indices, suffix_indices, o, lse=None, stream=None):
+        self.prefix.run(q, k_pool, v_pool, strides, strides, prefix_indices, self.o_p, self.l_p, stream=stream)
+        self.suffix.run(q, k_pool, v_pool, strides, strides, suffix_indices, self.o_s, self.l_s, stream=stream)
+        merge_states(self.o_p, self.l_p, self.o_s, self.l_s, o_out=o, lse_out=lse, stream=stream)
+        return o, lse
+
+    def launches(self) -> int:
+        return self.prefix.last_launches() + self.suffix.last_launches() + 1

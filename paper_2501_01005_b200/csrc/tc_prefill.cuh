@@ -6,9 +6,10 @@
 //     S[128 rows x 128 tok] = Q[128 x D] . K^T          (tcgen05, fp32 in TMEM, double-buffered)
 //     O[128 x D]           += P[128 x 128] . V          (P bf16/fp16 in smem, O accumulates in TMEM)
 // Warp roles (one CTA per SM, persistent over the plan queue):
-//   warp 0     TMA producer: Q tile per item (double-buffered) and K/V pages through a 2-deep
-//              ring; per page one box {64 d, B_c tokens} per 64-column half of the 4-D pool view,
-//              the page coordinate taken from the BSR indices (§3.2.1).
+//   warps 0, 5 TMA producers: Q tile per item (double-buffered) + K pages, and V pages, through
+//              separate 2-deep rings (K is freed as soon as its S MMA completes); per page one box
+//              {64 d, B_c tokens} per 64-column half of the 4-D pool view, the page coordinate
+//              taken from the BSR indices (§3.2.1).
 //   warps 1-4  128 threads, thread = fused row = TMEM lane: the row max / sum are thread-local
 //              (no shuffles), online softmax in the log2 domain with lazy O rescaling
 //              (threshold 2^8; exact because o and lse use the same max). Causal / custom masks
@@ -23,18 +24,44 @@ namespace bsra {
 namespace pre {
 constexpr int kM = 128;                       // fused rows per tile (MMA M)
 constexpr int kTile = 128;                    // kv tokens per tile (MMA N of S, K of PV)
-constexpr int kStages = 2;
+constexpr int kStages = 2;                    // depth of the K ring and of the V ring
 constexpr int kHalf = 128 * 128;              // 128 rows x 64 cols x 2 B = 16 KB
 constexpr int kOp = 2 * kHalf;                // one 128 x 128 operand: 32 KB
 constexpr int kOffQ = 0;                      // 2 Q buffers
-constexpr int kOffKV = 2 * kOp;               // kStages x (K, V)
-constexpr int kOffP = kOffKV + kStages * 2 * kOp;
+constexpr int kOffK = 2 * kOp;                // K ring
+constexpr int kOffV = kOffK + kStages * kOp;  // V ring
+constexpr int kOffP = kOffV + kStages * kOp;  // P (A operand of PV)
 constexpr int kOffBar = kOffP + kOp;
 constexpr int kSmemBytes = kOffBar + 256 + 1024;
-constexpr int kThreads = 160;
+constexpr int kThreads = 192;                 // warp 0: Q+K producer, warps 1-4: softmax/MMA, warp 5: V producer
 constexpr uint32_t kTmemCols = 512;           // S buffers at 0 / 128, O at 256
 constexpr float kRescaleThresh = 8.f;
 }  // namespace pre
+
+// One producer warp's share of a KV tile: lane j loads sub-block j (one page, or 128 tokens of
+// a page >= 128) — both 64-column halves — with the page coordinate from the BSR indices.
+// (page, in-page offset) of this lane's sub-block; loaded before the producer waits for a free
+// stage so the index latency overlaps the wait.
+__device__ __forceinline__ void kv_tile_coords(const AttnParams& p, const DecItem& d, int64_t t0, int n, int B,
+                                               int lane, int& page, int& off) {
+  const int nsub = (n + B - 1) / B;
+  page = 0;
+  off = 0;
+  if (lane < nsub) {
+    const int64_t tok = t0 + (int64_t)lane * B;
+    page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
+    off = (int)(tok % p.page_size);
+  }
+}
+__device__ __forceinline__ void load_kv_tile(const CUtensorMap* tm, uint8_t* dst, uint64_t* bar, const DecItem& d,
+                                             int n, int B, int lane, int half_bytes, int page, int off) {
+  const int nsub = (n + B - 1) / B;
+  if (lane < nsub) {
+    uint8_t* kd = dst + lane * B * 128;
+    ptx::tma_load_4d(kd, tm, bar, 0, d.kvh, off, page);
+    ptx::tma_load_4d(kd + half_bytes, tm, bar, 64, d.kvh, off, page);
+  }
+}
 
 template <int kMask>
 __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __grid_constant__ TcParams tp) {
@@ -43,12 +70,14 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  uint64_t* full = bar;                  // [kStages]
-  uint64_t* empty = bar + kStages;       // [kStages]
-  uint64_t* full_q = bar + 2 * kStages;  // [2]
-  uint64_t* empty_q = full_q + 2;        // [2]
-  uint64_t* bar_s = empty_q + 2;         // [2]
-  uint64_t* bar_pv = bar_s + 2;          // [1]
+  uint64_t* full_k = bar;                  // [kStages]
+  uint64_t* empty_k = bar + kStages;       // [kStages]  freed by the S MMA
+  uint64_t* full_v = bar + 2 * kStages;    // [kStages]
+  uint64_t* empty_v = bar + 3 * kStages;   // [kStages]  freed by the PV MMA
+  uint64_t* full_q = bar + 4 * kStages;    // [2]
+  uint64_t* empty_q = full_q + 2;          // [2]
+  uint64_t* bar_s = empty_q + 2;           // [2]
+  uint64_t* bar_pv = bar_s + 2;            // [1]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_pv + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -58,8 +87,10 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&full_k[s], 1);
+      ptx::mbar_init(&empty_k[s], 1);
+      ptx::mbar_init(&full_v[s], 1);
+      ptx::mbar_init(&empty_v[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&full_q[b], 1);
@@ -75,55 +106,53 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ============================ TMA producer ============================
+  if (warp == 0 || warp == 5) {
+    // ===================== TMA producers (warp 0: Q + K, warp 5: V) =====================
+    const bool isK = warp == 0;
     if (lane == 0) {
-      ptx::tma_prefetch_desc(&tp.tq);
-      ptx::tma_prefetch_desc(&tp.tk);
-      ptx::tma_prefetch_desc(&tp.tv);
+      if (isK) {
+        ptx::tma_prefetch_desc(&tp.tq);
+        ptx::tma_prefetch_desc(&tp.tk);
+      } else {
+        ptx::tma_prefetch_desc(&tp.tv);
+      }
     }
     const int B = tp.box_tok;
     int stage = 0;
     uint32_t ephase = 1;
     uint32_t qphase[2] = {1, 1};
     int qb = 0;
+    uint64_t* fullx = isK ? full_k : full_v;
+    uint64_t* emptyx = isK ? empty_k : empty_v;
+    const CUtensorMap* tm = isK ? &tp.tk : &tp.tv;
+    const int ring = isK ? kOffK : kOffV;
     for (int it = it0; it < it1; ++it) {
       const DecItem d = dec_item(pv, it, g);
-      if (lane == 0) {
-        ptx::mbar_wait(&empty_q[qb], qphase[qb]);
-        ptx::mbar_arrive_expect_tx(&full_q[qb], kOp);
-        const int head0 = d.kvh * g + (g > kM ? d.row0 % g : 0);
-        const int tok0 = (int)d.qo_begin + d.row0 / g;
-        uint8_t* qdst = smem + kOffQ + qb * kOp;
-        ptx::tma_load_3d(qdst, &tp.tq, &full_q[qb], 0, head0, tok0);
-        ptx::tma_load_3d(qdst + kHalf, &tp.tq, &full_q[qb], 64, head0, tok0);
+      if (isK) {
+        if (lane == 0) {
+          ptx::mbar_wait(&empty_q[qb], qphase[qb]);
+          ptx::mbar_arrive_expect_tx(&full_q[qb], kOp);
+          const int head0 = d.kvh * g + (g > kM ? d.row0 % g : 0);
+          const int tok0 = (int)d.qo_begin + d.row0 / g;
+          uint8_t* qdst = smem + kOffQ + qb * kOp;
+          ptx::tma_load_3d(qdst, &tp.tq, &full_q[qb], 0, head0, tok0);
+          ptx::tma_load_3d(qdst + kHalf, &tp.tq, &full_q[qb], 64, head0, tok0);
+        }
+        qphase[qb] ^= 1;
+        qb ^= 1;
       }
-      qphase[qb] ^= 1;
-      qb ^= 1;
-      const int ntiles = (int)((d.ke - d.kb + kTile - 1) / kTile);
-      for (int ti = 0; ti < ntiles; ++ti) {
+      for (int ti = 0; ti < d.ntiles; ++ti) {
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
         const int n = (int)imin64(kTile, d.ke - t0);
         const int nsub = (n + B - 1) / B;
-        int page = 0, off = 0;
-        if (lane < nsub) {
-          const int64_t tok = t0 + (int64_t)lane * B;
-          page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
-          off = (int)(tok % p.page_size);
-        }
+        int page, off;
+        kv_tile_coords(p, d, t0, n, B, lane, page, off);
         if (lane == 0) {
-          ptx::mbar_wait(&empty[stage], ephase);
-          ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * 512);
+          ptx::mbar_wait(&emptyx[stage], ephase);
+          ptx::mbar_arrive_expect_tx(&fullx[stage], (uint32_t)nsub * B * 256);
         }
         __syncwarp();
-        if (lane < nsub) {
-          uint8_t* kd = smem + kOffKV + stage * 2 * kOp + lane * B * 128;
-          uint8_t* vd = kd + kOp;
-          ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
-          ptx::tma_load_4d(kd + kHalf, &tp.tk, &full[stage], 64, d.kvh, off, page);
-          ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
-          ptx::tma_load_4d(vd + kHalf, &tp.tv, &full[stage], 64, d.kvh, off, page);
-        }
+        load_kv_tile(tm, smem + ring + stage * kOp, &fullx[stage], d, n, B, lane, kHalf, page, off);
         __syncwarp();
         if (++stage == kStages) {
           stage = 0;
@@ -150,15 +179,17 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
     uint32_t qphase[2] = {0, 0};
     int qb = 0;
 
+    // elected thread: S(b) = Q K(st)^T; frees the K stage and signals the S buffer on completion
     auto issue_S = [&](int st, int b, uint32_t qaddr) {
       ptx::tc_fence_after();
-      const uint32_t ka = sbase + kOffKV + st * 2 * kOp;
+      const uint32_t ka = sbase + kOffK + st * kOp;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t a = ptx::smem_desc_sw128(qaddr + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
         const uint64_t bd = ptx::smem_desc_sw128(ka + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
         ptx::mma_f16_ss(tmem + b * 128, a, bd, idS, kk > 0);
       }
+      ptx::mma_commit(&empty_k[st]);
       ptx::mma_commit(&bar_s[b]);
     };
     auto wait_pv = [&]() {
@@ -183,7 +214,7 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
       qphase[qb] ^= 1;
       bool next_issued = false;
       if (d.ntiles > 0 && ct == 0) {
-        ptx::mbar_wait(&full[stage], fphase);
+        ptx::mbar_wait(&full_k[stage], fphase);
         issue_S(stage, sbuf, qaddr);
       }
       for (int ti = 0; ti < d.ntiles; ++ti) {
@@ -192,25 +223,12 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
         const int nstage = stage + 1 == kStages ? 0 : stage + 1;
         const uint32_t nfphase = nstage == 0 ? fphase ^ 1 : fphase;
         next_issued = false;
-        if (ct == 0 && ti + 1 < d.ntiles && ptx::mbar_test_wait(&full[nstage], nfphase)) {
+        if (ct == 0 && ti + 1 < d.ntiles && ptx::mbar_test_wait(&full_k[nstage], nfphase)) {
           issue_S(nstage, sbuf ^ 1, qaddr);
           next_issued = true;
         }
         ptx::mbar_wait(&bar_s[sbuf], sph[sbuf]);
         sph[sbuf] ^= 1;
-        uint8_t* vS = smem + kOffKV + stage * 2 * kOp + kOp;
-        if (n < kTile && r >= n) {  // V rows past the chunk -> 0 (0 * garbage would poison O)
-          ptx::mbar_wait(&full[stage], fphase);
-          uint4 z = make_uint4(0, 0, 0, 0);
-          uint4* v0 = reinterpret_cast<uint4*>(vS + r * 128);
-          uint4* v1 = reinterpret_cast<uint4*>(vS + kHalf + r * 128);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            v0[j] = z;
-            v1[j] = z;
-          }
-          ptx::fence_proxy_async();
-        }
         ptx::tc_fence_after();
         float s[kTile];
         const uint32_t tS = tmem + lane_addr + sbuf * 128;
@@ -249,31 +267,35 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
         }
         const float mneg = m == -INFINITY ? 0.f : -m;  // p = 2^(s*scale - m); masked s = -inf -> 0
         const float sc = p.scale_log2;
-        // ---- P = exp2(s - m) (bf16/fp16), row sum; P in smem (K-major SW128 A operand)
-        wait_pv();  // PV(i-1) has finished reading P (and O is quiescent)
         float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-        uint8_t* prow = smem + kOffP + (r >> 3) * 1024 + (r & 7) * 128;
+        uint32_t pw[kTile / 2];  // P packed as bf16x2 / f16x2 (halves the live registers)
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 tokens
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float p0 = ptx_ex2(fmaf(s[c * 8 + 2 * e], sc, mneg));
-            const float p1 = ptx_ex2(fmaf(s[c * 8 + 2 * e + 1], sc, mneg));
-            rs4[e] += p0 + p1;
-            if (tp.f16) {
-              __half2 h = __floats2half2_rn(p0, p1);
-              w[e] = *reinterpret_cast<uint32_t*>(&h);
-            } else {
-              __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
-              w[e] = *reinterpret_cast<uint32_t*>(&h);
-            }
+        for (int j = 0; j < kTile; j += 2) {
+          const float p0 = ptx_ex2(fmaf(s[j], sc, mneg));
+          const float p1 = ptx_ex2(fmaf(s[j + 1], sc, mneg));
+          rs4[(j >> 1) & 3] += p0 + p1;
+          if (tp.f16) {
+            __half2 h = __floats2half2_rn(p0, p1);
+            pw[j >> 1] = *reinterpret_cast<uint32_t*>(&h);
+          } else {
+            __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+            pw[j >> 1] = *reinterpret_cast<uint32_t*>(&h);
           }
-          const int a = c >> 3, cc = c & 7;
-          *reinterpret_cast<uint4*>(prow + a * kHalf + ((cc ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
         }
-        const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-        l = l * alpha + rs;
+        l = l * alpha + ((rs4[0] + rs4[1]) + (rs4[2] + rs4[3]));
+        if (n < kTile && r >= n) {  // V rows past the chunk -> 0 (0 * garbage would poison O)
+          ptx::mbar_wait(&full_v[stage], fphase);
+          uint8_t* vS = smem + kOffV + stage * kOp;
+          uint4 z = make_uint4(0, 0, 0, 0);
+          uint4* v0 = reinterpret_cast<uint4*>(vS + r * 128);
+          uint4* v1 = reinterpret_cast<uint4*>(vS + kHalf + r * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            v0[j] = z;
+            v1[j] = z;
+          }
+        }
+        wait_pv();  // PV(i-1) has finished reading P, and O is quiescent
         // tcgen05.ld/st are warp-collective: the whole warp rescales if any of its rows must
         if (__any_sync(0xffffffffu, rescale)) {
           ptx::tc_fence_after();
@@ -290,23 +312,34 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
           }
           ptx::tmem_st_wait();
         }
+        // ---- P (bf16/fp16) -> smem, K-major SW128 A operand
+        {
+          uint8_t* prow = smem + kOffP + (r >> 3) * 1024 + (r & 7) * 128;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {  // 16 chunks of 8 tokens
+            const int a = c >> 3, cc = c & 7;
+            *reinterpret_cast<uint4*>(prow + a * kHalf + ((cc ^ (r & 7)) << 4)) =
+                make_uint4(pw[4 * c], pw[4 * c + 1], pw[4 * c + 2], pw[4 * c + 3]);
+          }
+        }
         ptx::fence_proxy_async();
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, 128);
         if (ct == 0) {
           ptx::tc_fence_after();
+          ptx::mbar_wait(&full_v[stage], fphase);
           const uint32_t pa = sbase + kOffP;
-          const uint32_t va = sbase + kOffKV + stage * 2 * kOp + kOp;
+          const uint32_t va = sbase + kOffV + stage * kOp;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t a = ptx::smem_desc_sw128(pa + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
             const uint64_t b = ptx::smem_desc_sw128(va + kk * 2048, kHalf, 1024);
             ptx::mma_f16_ss(tmem + 256, a, b, idO, (ti > 0 || kk > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&empty[stage]);
+          ptx::mma_commit(&empty_v[stage]);
           ptx::mma_commit(bar_pv);
           if (!next_issued && ti + 1 < d.ntiles) {
-            ptx::mbar_wait(&full[nstage], nfphase);
+            ptx::mbar_wait(&full_k[nstage], nfphase);
             issue_S(nstage, sbuf ^ 1, qaddr);
           }
         }

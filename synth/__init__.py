@@ -221,3 +221,64 @@ def raw_bits(t: torch.Tensor) -> np.ndarray:
     if t.dtype == torch.float32:
         return t.numpy()
     return t.view(torch.int16).numpy().view(np.uint16)
+
+
+# ------------------------------------------------------- composable formats ---
+@dataclasses.dataclass
+class ComposableInputs:
+    """Shared-prefix parallel generation (fig:flashinfer-composable-formats):
+    n branches share `prefix_len` tokens of KV; each branch has its own `suffix_len` tokens.
+    The same physical pool is described three ways (index arrays only, no data movement):
+      single : one BSR, request b = prefix pages + its suffix pages (B_r = 1)
+      prefix : one "request" whose l_qo = n query rows (the branches) attend the shared pages
+               (the large-B_r block of the paper's figure)
+      suffix : n requests over their own suffix pages."""
+    q: torch.Tensor          # [n, H_qo, D] one decode query per branch
+    k_pool: torch.Tensor
+    v_pool: torch.Tensor
+    strides: tuple
+    single: dict
+    prefix: dict
+    suffix: dict
+    sm_scale: float
+    H_qo: int
+    H_kv: int
+    D: int
+    page_size: int
+    dtype: str
+
+
+def c4_composable(n_branch=64, prefix_len=8192, suffix_len=256, H_qo=32, H_kv=8, D=128, page_size=16, dtype="bf16",
+                  device="cpu", seed_base=0, permute=True) -> ComposableInputs:
+    """BASELINE.json configs[3]: 8K shared prefix + 64 branches x 256-token suffixes (decode step).
+    Heads follow Llama-3-8B (32/8; an assumption, BASELINE gives only bf16)."""
+    ps = page_size
+    n_pre = -(-prefix_len // ps)
+    n_suf = -(-suffix_len // ps)
+    assert prefix_len % ps == 0, "the shared prefix ends on a page boundary (a page is never shared partially)"
+    total = n_pre + n_branch * n_suf
+    perm = np.random.default_rng(SEED_PERM + seed_base).permutation(total) if permute else np.arange(total)
+    pre_pages = perm[:n_pre].astype(np.int32)
+    suf_pages = perm[n_pre:].astype(np.int32).reshape(n_branch, n_suf)
+    suf_last = suffix_len - (n_suf - 1) * ps
+    dt = DTYPES[dtype]
+    shape = (total, ps, H_kv, D)
+    strides = (ps * H_kv * D, H_kv * D, D)
+    q = torch.randn((n_branch, H_qo, D), generator=_gen(device, SEED_Q + seed_base), device=device).to(dt)
+    k = torch.empty(shape, device=device, dtype=dt)
+    v = torch.empty(shape, device=device, dtype=dt)
+    gk, gv = _gen(device, SEED_K + seed_base), _gen(device, SEED_V + seed_base)
+    k.copy_(torch.randn(shape, generator=gk, device=device).to(dt))
+    v.copy_((torch.rand(shape, generator=gv, device=device) * 2 - 1).to(dt))
+    ar = np.arange(n_branch + 1, dtype=np.int32)
+    single = dict(qo_indptr=ar.copy(), kv_page_indptr=(ar * (n_pre + n_suf)).astype(np.int32),
+                  kv_last_page_len=np.full(n_branch, suf_last, np.int32),
+                  kv_page_indices=np.concatenate([np.concatenate([pre_pages, suf_pages[b]])
+                                                  for b in range(n_branch)]).astype(np.int32))
+    prefix = dict(qo_indptr=np.array([0, n_branch], np.int32), kv_page_indptr=np.array([0, n_pre], np.int32),
+                  kv_last_page_len=np.array([ps], np.int32), kv_page_indices=pre_pages.copy())
+    suffix = dict(qo_indptr=ar.copy(), kv_page_indptr=(ar * n_suf).astype(np.int32),
+                  kv_last_page_len=np.full(n_branch, suf_last, np.int32),
+                  kv_page_indices=suf_pages.reshape(-1).copy())
+    return ComposableInputs(q, k, v, strides, single, prefix, suffix, 1.0 / float(np.sqrt(D)), H_qo, H_kv, D, ps,
+                            dtype)

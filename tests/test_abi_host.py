@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_library_exports_every_declared_symbol():
-    hdr = open(os.path.join(ROOT, "include", "bsra.h")).read()
+    hdr = open(os.path.join(ROOT, "include", "bsra.h")).read() + open(os.path.join(ROOT, "include", "bsra_dist.h")).read()
     hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)  # drop comments
     declared = set(re.findall(r"\b(bsra_[a-z_]+)\(", hdr))
     assert declared, "no declarations parsed"
