@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbsra.so")
+LIB_PATH = os.environ.get("BSRA_LIB") or os.path.join(_HERE, "libbsra.so")  # override: A/B builds
 
 F32, F16, BF16 = 0, 1, 2
 MASK = {"none": 0, "causal": 1, "custom": 2}

@@ -40,13 +40,19 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
-// Watchdog: a wait that never completes (a pipeline bug) traps after ~2^26 polls instead of
-// hanging the GPU; the launch then fails with an error.
+// Debug builds (make WATCHDOG=1 -> -DBSRA_WATCHDOG): a wait that never completes (a pipeline
+// bug) traps after ~2^26 polls instead of hanging the GPU. Off by default: the counter in the
+// polling loop measured 20% slower decode (bench A/B on one box, 0.163 vs 0.136 ms/launch).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#ifndef BSRA_WATCHDOG
+  while (!mbar_try_wait(bar, phase)) {
+  }
+#else
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, phase)) {
     if (++spins > (1u << 26)) __trap();
   }
+#endif
 }
 
 // ---------------------------------------------------------------------- TMA
