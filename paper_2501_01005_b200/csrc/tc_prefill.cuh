@@ -16,8 +16,11 @@
 //              are applied per element only on tiles that cross a row's limit.
 // Epilogue: unsplit rows write o / lse (App. D.2), split rows fp32 partial slots.
 #pragma once
+#include <cstdlib>
+
 #include "tc_decode.cuh"
 #include "tc_kernels.hpp"
+#include "tc_prefill2.cuh"
 
 namespace bsra {
 
@@ -458,10 +461,19 @@ inline int tc_prefill_launch(const AttnParams& p, const TcLaunch& L, cudaStream_
     return -1;
   }
   cudaError_t e;
-  switch (L.mask) {
-    case 0: e = launch_prefill_t<0>(tp, L.grid, st); break;
-    case 1: e = launch_prefill_t<1>(tp, L.grid, st); break;
-    default: e = launch_prefill_t<2>(tp, L.grid, st); break;
+  static const bool v1 = getenv("BSRA_PREFILL_V1") != nullptr;  // A/B against the one-warpgroup kernel
+  if (v1) {
+    switch (L.mask) {
+      case 0: e = launch_prefill_t<0>(tp, L.grid, st); break;
+      case 1: e = launch_prefill_t<1>(tp, L.grid, st); break;
+      default: e = launch_prefill_t<2>(tp, L.grid, st); break;
+    }
+  } else {
+    switch (L.mask) {
+      case 0: e = launch_prefill2_t<0>(tp, L.grid, st); break;
+      case 1: e = launch_prefill2_t<1>(tp, L.grid, st); break;
+      default: e = launch_prefill2_t<2>(tp, L.grid, st); break;
+    }
   }
   if (e != cudaSuccess) return -1;
   *name = "tc_prefill";

@@ -1,0 +1,6 @@
+timeout -s KILL 120 python -m pytest tests/test_gpu_tc.py -q -x -k "prefill_masks_tiles and causal and 128" 2>&1 | tail -15
+timeout -s KILL 400 python -m pytest tests/test_gpu_tc.py tests/test_composable.py -q --maxfail=5 -k "prefill or composable" 2>&1 | tail -8
+for v in 2 1; do
+if [ $v = 1 ]; then export BSRA_PREFILL_V1=1; fi
+timeout -s KILL 300 python bench.py --no-cpu-baseline --no-e2e --no-composable --no-long --steps 5 --layers 4 2>/dev/null | python -c "import json,sys;d=json.load(sys.stdin);print('v$v',d['prefill']['value'],d['prefill']['ms_per_layer'])"
+done
