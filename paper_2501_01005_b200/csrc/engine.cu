@@ -120,6 +120,7 @@ struct bsra_engine {
   float sm_scale = 0.f;
   int64_t total_qo = 0;
   int32_t max_qo = 0;
+  long long* trace = nullptr;  // debug: device buffer for kernel pipeline traces
   int32_t last_launches = 0;
   const char* selected = "none";
 };
@@ -345,6 +346,7 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
   p.part_o = reinterpret_cast<float*>(e->ws + e->lay.off_part_o);
   p.part_lse = reinterpret_cast<float*>(e->ws + e->lay.off_part_lse);
   p.counters = reinterpret_cast<int32_t*>(e->ws + e->lay.off_counters);
+  p.trace = e->trace;
   p.H_qo = c.num_qo_heads;
   p.H_kv = c.num_kv_heads;
   p.g = c.num_qo_heads / c.num_kv_heads;
@@ -398,6 +400,12 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
 }
 
 int32_t bsra_last_run_launches(const bsra_engine* e) { return e ? e->last_launches : 0; }
+
+// Debug hook (not part of the public header): kernels that support tracing record CTA 0's
+// pipeline events into this device buffer (NULL disables). See scripts/trace_prefill.py.
+extern "C" void bsra_debug_set_trace(bsra_engine* e, long long* dev_buf) {
+  if (e) e->trace = dev_buf;
+}
 
 const char* bsra_selected_kernel(const bsra_engine* e) { return e ? e->selected : "none"; }
 

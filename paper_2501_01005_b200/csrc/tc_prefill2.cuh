@@ -2,17 +2,20 @@
 //
 // Same math and plan contract as tc_prefill.cuh (one work item = (request, kv head, q tile of
 // 128 head-fused rows, kv chunk) from Algorithm 1, App. A head fusion, online softmax P:95,
-// writethrough App. D.2), re-organised so the tensor core never waits for one softmax:
+// writethrough App. D.2), organised so that neither the tensor core nor the TMA engine waits on
+// address arithmetic:
 //   * the CTA's plan queue is split into two item streams (even / odd queue positions), one per
-//     softmax warpgroup (WG); each WG owns its S/P and O accumulators in TMEM (4 x 128 columns);
-//   * a dedicated MMA warp walks the two streams' KV tiles in a fixed interleaved order and
-//     issues S_w = Q_w K^T as soon as K has landed and WG w released its S buffer, and
-//     O_w += P_w V with P_w read straight from TMEM (TS-MMA; P overwrites the consumed S columns);
-//   * producers: warp 0 loads Q (per WG) and K, warp 1 loads V, through separate rings, in the
-//     same interleaved order; per page one TMA box {64 d, B_c tokens} per 64-column half, page
-//     coordinate from the BSR indices (§3.2.1);
-//   * softmax reads S from TMEM twice (max pass, exp pass) to keep registers low, uses ex2.approx
-//     with the scale folded into an FFMA, lazy O rescale (threshold 2^8, exact).
+//     softmax warpgroup (WG); WG w owns S/P_w and O_w in TMEM (4 x 128 columns);
+//   * a scheduler warp walks the two streams' KV tiles in a fixed interleaved order, batch-loads
+//     the tiles' BSR page ids with all 32 lanes, and publishes one small descriptor per tile into
+//     a shared-memory ring — the producers and the MMA warp only read descriptors;
+//   * warp 0 loads Q (per WG) and K, warp 1 loads V through separate rings; per page one TMA box
+//     {64 d, B_c tokens} per 64-column half, page id from the descriptor (§3.2.1);
+//   * the MMA warp issues S_w = Q_w K^T as soon as K has landed and WG w is not holding its S
+//     buffer, and O_w += P_w V with P_w read straight from TMEM (TS-MMA; P overwrites the
+//     consumed S columns);
+//   * softmax reads S from TMEM twice (max pass, exp pass) to keep registers low, ex2.approx with
+//     the scale folded into an FFMA, lazy O rescale (threshold 2^8, exact).
 // Ordering facts used: tcgen05 MMAs of one thread complete in issue order, so S_w(t+1) ready
 // implies PV_w(t) done (O_w quiescent while WG w runs its softmax).
 #pragma once
@@ -25,17 +28,32 @@ namespace pre2 {
 constexpr int kTile = 128;
 constexpr int kKStages = 3;
 constexpr int kVStages = 2;
+constexpr int kDesc = 12;          // tile-descriptor ring
 constexpr int kHalf = 128 * 128;   // 16 KB: 128 rows x 128 B
 constexpr int kOp = 2 * kHalf;     // 32 KB operand (128 x 128 bf16, two SW128 halves)
 constexpr int kOffQ = 0;           // [2 WGs]
 constexpr int kOffK = 2 * kOp;
 constexpr int kOffV = kOffK + kKStages * kOp;
 constexpr int kOffBar = kOffV + kVStages * kOp;
-constexpr int kSmemBytes = kOffBar + 512 + 1024;
-constexpr int kThreads = 384;      // warps 0 Q+K producer, 1 V producer, 2 MMA, 3 idle, 4-7 WG0, 8-11 WG1
+constexpr int kOffDesc = kOffBar + 512;
+constexpr int kSmemBytes = kOffDesc + kDesc * 96 + 1024;
+constexpr int kThreads = 384;  // warps 0 Q+K producer, 1 V producer, 2 MMA, 3 scheduler, 4-7 WG0, 8-11 WG1
 constexpr uint32_t kTmemCols = 512;  // S/P_w at w*128, O_w at 256 + w*128
 constexpr float kRescaleThresh = 8.f;
 }  // namespace pre2
+
+// One KV tile of the interleaved order, as published by the scheduler warp.
+struct TileDesc {
+  int32_t w;           // softmax WG (-1: end of schedule)
+  int32_t flags;       // bit0: first tile of its item, bit1: last tile of its item
+  int32_t kvh;
+  int32_t t0;          // first token of the tile within the request
+  int32_t n;           // tokens in the tile
+  int32_t head0, tok0; // Q tile coordinates (first tile only)
+  int32_t pad;
+  int32_t page[16];    // page id of sub-block j (B_c tokens, or 128 of a page >= 128)
+};
+static_assert(sizeof(TileDesc) == 96, "TileDesc layout");
 
 // Walks one WG's item stream (queue positions it0+w, it0+w+2, ...) tile by tile.
 struct ItemStream {
@@ -56,34 +74,33 @@ struct ItemStream {
     }
   }
   __device__ __forceinline__ bool alive() const { return it < it1; }
-  // advance one tile; returns true if an item boundary was crossed
-  __device__ __forceinline__ bool advance(const PlanView& pv, int g) {
-    if (++ti < d.ntiles) return false;
+  __device__ __forceinline__ void advance(const PlanView& pv, int g) {
+    if (++ti < d.ntiles) return;
     ti = 0;
     it += 2;
     skip_empty(pv, g);
-    return true;
   }
 };
 
 // Deterministic interleave of the two streams: alternate while both are alive.
 struct Interleave {
-  ItemStream s[2];
+  ItemStream s0, s1;
   int turn = 0;
   __device__ __forceinline__ void init(const PlanView& pv, int g, int it0, int it1) {
-    s[0].init(pv, g, it0, it1);
-    s[1].init(pv, g, it0 + 1, it1);
+    s0.init(pv, g, it0, it1);
+    s1.init(pv, g, it0 + 1, it1);
     turn = 0;
   }
   __device__ __forceinline__ int pick() const {  // -1 when both exhausted
-    if (s[0].alive() && s[1].alive()) return turn;
-    if (s[0].alive()) return 0;
-    if (s[1].alive()) return 1;
+    if (s0.alive() && s1.alive()) return turn;
+    if (s0.alive()) return 0;
+    if (s1.alive()) return 1;
     return -1;
   }
   __device__ __forceinline__ void step(const PlanView& pv, int g, int w) {
-    const bool both = s[0].alive() && s[1].alive();
-    s[w].advance(pv, g);
+    const bool both = s0.alive() && s1.alive();
+    if (w == 0) s0.advance(pv, g);
+    else s1.advance(pv, g);
     if (both) turn ^= 1;
   }
 };
@@ -104,7 +121,10 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   uint64_t* bar_s = empty_q + 2;             // [2] S_w ready
   uint64_t* p_ready = bar_s + 2;             // [2] P_w written (128 arrivals)
   uint64_t* bar_o = p_ready + 2;             // [2] last PV of WG w's item done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_o + 2);
+  uint64_t* desc_full = bar_o + 2;           // [kDesc] descriptor published
+  uint64_t* desc_empty = desc_full + kDesc;  // [kDesc] released by K producer, V producer, MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(desc_empty + kDesc);
+  TileDesc* descs = reinterpret_cast<TileDesc*>(smem + kOffDesc);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const PlanView pv = load_plan(p.plan);
@@ -127,6 +147,10 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       ptx::mbar_init(&p_ready[w], 128);
       ptx::mbar_init(&bar_o[w], 1);
     }
+    for (int s = 0; s < kDesc; ++s) {
+      ptx::mbar_init(&desc_full[s], 1);
+      ptx::mbar_init(&desc_empty[s], 3);
+    }
     ptx::fence_barrier_init();
   }
   if (warp == 2) ptx::tmem_alloc<kTmemCols>(tmem_slot);
@@ -135,8 +159,92 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int B = tp.box_tok;
+  const int ps = p.page_size;
+  // debug trace (CTA 0): trace[ev * 1024 + i] = clock64() of the i-th event of kind ev
+  long long* const trace = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
+#define BSRA_TRACE(ev, i) \
+  if (trace && (i) < 1024) trace[(ev) * 1024 + (i)] = clock64();
+  if (threadIdx.x == 0) BSRA_TRACE(9, 0);
 
-  if (warp == 0 || warp == 1) {
+  if (warp == 3) {
+    // ===================== scheduler: interleaved tile descriptors =====================
+    Interleave il;
+    il.init(pv, g, it0, it1);
+    const int spp = kTile / B;             // sub-blocks of a full tile (<= 16)
+    const int G = min(4, 32 / spp);        // positions per batched index load
+    int pos = 0;
+    bool done = false;
+    while (!done) {
+      // collect up to G positions (warp-uniform bookkeeping)
+      int cw[4], cflags[4], ckvh[4], ct0[4], cn[4], chead0[4], ctok0[4];
+      int64_t cpb[4];
+      int cnt = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k >= G) break;
+        const int w = il.pick();
+        if (w < 0) {
+          done = true;
+          break;
+        }
+        const ItemStream& s = w == 0 ? il.s0 : il.s1;
+        const DecItem& d = s.d;
+        cw[k] = w;
+        cflags[k] = (s.ti == 0 ? 1 : 0) | (s.ti + 1 == d.ntiles ? 2 : 0);
+        ckvh[k] = d.kvh;
+        ct0[k] = (int)(d.kb + (int64_t)s.ti * kTile);
+        cn[k] = (int)imin64(kTile, d.ke - ct0[k]);
+        chead0[k] = d.kvh * g + (g > 128 ? d.row0 % g : 0);
+        ctok0[k] = (int)d.qo_begin + d.row0 / g;
+        cpb[k] = d.page_begin;
+        il.step(pv, g, w);
+        cnt = k + 1;
+      }
+      // batched page-id loads: lane -> (position lane / spp, sub-block lane % spp)
+      const int kq = lane / spp, j = lane % spp;
+      int page = 0;
+      if (kq < cnt) {
+        int t0 = 0, n = 0;
+        int64_t pb = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k == kq) {
+            t0 = ct0[k];
+            n = cn[k];
+            pb = cpb[k];
+          }
+        if (j * B < n) page = __ldg(p.page_indices + pb + (t0 + j * B) / ps);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k >= cnt) break;
+        const int slot = pos % kDesc;
+        const uint32_t ph = ((pos / kDesc) & 1) ^ 1;
+        ptx::mbar_wait(&desc_empty[slot], ph);
+        TileDesc& D = descs[slot];
+        if (lane == 0) {
+          D.w = cw[k];
+          D.flags = cflags[k];
+          D.kvh = ckvh[k];
+          D.t0 = ct0[k];
+          D.n = cn[k];
+          D.head0 = chead0[k];
+          D.tok0 = ctok0[k];
+        }
+        if (kq == k) D.page[j] = page;
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&desc_full[slot]);
+        ++pos;
+      }
+    }
+    // terminator
+    const int slot = pos % kDesc;
+    ptx::mbar_wait(&desc_empty[slot], ((pos / kDesc) & 1) ^ 1);
+    if (lane == 0) {
+      descs[slot].w = -1;
+      ptx::mbar_arrive(&desc_full[slot]);
+    }
+  } else if (warp == 0 || warp == 1) {
     // ===================== producers: warp 0 = Q + K, warp 1 = V =====================
     const bool isK = warp == 0;
     if (lane == 0) {
@@ -147,8 +255,6 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         ptx::tma_prefetch_desc(&tp.tv);
       }
     }
-    Interleave il;
-    il.init(pv, g, it0, it1);
     int stage = 0;
     uint32_t ephase = 1;
     uint32_t qphase[2] = {1, 1};
@@ -157,28 +263,26 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
     uint64_t* emptyx = isK ? empty_k : empty_v;
     const CUtensorMap* tm = isK ? &tp.tk : &tp.tv;
     const int ring = isK ? kOffK : kOffV;
-    for (int w = il.pick(); w >= 0; w = il.pick()) {
-      const DecItem& d = il.s[w].d;
-      const int ti = il.s[w].ti;
-      if (isK && ti == 0 && lane == 0) {  // Q of WG w's next item
-        ptx::mbar_wait(&empty_q[w], qphase[w]);
-        qphase[w] ^= 1;
-        ptx::mbar_arrive_expect_tx(&full_q[w], kOp);
-        const int head0 = d.kvh * g + (g > 128 ? d.row0 % g : 0);
-        const int tok0 = (int)d.qo_begin + d.row0 / g;
-        uint8_t* qdst = smem + kOffQ + w * kOp;
-        ptx::tma_load_3d(qdst, &tp.tq, &full_q[w], 0, head0, tok0);
-        ptx::tma_load_3d(qdst + kHalf, &tp.tq, &full_q[w], 64, head0, tok0);
-      }
-      const int64_t t0 = d.kb + (int64_t)ti * kTile;
-      const int n = (int)imin64(kTile, d.ke - t0);
+    for (int pos = 0;; ++pos) {
+      const int slot = pos % kDesc;
+      ptx::mbar_wait(&desc_full[slot], (pos / kDesc) & 1);
+      const TileDesc& D = descs[slot];
+      const int w = D.w;
+      if (w < 0) break;
+      const int kvh = D.kvh, t0 = D.t0, n = D.n;
       const int nsub = (n + B - 1) / B;
-      int page = 0, off = 0;
-      if (lane < nsub) {
-        const int64_t tok = t0 + (int64_t)lane * B;
-        page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
-        off = (int)(tok % p.page_size);
+      const int page = lane < nsub ? D.page[lane] : 0;
+      const int off = (t0 + lane * B) % ps;
+      if (isK && (D.flags & 1) && lane == 0) {  // Q of WG w's next item
+        ptx::mbar_wait(&empty_q[w], qphase[w]);
+        ptx::mbar_arrive_expect_tx(&full_q[w], kOp);
+        uint8_t* qdst = smem + kOffQ + w * kOp;
+        ptx::tma_load_3d(qdst, &tp.tq, &full_q[w], 0, D.head0, D.tok0);
+        ptx::tma_load_3d(qdst + kHalf, &tp.tq, &full_q[w], 64, D.head0, D.tok0);
       }
+      if (isK && (D.flags & 1)) qphase[w] ^= 1;
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&desc_empty[slot]);  // descriptor fields are in registers
       if (lane == 0) {
         ptx::mbar_wait(&emptyx[stage], ephase);
         ptx::mbar_arrive_expect_tx(&fullx[stage], (uint32_t)nsub * B * 256);
@@ -186,81 +290,88 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       __syncwarp();
       if (lane < nsub) {
         uint8_t* dst = smem + ring + stage * kOp + lane * B * 128;
-        ptx::tma_load_4d(dst, tm, &fullx[stage], 0, d.kvh, off, page);
-        ptx::tma_load_4d(dst + kHalf, tm, &fullx[stage], 64, d.kvh, off, page);
+        if (lane == 0) BSRA_TRACE(isK ? 0 : 1, pos);
+        ptx::tma_load_4d(dst, tm, &fullx[stage], 0, kvh, off, page);
+        ptx::tma_load_4d(dst + kHalf, tm, &fullx[stage], 64, kvh, off, page);
       }
       __syncwarp();
       if (++stage == nst) {
         stage = 0;
         ephase ^= 1;
       }
-      il.step(pv, g, w);
     }
   } else if (warp == 2) {
-    // ===================== MMA issuer (one elected lane) =====================
+    // ===================== MMA issuer =====================
+    // Two cursors over the descriptor ring: S in order (K ring), PV in order (V ring). A WG has
+    // one S buffer, so its next S is issued only after the PV of its current tile (in-order
+    // tensor pipe => no WAR hazard on TMEM).
     const uint32_t fmt = tp.f16 ? 0u : 1u;
     const uint32_t idS = ptx::idesc_f16(fmt, 128, kTile, 0, 0);  // A = Q (K-major), B = K (K-major)
     const uint32_t idO = ptx::idesc_f16(fmt, 128, 128, 0, 1);    // A = P (TMEM), B = V (MN-major)
     const uint32_t sbase = ptx::smem_u32(smem);
-    // Two cursors over the same interleaved tile sequence: `sq` issues S (K ring order), `il`
-    // issues PV (V ring order). A WG has one S buffer, so S of its next tile waits until the PV
-    // of its current tile has been issued (in-order tensor pipe => no WAR hazard on TMEM).
-    Interleave il, sq;
-    il.init(pv, g, it0, it1);
-    sq.init(pv, g, it0, it1);
     int kst = 0, vst = 0;
     uint32_t kph = 0, vph = 0;
     uint32_t qph[2] = {0, 0}, pph[2] = {0, 0};
-    bool q_loaded[2] = {false, false};
-    int pending[2] = {0, 0};  // WG w has an S issued whose PV is not yet issued
-    auto issue_S = [&](int w) {
-      const DecItem& d = sq.s[w].d;
-      const bool last = sq.s[w].ti + 1 == d.ntiles;
-      if (!q_loaded[w]) {  // first tile of a new item: wait for its Q
-        if (lane == 0) ptx::mbar_wait(&full_q[w], qph[w]);
-        qph[w] ^= 1;
-        q_loaded[w] = true;
-      }
-      if (lane == 0) {
-        ptx::mbar_wait(&full_k[kst], kph);
-        ptx::tc_fence_after();
-        const uint32_t qa = sbase + kOffQ + w * kOp, ka = sbase + kOffK + kst * kOp;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t a = ptx::smem_desc_sw128(qa + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
-          const uint64_t b = ptx::smem_desc_sw128(ka + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
-          ptx::mma_f16_ss(tmem + w * 128, a, b, idS, kk > 0);
+    int pending[2] = {0, 0};
+    int s_pos = 0, pv_pos = 0;
+    bool s_done = false;
+    for (;;) {
+      // ---- issue S in order while the next tile's WG is not holding its S buffer
+      while (!s_done) {
+        const int slot = s_pos % kDesc;
+        const uint32_t ph = (s_pos / kDesc) & 1;
+        if (pv_pos == s_pos) ptx::mbar_wait(&desc_full[slot], ph);
+        else if (!ptx::mbar_test_wait(&desc_full[slot], ph)) break;
+        const TileDesc& D = descs[slot];
+        const int w = D.w;
+        if (w < 0) {
+          s_done = true;
+          break;
         }
-        ptx::mma_commit(&empty_k[kst]);
-        ptx::mma_commit(&bar_s[w]);
-        if (last) ptx::mma_commit(&empty_q[w]);  // last S of the item: Q buffer free
+        if (pending[w]) break;
+        const int flags = D.flags;
+        if (flags & 1) {  // first tile of an item: its Q must have landed
+          ptx::mbar_wait(&full_q[w], qph[w]);
+          qph[w] ^= 1;
+        }
+        ptx::mbar_wait(&full_k[kst], kph);
+        if (lane == 0) {
+          BSRA_TRACE(2, s_pos);
+          ptx::tc_fence_after();
+          const uint32_t qa = sbase + kOffQ + w * kOp, ka = sbase + kOffK + kst * kOp;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t a = ptx::smem_desc_sw128(qa + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
+            const uint64_t b = ptx::smem_desc_sw128(ka + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
+            ptx::mma_f16_ss(tmem + w * 128, a, b, idS, kk > 0);
+          }
+          ptx::mma_commit(&empty_k[kst]);
+          ptx::mma_commit(&bar_s[w]);
+          if (flags & 2) ptx::mma_commit(&empty_q[w]);  // last S of the item: Q buffer free
+        }
+        __syncwarp();
+        if (++kst == kKStages) {
+          kst = 0;
+          kph ^= 1;
+        }
+        pending[w] = 1;
+        ++s_pos;
       }
-      __syncwarp();
-      if (last) q_loaded[w] = false;
-      if (++kst == kKStages) {
-        kst = 0;
-        kph ^= 1;
-      }
-      pending[w] = 1;
-      sq.step(pv, g, w);
-    };
-    for (int w = il.pick(); w >= 0; w = il.pick()) {
-      for (int sw = sq.pick(); sw >= 0 && !pending[sw]; sw = sq.pick()) issue_S(sw);
-      const DecItem d = il.s[w].d;
-      const int ti = il.s[w].ti;
-      const int64_t t0 = d.kb + (int64_t)ti * kTile;
-      const int n = (int)imin64(kTile, d.ke - t0);
-      // wait V, zero rows past the chunk (0 * garbage could be NaN)
+      if (pv_pos == s_pos) break;  // schedule finished and every PV issued
+      // ---- PV of the oldest tile
+      const int slot = pv_pos % kDesc;
+      const TileDesc& D = descs[slot];
+      const int w = D.w, n = D.n, flags = D.flags;
       ptx::mbar_wait(&full_v[vst], vph);
-      if (n < kTile) {
+      if (n < kTile) {  // rows past the chunk -> 0 (0 * garbage could be NaN)
         uint8_t* vS = smem + kOffV + vst * kOp;
         for (int rr = n + lane; rr < kTile; rr += 32) {
           uint4* v0 = reinterpret_cast<uint4*>(vS + rr * 128);
           uint4* v1 = reinterpret_cast<uint4*>(vS + kHalf + rr * 128);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            v0[j] = make_uint4(0, 0, 0, 0);
-            v1[j] = make_uint4(0, 0, 0, 0);
+          for (int jj = 0; jj < 8; ++jj) {
+            v0[jj] = make_uint4(0, 0, 0, 0);
+            v1[jj] = make_uint4(0, 0, 0, 0);
           }
         }
         ptx::fence_proxy_async();
@@ -269,15 +380,17 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       ptx::mbar_wait(&p_ready[w], pph[w]);
       pph[w] ^= 1;
       if (lane == 0) {
+        BSRA_TRACE(3, pv_pos);
         ptx::tc_fence_after();
         const uint32_t va = sbase + kOffV + vst * kOp;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t b = ptx::smem_desc_sw128(va + kk * 2048, kHalf, 1024);
-          ptx::mma_f16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, b, idO, (ti > 0 || kk > 0) ? 1u : 0u);
+          ptx::mma_f16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, b, idO, ((flags & 1) && kk == 0) ? 0u : 1u);
         }
         ptx::mma_commit(&empty_v[vst]);
-        if (ti + 1 == d.ntiles) ptx::mma_commit(&bar_o[w]);
+        if (flags & 2) ptx::mma_commit(&bar_o[w]);
+        ptx::mbar_arrive(&desc_empty[slot]);
       }
       __syncwarp();
       if (++vst == kVStages) {
@@ -285,7 +398,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         vph ^= 1;
       }
       pending[w] = 0;
-      il.step(pv, g, w);
+      ++pv_pos;
     }
   } else if (warp >= 4) {
     // ===================== softmax warpgroups =====================
@@ -297,6 +410,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
     const uint32_t tO = tmem + lane_addr + 256 + w * 128;
     const float sc = p.scale_log2;
     uint32_t sph = 0, oph = 0;
+    int tcount = 0;
     for (int it = it0 + w; it < it1; it += 2) {
       const DecItem d = dec_item(pv, it, g);
       const bool row_ok = r < d.nrows;
@@ -313,6 +427,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         const bool need_mask = kMask == 2 || nvis < kTile;
         ptx::mbar_wait(&bar_s[w], sph);
         sph ^= 1;
+        if (r == 0) BSRA_TRACE(5 + 2 * w, tcount);
         ptx::tc_fence_after();
         // ---- pass 1: raw row max
         float mx = -INFINITY;
@@ -400,6 +515,8 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_ready[w]);
+        if (r == 0) BSRA_TRACE(6 + 2 * w, tcount);
+        ++tcount;
       }
       // ---- epilogue: wait for the item's last PV, normalise, write
       if (d.ntiles > 0) {
@@ -458,6 +575,8 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) BSRA_TRACE(9, 1);
+#undef BSRA_TRACE
   if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 
