@@ -109,6 +109,39 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Warp-converged variants: all 32 lanes execute the instruction stream, one lane (elect.sync)
+// issues. Keeping the warp converged lets ptxas hold the (warp-uniform) descriptors in uniform
+// registers instead of wrapping every MMA in an R2UR.BROADCAST / ELECT loop (measured ~90
+// cycles per MMA issued from under `if (lane == 0)`).
+__device__ __forceinline__ void mma_f16_ss_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred e, p;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred e, p;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n @e mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
 // arrive on an mbarrier when all previously issued tcgen05 ops of this thread complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
@@ -231,6 +264,23 @@ __device__ __forceinline__ float ptx_ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;\n" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe (offloads the SFU): x = n + f with n = rint(x), f in [-1/2, 1/2];
+// 2^f by a degree-3 minimax polynomial (Lawson-fitted, max rel. error 7.5e-5, far below the bf16
+// rounding P receives before the PV MMA and the 1e-3 lse tolerance); 2^n added to the exponent
+// field. Valid for x in [-126, 126]; x <= -126 (incl. masked -inf) returns 0.
+__device__ __forceinline__ float poly_ex2(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;          // 1.5 * 2^23: rint(x) lands in the mantissa
+  const float n = t - 12582912.f;
+  const float f = x - n;
+  float p = fmaf(f, 0.05517138f, 0.24261121f);
+  p = fmaf(p, f, 0.693261f);
+  p = fmaf(p, f, 0.99992806f);
+  const int ni = __float_as_int(t) - 0x4B400000;
+  const float r = __int_as_float(__float_as_int(p) + (ni << 23));
+  return x <= -126.f ? 0.f : r;
 }
 
 namespace ptx {

@@ -335,21 +335,23 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           qph[w] ^= 1;
         }
         ptx::mbar_wait(&full_k[kst], kph);
-        if (lane == 0) {
-          BSRA_TRACE(2, s_pos);
-          ptx::tc_fence_after();
-          const uint32_t qa = sbase + kOffQ + w * kOp, ka = sbase + kOffK + kst * kOp;
+        if (lane == 0) BSRA_TRACE(2, s_pos);
+        ptx::tc_fence_after();
+        {
+          // warp-converged issue (elect inside the asm); descriptors: +2 (32 B) per K step
+          // inside a 64-column atom, +1024 (16 KB) per atom
+          const uint64_t a0 = ptx::smem_desc_sw128(sbase + kOffQ + w * kOp, 16, 1024);
+          const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffK + kst * kOp, 16, 1024);
+          const uint32_t dS = tmem + w * 128;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t a = ptx::smem_desc_sw128(qa + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
-            const uint64_t b = ptx::smem_desc_sw128(ka + (kk >> 2) * kHalf + (kk & 3) * 32, 16, 1024);
-            ptx::mma_f16_ss(tmem + w * 128, a, b, idS, kk > 0);
+            const uint64_t step = (uint64_t)((kk >> 2) * (kHalf >> 4) + (kk & 3) * 2);
+            ptx::mma_f16_ss_warp(dS, a0 + step, b0 + step, idS, kk > 0);
           }
-          ptx::mma_commit(&empty_k[kst]);
-          ptx::mma_commit(&bar_s[w]);
-          if (flags & 2) ptx::mma_commit(&empty_q[w]);  // last S of the item: Q buffer free
         }
-        __syncwarp();
+        ptx::mma_commit_warp(&empty_k[kst]);
+        ptx::mma_commit_warp(&bar_s[w]);
+        if (flags & 2) ptx::mma_commit_warp(&empty_q[w]);  // last S of the item: Q buffer free
         if (++kst == kKStages) {
           kst = 0;
           kph ^= 1;
@@ -379,20 +381,18 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       }
       ptx::mbar_wait(&p_ready[w], pph[w]);
       pph[w] ^= 1;
-      if (lane == 0) {
-        BSRA_TRACE(3, pv_pos);
-        ptx::tc_fence_after();
-        const uint32_t va = sbase + kOffV + vst * kOp;
+      if (lane == 0) BSRA_TRACE(3, pv_pos);
+      ptx::tc_fence_after();
+      {
+        const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffV + vst * kOp, kHalf, 1024);
+        const uint32_t dO = tmem + 256 + w * 128, aP = tmem + w * 128;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint64_t b = ptx::smem_desc_sw128(va + kk * 2048, kHalf, 1024);
-          ptx::mma_f16_ts(tmem + 256 + w * 128, tmem + w * 128 + kk * 8, b, idO, ((flags & 1) && kk == 0) ? 0u : 1u);
-        }
-        ptx::mma_commit(&empty_v[vst]);
-        if (flags & 2) ptx::mma_commit(&bar_o[w]);
-        ptx::mbar_arrive(&desc_empty[slot]);
+        for (int kk = 0; kk < 8; ++kk)  // +128 (2 KB = 16 tokens) per K step of the MN-major V
+          ptx::mma_f16_ts_warp(dO, aP + kk * 8, b0 + (uint64_t)(kk * 128), idO, ((flags & 1) && kk == 0) ? 0u : 1u);
       }
-      __syncwarp();
+      ptx::mma_commit_warp(&empty_v[vst]);
+      if (flags & 2) ptx::mma_commit_warp(&bar_o[w]);
+      ptx::mbar_arrive_warp(&desc_empty[slot]);
       if (++vst == kVStages) {
         vst = 0;
         vph ^= 1;
@@ -429,16 +429,17 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         sph ^= 1;
         if (r == 0) BSRA_TRACE(5 + 2 * w, tcount);
         ptx::tc_fence_after();
-        // ---- pass 1: raw row max
+        // ---- pass 1: raw row max (two 32-column TMEM loads in flight per round trip)
         float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float s[32];
+        for (int c = 0; c < 4; c += 2) {
+          float s[64];
           ptx::tmem_ld32(tS + c * 32, s);
+          ptx::tmem_ld32(tS + c * 32 + 32, s + 32);
           ptx::tmem_ld_wait();
           if (need_mask) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
+            for (int j = 0; j < 64; ++j) {
               bool vis = c * 32 + j < nvis;
               if (kMask == 2) vis = vis && mask_bit(p.mask, mbase + t0 + c * 32 + j);
               s[j] = vis ? s[j] : -INFINITY;
@@ -446,7 +447,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           }
           float a0 = fmaxf(s[0], s[1]), a1 = fmaxf(s[2], s[3]), a2 = fmaxf(s[4], s[5]), a3 = fmaxf(s[6], s[7]);
 #pragma unroll
-          for (int j = 8; j < 32; j += 4) {
+          for (int j = 8; j < 64; j += 4) {
             a0 = fmaxf(a0, s[j]);
             a1 = fmaxf(a1, s[j + 1]);
             a2 = fmaxf(a2, s[j + 2]);
@@ -481,11 +482,13 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         // ---- pass 2: P = 2^(s*scale - m) packed to 16-bit pairs, written over the consumed S columns
         const float mneg = m == -INFINITY ? 0.f : -m;
         float rs0 = 0.f, rs1 = 0.f;
+        float sbuf[2][32];  // chunk c+1's TMEM load overlaps chunk c's exponentials
+        ptx::tmem_ld32(tS, sbuf[0]);
+        ptx::tmem_ld_wait();
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          float s[32];
-          ptx::tmem_ld32(tS + c * 32, s);
-          ptx::tmem_ld_wait();
+          float* s = sbuf[c & 1];
+          if (c + 1 < 4) ptx::tmem_ld32(tS + (c + 1) * 32, sbuf[(c + 1) & 1]);
           if (need_mask) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
@@ -510,6 +513,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
             }
           }
           ptx::tmem_st16(tS + c * 16, pk);
+          ptx::tmem_ld_wait();  // chunk c+1 has landed (its columns are >= 32(c+1) > P's 16(c+1))
         }
         l = l * alpha + (rs0 + rs1);
         ptx::tmem_st_wait();
