@@ -43,6 +43,11 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t phase) {
 // Debug builds (make WATCHDOG=1 -> -DBSRA_WATCHDOG): a wait that never completes (a pipeline
 // bug) traps after ~2^26 polls instead of hanging the GPU. Off by default: the counter in the
 // polling loop measured 20% slower decode (bench A/B on one box, 0.163 vs 0.136 ms/launch).
+// warp-uniform non-blocking probe (lane 0 decides; lanes polling separately could disagree)
+__device__ __forceinline__ bool mbar_test_wait_warp(uint64_t* bar, uint32_t phase) {
+  const int ok = (threadIdx.x & 31) == 0 ? (int)mbar_test_wait(bar, phase) : 0;
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #ifndef BSRA_WATCHDOG
   while (!mbar_try_wait(bar, phase)) {

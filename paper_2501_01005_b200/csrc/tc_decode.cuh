@@ -207,16 +207,18 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     int qb = 0;
 
     // elected thread: issue S^T(tile in `st`, buffer `b`) = K Q^T
+    // issued by all 32 lanes of warp 1 (elect.sync inside the asm keeps the warp converged)
     auto issue_S = [&](int st, int b, uint32_t qaddr) {
       ptx::tc_fence_after();
-      const uint32_t ka = sbase + st * kStageBytes;
+      const uint64_t a0 = ptx::smem_desc_sw128(sbase + st * kStageBytes, 16, 1024);
+      const uint64_t b0 = ptx::smem_desc_sw128(qaddr, 16, 1024);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        const uint64_t a = ptx::smem_desc_sw128(ka + (kk >> 2) * kHalfBytes + (kk & 3) * 32, 16, 1024);
-        const uint64_t bd = ptx::smem_desc_sw128(qaddr + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
-        ptx::mma_f16_ss(tmem + b * 16, a, bd, idS, kk > 0);
+        const uint64_t sa = (uint64_t)((kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2);
+        const uint64_t sb = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
+        ptx::mma_f16_ss_warp(tmem + b * 16, a0 + sa, b0 + sb, idS, kk > 0);
       }
-      ptx::mma_commit(&bar_s[b]);
+      ptx::mma_commit_warp(&bar_s[b]);
     };
     auto wait_pv = [&](int b) {
       if (pv_pending[b]) {
@@ -242,7 +244,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       }
       // prologue: S^T of tile 0
       bool next_issued = false;
-      if (d.ntiles > 0 && ct == 0) {
+      if (d.ntiles > 0 && warp == 1) {
         ptx::mbar_wait(&full[stage], fphase);
         issue_S(stage, sbuf, qaddr);
       }
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         const uint32_t nfphase = nstage == 0 ? fphase ^ 1 : fphase;
         // early issue of the next S^T when its K tile has already landed
         next_issued = false;
-        if (ct == 0 && ti + 1 < d.ntiles && ptx::mbar_test_wait(&full[nstage], nfphase)) {
+        if (warp == 1 && ti + 1 < d.ntiles && ptx::mbar_test_wait_warp(&full[nstage], nfphase)) {
           issue_S(nstage, sbuf ^ 1, qaddr);
           next_issued = true;
         }
@@ -345,18 +347,17 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, 128);
         // ---- O^T += V^T P^T ; then the next S^T if it was not issued early
-        if (ct == 0) {
+        if (warp == 1) {
           ptx::tc_fence_after();
-          const uint32_t va = sbase + stage * kStageBytes + kKVBytes;
-          const uint32_t pa = sbase + kOffP + pbuf * kPBytes;
+          const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes + kKVBytes, kHalfBytes, 1024);
+          const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffP + pbuf * kPBytes, 16, 1024);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t a = ptx::smem_desc_sw128(va + kk * 2048, kHalfBytes, 1024);
-            const uint64_t b = ptx::smem_desc_sw128(pa + (kk >> 2) * (kN * 128) + (kk & 3) * 32, 16, 1024);
-            ptx::mma_f16_ss(tmem + 32, a, b, idO, (ti > 0 || kk > 0) ? 1u : 0u);
+            const uint64_t sb = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
+            ptx::mma_f16_ss_warp(tmem + 32, a0 + (uint64_t)(kk * 128), b0 + sb, idO, (ti > 0 || kk > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(&empty[stage]);  // K/V stage free once these MMAs complete
-          ptx::mma_commit(&bar_pv[pbuf]);
+          ptx::mma_commit_warp(&empty[stage]);  // K/V stage free once these MMAs complete
+          ptx::mma_commit_warp(&bar_pv[pbuf]);
           if (!next_issued && ti + 1 < d.ntiles) {
             ptx::mbar_wait(&full[nstage], nfphase);
             issue_S(nstage, sbuf ^ 1, qaddr);

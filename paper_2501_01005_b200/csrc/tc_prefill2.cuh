@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         const int slot = s_pos % kDesc;
         const uint32_t ph = (s_pos / kDesc) & 1;
         if (pv_pos == s_pos) ptx::mbar_wait(&desc_full[slot], ph);
-        else if (!ptx::mbar_test_wait(&desc_full[slot], ph)) break;
+        else if (!ptx::mbar_test_wait_warp(&desc_full[slot], ph)) break;
         const TileDesc& D = descs[slot];
         const int w = D.w;
         if (w < 0) {
