@@ -29,6 +29,8 @@ import torch
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# stdout carries exactly one JSON line: keep NCCL's version banner / info off it
+os.environ["NCCL_DEBUG"] = os.environ.get("BSRA_NCCL_DEBUG", "WARN")
 
 import synth  # noqa: E402
 

@@ -12,6 +12,7 @@
 // (App. D.2).
 #pragma once
 #include "common.cuh"
+#include "merge.cuh"
 
 namespace bsra {
 
@@ -173,6 +174,10 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
           if (lane == 0) p.part_lse[prow] = lse;
         }
       }
+    }
+    if (slot >= 0) {  // split item: the CTA completing its merge list folds it (fused contraction)
+      __shared__ int s_flag;
+      fused_contraction<T, D>(p, pv, slot, threadIdx.x, blockDim.x, 0, &s_flag);
     }
   }
 }

@@ -117,6 +117,7 @@ struct bsra_engine {
   std::vector<int32_t> image;  // host copy of the current plan
   bsra::PlanSummary summary;
   bool planned = false;
+  bool counters_zeroed = false;
   float sm_scale = 0.f;
   int64_t total_qo = 0;
   int32_t max_qo = 0;
@@ -262,6 +263,10 @@ bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, c
   CUDA_TRY(cudaMemcpyAsync(e->ws + e->lay.off_plan, e->staging, im.size() * 4, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(e->staged, st));
   e->have_event_pending = true;
+  if (!e->counters_zeroed) {  // merge-list arrival counters start at 0; the merging CTA resets them
+    CUDA_TRY(cudaMemsetAsync(e->ws + e->lay.off_counters, 0, (size_t)(e->lay.num_ctas + 1) * 4, st));
+    e->counters_zeroed = true;
+  }
   e->image.swap(im);
   e->summary = sum;
   e->planned = true;
@@ -290,18 +295,6 @@ bsra_status launch_simt(const bsra::AttnParams& p, int grid, cudaStream_t st) {
 template <typename T>
 bsra_status launch_simt_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st) {
   return D == 64 ? launch_simt<T, 64>(p, grid, st) : launch_simt<T, 128>(p, grid, st);
-}
-
-template <typename TO, int D>
-bsra_status launch_contraction_t(const bsra::AttnParams& p, int grid, cudaStream_t st) {
-  bsra::contraction_kernel<TO, D><<<grid, 256, 0, st>>>(p);
-  CUDA_TRY(cudaGetLastError());
-  return BSRA_OK;
-}
-
-template <typename TO>
-bsra_status launch_contraction_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st) {
-  return D == 64 ? launch_contraction_t<TO, 64>(p, grid, st) : launch_contraction_t<TO, 128>(p, grid, st);
 }
 
 }  // namespace
@@ -389,13 +382,8 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
     }
     if (s) return s;
   }
-  // contraction stage: fixed grid, exits immediately when nothing was split
-  const int cgrid = std::max(1, std::min(grid, 2 * 148));
-  if (c.o_dtype == BSRA_F32 || c.dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
-  else if (c.dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
-  else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
-  if (s) return s;
-  e->last_launches = 2;
+  // the contraction runs inside the persistent kernel (merge.cuh:fused_contraction)
+  e->last_launches = 1;
   return BSRA_OK;
 }
 

@@ -1,9 +1,10 @@
 // merge.cuh — the attention-state operator ⊕ (§2.2) on the GPU.
 //
-//  * contraction_kernel: the plan-driven "contraction" stage: for every merge
-//    list (one per split (request, kv head, q tile)) fold ⊕ over its partial slots in the
-//    plan's fixed order (ascending kv_begin, R17) — a left fold, no atomics on values
-//    (P:240), so results are deterministic.
+//  * fused_contraction: the plan-driven "contraction" stage, fused into the persistent
+//    attention kernels: for every merge list (one per split (request, kv head, q tile))
+//    fold ⊕ over its partial slots in the plan's fixed order (ascending kv_begin, R17)
+//    — a left fold, no atomics on values (an arrival counter only elects the merging CTA),
+//    so results are deterministic.
 //  * merge_states_kernel / merge_many_kernel: ⊕ of whole state tensors (composable formats,
 //    P:172-174; cross-GPU sequence split).
 // One warp per state; each lane owns D/32 consecutive dims. Max-shifted form; the empty state
@@ -39,35 +40,66 @@ __device__ __forceinline__ void store_row(void* out, int64_t row, int lane, cons
   }
 }
 
-template <typename TO, int D>
-__global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant__ AttnParams p) {
-  constexpr int kPer = D / 32;
-  const PlanView pv = load_plan(p.plan);
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int64_t total = (int64_t)pv.n_lists * pv.T_q;
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += nwarps) {
-    const int li = (int)(w / pv.T_q), r = (int)(w % pv.T_q);
-    const int req = pv.list_req[li], kvh = pv.list_kvh[li], qt = pv.list_qtile[li];
-    const int lq = pv.req_qo_len[req];
-    const int f = qt * pv.T_q + r;
-    if (f >= lq * p.g) continue;
-    const int tok = f / p.g, head = kvh * p.g + f % p.g;
-    float acc[kPer], acc_lse = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) acc[j] = 0.f;
-    for (int s = pv.list_indptr[li]; s < pv.list_indptr[li + 1]; ++s) {
-      const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
-      float o[kPer];
-      const float* src = p.part_o + prow * D + lane * kPer;
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) o[j] = src[j];
-      oplus<kPer>(acc, acc_lse, o, p.part_lse[prow]);
-    }
-    const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
-    store_row<TO, D>(p.o, orow, lane, acc, p.o_f32);
-    if (p.lse && lane == 0) p.lse[orow] = acc_lse;
+// ---------------------------------------------------------------------------------------------
+// Fused contraction ("We merge the two stages into one persistent kernel"): after the
+// `nthr` threads of a CTA (or warpgroup) have written the partial rows of a split item, they
+// call this. The CTA whose arrival completes a merge list folds that list's slots in the plan's
+// fixed order (deterministic: the result does not depend on which CTA merges) and resets the
+// list's counter for the next launch. Partials of other CTAs are read with ld.global.cg (L1 is
+// not coherent across SMs).
+__device__ __forceinline__ int list_of_slot(const PlanView& pv, int slot) {
+  int lo = 0, hi = pv.n_lists;  // list_indptr[lo] <= slot < list_indptr[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (pv.list_indptr[mid] <= slot) lo = mid;
+    else hi = mid;
   }
+  return lo;
+}
+
+template <typename TO, int D>
+__device__ __forceinline__ void fused_contraction(const AttnParams& p, const PlanView& pv, int slot, int tid, int nthr,
+                                                  int bar_id, volatile int* s_flag) {
+  __threadfence();  // this thread's partial writes are visible device-wide
+  asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");
+  if (tid == 0) {
+    const int l = list_of_slot(pv, slot);
+    const int len = pv.list_indptr[l + 1] - pv.list_indptr[l];
+    const int old = atomicAdd(p.counters + l, 1);
+    const bool last = old == len - 1;
+    if (last) p.counters[l] = 0;  // every other arrival of this launch has happened
+    *s_flag = last ? l : -1;
+  }
+  asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");
+  const int l = *s_flag;
+  if (l >= 0) {
+    __threadfence();  // acquire: the other CTAs' partials are visible
+    const int req = pv.list_req[l], kvh = pv.list_kvh[l], qt = pv.list_qtile[l];
+    const int lq = pv.req_qo_len[req];
+    const int nrows = min(pv.T_q, lq * p.g - qt * pv.T_q);
+    const int s0 = pv.list_indptr[l], s1 = pv.list_indptr[l + 1];
+    for (int e = tid; e < nrows * D; e += nthr) {
+      const int r = e / D, dd = e % D;
+      float acc = 0.f, acc_l = -INFINITY;
+      for (int s = s0; s < s1; ++s) {
+        const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
+        const float ls = __ldcg(p.part_lse + prow);
+        const float os = __ldcg(p.part_o + prow * D + dd);
+        const float mx = fmaxf(acc_l, ls);
+        if (mx == -INFINITY) continue;
+        const float wa = __expf(acc_l - mx), wb = __expf(ls - mx);
+        acc = (wa * acc + wb * os) / (wa + wb);
+        acc_l = mx + __logf(wa + wb);
+      }
+      const int f = qt * pv.T_q + r;
+      const int tok = f / p.g, head = kvh * p.g + f % p.g;
+      const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
+      if (p.o_f32) reinterpret_cast<float*>(p.o)[orow * D + dd] = acc;
+      else reinterpret_cast<TO*>(p.o)[orow * D + dd] = from_float<TO>(acc);
+      if (p.lse && dd == 0) p.lse[orow] = acc_l;
+    }
+  }
+  asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");  // s_flag reuse
 }
 
 template <typename TI, typename TO, int D>

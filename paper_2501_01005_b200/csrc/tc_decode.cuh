@@ -25,6 +25,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "merge.cuh"
 #include "ptx.cuh"
 
 namespace bsra {
@@ -411,6 +412,11 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
             if (row == 0) p.part_lse[prow] = lse;
           }
         }
+      }
+      if (d.slot >= 0) {  // split item: the CTA completing its merge list folds it (fused contraction)
+        volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+        if (tp.f16) fused_contraction<__half, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
+        else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
       }
       ptx::named_bar_sync(1, 128);  // red2 reuse; TMEM reads done before the next item's MMAs
     }

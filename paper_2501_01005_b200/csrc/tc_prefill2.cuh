@@ -574,6 +574,11 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         if (d.slot >= 0) p.part_lse[prow] = lse;
         else if (p.lse) p.lse[orow] = lse;
       }
+      if (d.slot >= 0) {  // split item: the WG completing its merge list folds it (fused contraction)
+        volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1 + w);
+        if (tp.f16) fused_contraction<__half, 128>(p, pv, d.slot, r, 128, 2 + w, s_flag);
+        else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, r, 128, 2 + w, s_flag);
+      }
       ptx::tc_fence_before();  // O_w reads done before this WG's next p_ready (next item's PV)
     }
   }
