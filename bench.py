@@ -465,6 +465,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-composable", action="store_true")
     ap.add_argument("--no-long", action="store_true")
+    ap.add_argument("--no-pdl", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
@@ -479,7 +480,8 @@ def main():
     # ---- configs[1]: batched paged decode, Llama-3-8B heads, batch 128 per rank
     wl = synth.c2_decode_llama8b()
     L = Layered(wl, args.layers, dev, seed_base=1000 * rank)
-    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel)
+    # consecutive layers are independent -> programmatic dependent launch between them
+    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel, pdl=not args.no_pdl)
     by = decode_bytes(wl)
     s, one_step, launches_per_step = time_device_steps(L, eng, args.steps, args.warmup, not args.no_graph)
     clk = ClockSampler(local)

@@ -69,8 +69,16 @@ typedef struct {
   int32_t kv_chunk_align;    /* chunk boundaries aligned to this many tokens; 0 => page_size  */
   int32_t kv_chunk_min;      /* floor for the chunk size L_kv; 0 => none                        */
   int32_t kernel;            /* bsra_kernel                                                     */
-  int32_t reserved[7];       /* must be zero                                                    */
+  int32_t flags;             /* BSRA_FLAG_* bits                                                */
+  int32_t reserved[6];       /* must be zero                                                    */
 } bsra_config;
+
+/* flags: BSRA_FLAG_PDL launches the tcgen05 kernels with programmatic dependent launch: a run()
+ * may start streaming K/V while the previous kernel on the stream drains, and waits for it
+ * (griddepcontrol.wait) before writing o / lse / workspace. Only valid when the inputs of a
+ * run() (q, pools, indices, mask) are NOT produced by the kernel immediately preceding it on
+ * the stream — e.g. consecutive layers' attention captured back to back. */
+#define BSRA_FLAG_PDL 1
 
 typedef struct bsra_engine bsra_engine;
 

@@ -36,7 +36,11 @@ class Config(ctypes.Structure):
                 ("mask", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("max_total_qo_rows", ctypes.c_int32),
                 ("num_ctas", ctypes.c_int32), ("tile_set_mask", ctypes.c_int32), ("tile_q", ctypes.c_int32),
                 ("cost_alpha", ctypes.c_int64), ("cost_beta", ctypes.c_int64), ("kv_chunk_align", ctypes.c_int32),
-                ("kv_chunk_min", ctypes.c_int32), ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("kv_chunk_min", ctypes.c_int32), ("kernel", ctypes.c_int32), ("flags", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 6)]
+
+
+FLAG_PDL = 1  # BSRA_FLAG_PDL (include/bsra.h)
 
 
 _lib = None
@@ -102,8 +106,9 @@ def _i32(a) -> np.ndarray:
 
 def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="none", max_batch=1,
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128), tile_q=0, alpha=1, beta=1,
-                kv_chunk_align=0, kv_chunk_min=0, kernel="auto") -> Config:
+                kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False) -> Config:
     c = Config()
+    c.flags = FLAG_PDL if pdl else 0
     c.num_qo_heads, c.num_kv_heads, c.head_dim, c.page_size = H_qo, H_kv, D, page_size
     c.dtype = DTYPE[dtype] if isinstance(dtype, str) else dtype
     od = o_dtype if o_dtype is not None else dtype

@@ -64,7 +64,8 @@ bsra_status validate_config(const bsra_config& c) {
   if (c.cost_alpha < 0 || c.cost_beta < 0) return fail(BSRA_EINVAL, "negative cost parameters");
   if (c.kv_chunk_align < 0 || c.kv_chunk_min < 0) return fail(BSRA_EINVAL, "negative chunk parameters");
   if (c.kernel < BSRA_KERNEL_AUTO || c.kernel > BSRA_KERNEL_TC) return fail(BSRA_EINVAL, "bad kernel selector");
-  for (int i = 0; i < 7; ++i)
+  if (c.flags & ~BSRA_FLAG_PDL) return fail(BSRA_EINVAL, "unknown flag bits");
+  for (int i = 0; i < 6; ++i)
     if (c.reserved[i]) return fail(BSRA_EINVAL, "reserved fields must be zero");
   return BSRA_OK;
 }
@@ -365,6 +366,7 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
     tl.page_size = c.page_size;
     tl.max_qo = e->max_qo;
     tl.mask = c.mask;
+    tl.pdl = (c.flags & BSRA_FLAG_PDL) != 0;
     const char* why = "";
     int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
     if (rc < 0)

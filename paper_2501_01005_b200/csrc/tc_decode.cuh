@@ -38,7 +38,29 @@ struct TcParams {
   int32_t box_tok;  // min(page_size, 128)
   int32_t q_hb, q_tb;
   int32_t f16;      // 1 = fp16 inputs, 0 = bf16
+  int32_t pdl;      // launched with programmatic dependent launch (host-side launch choice)
 };
+
+// Kernel launch honouring TcParams::pdl (cudaLaunchAttributeProgrammaticStreamSerialization).
+template <typename Kern>
+inline cudaError_t launch_tc(Kern kernel, int grid, int threads, int smem, cudaStream_t st, const TcParams& tp) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = tp.pdl ? attr : nullptr;
+  cfg.numAttrs = tp.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, tp);
+}
+
+// PDL device side: let the next kernel on the stream start launching, and before this kernel's
+// first global write wait for the previous kernel to complete (no-ops without PDL).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 namespace dec {
 constexpr int kTile = 128;         // tokens per KV tile (= MMA M)
@@ -128,6 +150,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();  // PDL: the next kernel's CTAs may take SMs this grid releases
 
   if (warp == 0) {
     // ============================ TMA producer ============================
@@ -375,6 +398,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       wait_pv(1);
       if (ct == 0) ptx::mbar_arrive(&empty_q[qb]);
       qb ^= 1;
+      pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
       // ---- epilogue: denominators (sum over the 128 token lanes), normalise, write
       float ov[kC];
       if (d.ntiles > 0) {

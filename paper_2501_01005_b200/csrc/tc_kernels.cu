@@ -65,8 +65,7 @@ cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  tc_decode_kernel<kC, kMask><<<grid, dec::kThreads, dec::kSmemBytes, st>>>(tp);
-  return cudaGetLastError();
+  return launch_tc(tc_decode_kernel<kC, kMask>, grid, dec::kThreads, dec::kSmemBytes, st, tp);
 }
 
 template <int kC>
@@ -113,6 +112,7 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     tp.q_hb = g <= 16 ? g : 16;
     tp.q_tb = g <= 16 ? 16 / g : 1;
     tp.f16 = L.f16;
+    tp.pdl = L.pdl;
     if (!make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) ||
         !make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, ps, p.ks0, p.ks1, p.ks2, B) ||
         !make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, ps, p.vs0, p.vs1, p.vs2, B)) {

@@ -15,6 +15,7 @@ struct TcLaunch {
   int page_size = 0;
   int max_qo = 0;          // max l_qo of the current plan (live fused columns)
   int mask = 0;
+  bool pdl = false;        // programmatic dependent launch (BSRA_FLAG_PDL)
 };
 
 // Launches the tcgen05 kernel for this plan if one applies (bf16/f16, D = 128, supported page

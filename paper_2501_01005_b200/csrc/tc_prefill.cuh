@@ -459,6 +459,7 @@ inline int tc_prefill_launch(const AttnParams& p, const TcLaunch& L, cudaStream_
   tp.q_hb = g;
   tp.q_tb = 128 / g;
   tp.f16 = L.f16;
+  tp.pdl = L.pdl;
   if (!make_q_map_ext(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) ||
       !make_pool_map_ext(&tp.tk, p.k, L.f16, p.H_kv, L.page_size, p.ks0, p.ks1, p.ks2, B) ||
       !make_pool_map_ext(&tp.tv, p.v, L.f16, p.H_kv, L.page_size, p.vs0, p.vs1, p.vs2, B)) {

@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();  // PDL: the next kernel's CTAs may take SMs this grid releases
   const int B = tp.box_tok;
   const int ps = p.page_size;
   // debug trace (CTA 0): trace[ev * 1024 + i] = clock64() of the i-th event of kind ev
@@ -522,6 +523,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         if (r == 0) BSRA_TRACE(6 + 2 * w, tcount);
         ++tcount;
       }
+      pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
       // ---- epilogue: wait for the item's last PV, normalise, write
       if (d.ntiles > 0) {
         ptx::mbar_wait(&bar_o[w], oph);
@@ -598,8 +600,7 @@ inline cudaError_t launch_prefill2_t(const TcParams& tp, int grid, cudaStream_t 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  tc_prefill2_kernel<kMask><<<grid, pre2::kThreads, pre2::kSmemBytes, st>>>(tp);
-  return cudaGetLastError();
+  return launch_tc(tc_prefill2_kernel<kMask>, grid, pre2::kThreads, pre2::kSmemBytes, st, tp);
 }
 
 }  // namespace bsra

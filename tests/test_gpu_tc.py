@@ -174,3 +174,39 @@ def test_tc_prefill_deterministic(cuda_device):
     a = run_gpu(inp, eng)
     b = run_gpu(inp, eng)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("tile_q", [16, 128])
+def test_tc_pdl_back_to_back_layers(cuda_device, tile_q):
+    """BSRA_FLAG_PDL: consecutive independent layers captured in one graph overlap their
+    launches; every layer still matches the oracle, including split items (fused contraction
+    with the shared workspace across layers)."""
+    import torch
+    import paper_2501_01005_b200 as bsra
+    wl = synth.Workload("pdl", 32, 8, 128, 16, "bf16", "causal" if tile_q == 128 else "none",
+                        np.array([1, 1, 1] if tile_q == 16 else [100, 200, 300], np.int32),
+                        np.array([5000, 300, 77] if tile_q == 16 else [100, 2000, 300], np.int32))
+    layers = [synth.make_inputs(wl, device=cuda_device, seed_base=10 * r) for r in range(4)]
+    for inp in layers[1:]:
+        inp.kv_page_indices = layers[0].kv_page_indices
+    cfg = bsra.make_config(H_qo=32, H_kv=8, D=128, page_size=16, dtype="bf16", mask=wl.mask, max_batch=3,
+                           max_total_qo_rows=int(wl.qo_lens.sum()), num_ctas=148, tile_q=tile_q, pdl=True)
+    eng = bsra.Engine(cfg, 0)
+    i0 = layers[0]
+    eng.plan(i0.qo_indptr, i0.kv_page_indptr, i0.kv_last_page_len, i0.sm_scale)
+    nq = int(i0.qo_indptr[-1])
+    outs = [(torch.empty((nq, 32, 128), device=cuda_device, dtype=torch.bfloat16),
+             torch.empty((nq, 32), device=cuda_device)) for _ in layers]
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for inp, (o, l) in zip(layers, outs):
+            eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, i0.kv_page_indices, o, l, stream=s)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    for inp, (o, l) in zip(layers, outs):
+        inp.kv_page_indices = i0.kv_page_indices
+        assert_close((o.float().cpu().numpy(), l.cpu().numpy()), oracle.attention_from_inputs(inp), "bf16",
+                     what="pdl layer")
