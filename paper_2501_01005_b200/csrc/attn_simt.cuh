@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
         }
       }
     }
-    if (slot >= 0) {  // split item: the CTA completing its merge list folds it (fused contraction)
+    if (slot >= 0 && p.fused_merge) {  // split item: the CTA completing its merge list folds it
       __shared__ int s_flag;
       fused_contraction<T, D>(p, pv, slot, threadIdx.x, blockDim.x, 0, &s_flag);
     }

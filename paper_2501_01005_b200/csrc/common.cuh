@@ -28,6 +28,7 @@ struct AttnParams {
   float* part_lse;  // [slots][T_slot]
   int32_t* counters;  // per-merge-list arrival counters (fused contraction)
   long long* trace;   // optional pipeline trace (CTA 0 event clocks), NULL in production
+  int32_t fused_merge;  // 1: split items are merged in-kernel (decode engines); 0: contraction kernel
   int32_t H_qo, H_kv, g, page_size, mask_mode, o_f32, T_slot, D;
   float scale_log2;  // sm_scale * log2(e)
 };

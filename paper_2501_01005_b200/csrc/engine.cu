@@ -298,6 +298,18 @@ bsra_status launch_simt_d(const bsra::AttnParams& p, int D, int grid, cudaStream
   return D == 64 ? launch_simt<T, 64>(p, grid, st) : launch_simt<T, 128>(p, grid, st);
 }
 
+template <typename TO, int D>
+bsra_status launch_contraction_t(const bsra::AttnParams& p, int grid, cudaStream_t st) {
+  bsra::contraction_kernel<TO, D><<<grid, 256, 0, st>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  return BSRA_OK;
+}
+
+template <typename TO>
+bsra_status launch_contraction_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st) {
+  return D == 64 ? launch_contraction_t<TO, 64>(p, grid, st) : launch_contraction_t<TO, 128>(p, grid, st);
+}
+
 }  // namespace
 
 bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const void* v_pool, const int64_t* k_strides,
@@ -341,6 +353,10 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
   p.part_lse = reinterpret_cast<float*>(e->ws + e->lay.off_part_lse);
   p.counters = reinterpret_cast<int32_t*>(e->ws + e->lay.off_counters);
   p.trace = e->trace;
+  // Contraction placement, fixed per engine so a captured graph is valid for every re-plan:
+  // decode engines (tiles of <= 16 rows) merge split items in-kernel (the CTA completing a list
+  // folds it); engines that can emit 64/128-row tiles use the wide contraction kernel.
+  p.fused_merge = e->lay.T_max <= 16 ? 1 : 0;
   p.H_qo = c.num_qo_heads;
   p.H_kv = c.num_kv_heads;
   p.g = c.num_qo_heads / c.num_kv_heads;
@@ -384,8 +400,15 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
     }
     if (s) return s;
   }
-  // the contraction runs inside the persistent kernel (merge.cuh:fused_contraction)
   e->last_launches = 1;
+  if (!p.fused_merge) {  // contraction stage: fixed grid, exits at once if nothing split
+    const int cgrid = std::max(1, std::min(grid, 2 * 148));
+    if (c.o_dtype == BSRA_F32 || c.dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
+    else if (c.dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
+    else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
+    if (s) return s;
+    e->last_launches = 2;
+  }
   return BSRA_OK;
 }
 

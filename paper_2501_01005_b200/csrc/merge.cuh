@@ -78,28 +78,92 @@ __device__ __forceinline__ void fused_contraction(const AttnParams& p, const Pla
     const int lq = pv.req_qo_len[req];
     const int nrows = min(pv.T_q, lq * p.g - qt * pv.T_q);
     const int s0 = pv.list_indptr[l], s1 = pv.list_indptr[l + 1];
-    for (int e = tid; e < nrows * D; e += nthr) {
-      const int r = e / D, dd = e % D;
-      float acc = 0.f, acc_l = -INFINITY;
-      for (int s = s0; s < s1; ++s) {
-        const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
-        const float ls = __ldcg(p.part_lse + prow);
-        const float os = __ldcg(p.part_o + prow * D + dd);
-        const float mx = fmaxf(acc_l, ls);
-        if (mx == -INFINITY) continue;
-        const float wa = __expf(acc_l - mx), wb = __expf(ls - mx);
-        acc = (wa * acc + wb * os) / (wa + wb);
-        acc_l = mx + __logf(wa + wb);
+    // ⊕ over the list in closed form (max-shifted): per row one warp forms the slot weights
+    // w_s = e^{lse_s - m} once, then lanes accumulate D/32 contiguous dims per slot in slot order.
+    constexpr int kPer = D / 32;
+    const int lane = tid & 31, nwarps = nthr >> 5;
+    for (int r = tid >> 5; r < nrows; r += nwarps) {
+      float m = -INFINITY;
+      for (int s = s0 + lane; s < s1; s += 32)
+        m = fmaxf(m, __ldcg(p.part_lse + (int64_t)pv.list_slot[s] * p.T_slot + r));
+      m = warp_max(m);
+      float acc[kPer];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) acc[j] = 0.f;
+      float tot = 0.f;
+      if (m != -INFINITY) {
+        for (int s = s0; s < s1; ++s) {
+          const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
+          const float w = __expf(__ldcg(p.part_lse + prow) - m);  // 0 for an empty partial
+          tot += w;
+          if constexpr (kPer % 4 == 0) {
+            const float4* src = reinterpret_cast<const float4*>(p.part_o + prow * D + lane * kPer);
+#pragma unroll
+            for (int j = 0; j < kPer / 4; ++j) {
+              const float4 v = __ldcg(src + j);
+              acc[4 * j] = fmaf(w, v.x, acc[4 * j]);
+              acc[4 * j + 1] = fmaf(w, v.y, acc[4 * j + 1]);
+              acc[4 * j + 2] = fmaf(w, v.z, acc[4 * j + 2]);
+              acc[4 * j + 3] = fmaf(w, v.w, acc[4 * j + 3]);
+            }
+          } else {
+            const float* src = p.part_o + prow * D + lane * kPer;
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) acc[j] = fmaf(w, __ldcg(src + j), acc[j]);
+          }
+        }
       }
+      const float inv = tot > 0.f ? 1.f / tot : 0.f;
+      const float lse = tot > 0.f ? m + __logf(tot) : -INFINITY;
       const int f = qt * pv.T_q + r;
       const int tok = f / p.g, head = kvh * p.g + f % p.g;
       const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
-      if (p.o_f32) reinterpret_cast<float*>(p.o)[orow * D + dd] = acc;
-      else reinterpret_cast<TO*>(p.o)[orow * D + dd] = from_float<TO>(acc);
-      if (p.lse && dd == 0) p.lse[orow] = acc_l;
+      if (p.o_f32) {
+        float* dst = reinterpret_cast<float*>(p.o) + orow * D + lane * kPer;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) dst[j] = acc[j] * inv;
+      } else {
+        TO* dst = reinterpret_cast<TO*>(p.o) + orow * D + lane * kPer;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) dst[j] = from_float<TO>(acc[j] * inv);
+      }
+      if (p.lse && lane == 0) p.lse[orow] = lse;
     }
   }
   asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");  // s_flag reuse
+}
+
+// Standalone contraction (engines whose tiles can be 64/128 rows, where a merge list is too big
+// for the one CTA that completes it): one warp per (list, row), left fold in plan order.
+template <typename TO, int D>
+__global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant__ AttnParams p) {
+  constexpr int kPer = D / 32;
+  const PlanView pv = load_plan(p.plan);
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t total = (int64_t)pv.n_lists * pv.T_q;
+  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += nwarps) {
+    const int li = (int)(w / pv.T_q), r = (int)(w % pv.T_q);
+    const int req = pv.list_req[li], kvh = pv.list_kvh[li], qt = pv.list_qtile[li];
+    const int lq = pv.req_qo_len[req];
+    const int f = qt * pv.T_q + r;
+    if (f >= lq * p.g) continue;
+    const int tok = f / p.g, head = kvh * p.g + f % p.g;
+    float acc[kPer], acc_lse = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) acc[j] = 0.f;
+    for (int s = pv.list_indptr[li]; s < pv.list_indptr[li + 1]; ++s) {
+      const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
+      float o[kPer];
+      const float* src = p.part_o + prow * D + lane * kPer;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) o[j] = src[j];
+      oplus<kPer>(acc, acc_lse, o, p.part_lse[prow]);
+    }
+    const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
+    store_row<TO, D>(p.o, orow, lane, acc, p.o_f32);
+    if (p.lse && lane == 0) p.lse[orow] = acc_lse;
+  }
 }
 
 template <typename TI, typename TO, int D>

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           }
         }
       }
-      if (d.slot >= 0) {  // split item: the CTA completing its merge list folds it (fused contraction)
+      if (d.slot >= 0 && p.fused_merge) {  // split item: the CTA completing its merge list folds it
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
         if (tp.f16) fused_contraction<__half, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
         else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, ct, 128, 1, s_flag);

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
           if (row_ok) p.part_lse[prow] = lse;
         }
       }
-      if (d.slot >= 0) {  // split item: fused contraction (see merge.cuh)
+      if (d.slot >= 0 && p.fused_merge) {  // split item: fused contraction (see merge.cuh)
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
         if (tp.f16) fused_contraction<__half, 128>(p, pv, d.slot, r, 128, 1, s_flag);
         else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, r, 128, 1, s_flag);

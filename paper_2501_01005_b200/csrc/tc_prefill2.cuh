@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         if (d.slot >= 0) p.part_lse[prow] = lse;
         else if (p.lse) p.lse[orow] = lse;
       }
-      if (d.slot >= 0) {  // split item: the WG completing its merge list folds it (fused contraction)
+      if (d.slot >= 0 && p.fused_merge) {  // split item: the WG completing its merge list folds it
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1 + w);
         if (tp.f16) fused_contraction<__half, 128>(p, pv, d.slot, r, 128, 2 + w, s_flag);
         else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, r, 128, 2 + w, s_flag);
