@@ -501,13 +501,21 @@ def main():
     step_bytes = by["total"] * args.layers
     value = world * step_bytes / (ms * 1e-3) / 1e12
 
-    # ---- roofline of the dominant launch (run(): attention + contraction), CUDA events per launch
+    # ---- roofline of the dominant launch: one run() = one persistent tc_decode launch (the
+    # contraction is fused in-kernel for decode engines); CUDA events around each launch
     launch_ms = per_launch_ms(L, eng)
     achieved = by["total"] / (launch_ms * 1e-3) / 1e9
+    traffic = None
+    try:  # DRAM read+write per launch from the committed ncu --set full capture of this kernel
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            traffic = json.load(f)["tc_decode_kernel<4,0>"]["traffic_bytes"]
+    except Exception:
+        pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_kind": pk_kind,
-            "kernel": f"bsra attention ({eng.selected_kernel()}) + contraction, per run() launch pair",
-            "algorithmic_bytes_per_launch": by["total"], "launch_ms": launch_ms}
+            "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_kind": pk_kind,
+            "kernel": f"bsra {eng.selected_kernel()} (one launch per run(), contraction fused)",
+            "algorithmic_bytes_per_launch": by["total"], "launch_ms": launch_ms,
+            "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, one launch)"}
 
     # ---- e2e through the public API with host buffers
     e2e = None
