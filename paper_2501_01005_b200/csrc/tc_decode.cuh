@@ -39,6 +39,7 @@ struct TcParams {
   int32_t q_hb, q_tb;
   int32_t f16;      // 1 = fp16 inputs, 0 = bf16
   int32_t pdl;      // launched with programmatic dependent launch (host-side launch choice)
+  int32_t dbg;      // timing experiments only ($BSRA_DEBUG_PREFILL): 1 skip softmax, 2 skip MMAs, 4 one WG
 };
 
 // Kernel launch honouring TcParams::pdl (cudaLaunchAttributeProgrammaticStreamSerialization).

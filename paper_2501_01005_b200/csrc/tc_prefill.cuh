@@ -460,6 +460,8 @@ inline int tc_prefill_launch(const AttnParams& p, const TcLaunch& L, cudaStream_
   tp.q_tb = 128 / g;
   tp.f16 = L.f16;
   tp.pdl = L.pdl;
+  static const int dbg = getenv("BSRA_DEBUG_PREFILL") ? atoi(getenv("BSRA_DEBUG_PREFILL")) : 0;
+  tp.dbg = dbg;  // timing experiments only (never set in tests / bench)
   if (!make_q_map_ext(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) ||
       !make_pool_map_ext(&tp.tk, p.k, L.f16, p.H_kv, L.page_size, p.ks0, p.ks1, p.ks2, B) ||
       !make_pool_map_ext(&tp.tv, p.v, L.f16, p.H_kv, L.page_size, p.vs0, p.vs1, p.vs2, B)) {

@@ -57,12 +57,13 @@ static_assert(sizeof(TileDesc) == 96, "TileDesc layout");
 
 // Walks one WG's item stream (queue positions it0+w, it0+w+2, ...) tile by tile.
 struct ItemStream {
-  int it, it1;
+  int it, it1, stride;
   int ti;
   DecItem d;
-  __device__ __forceinline__ void init(const PlanView& pv, int g, int first, int end) {
+  __device__ __forceinline__ void init(const PlanView& pv, int g, int first, int end, int step) {
     it = first;
     it1 = end;
+    stride = step;
     ti = 0;
     skip_empty(pv, g);
   }
@@ -70,25 +71,26 @@ struct ItemStream {
     while (it < it1) {
       d = dec_item(pv, it, g);
       if (d.ntiles > 0) return;
-      it += 2;
+      it += stride;
     }
   }
   __device__ __forceinline__ bool alive() const { return it < it1; }
   __device__ __forceinline__ void advance(const PlanView& pv, int g) {
     if (++ti < d.ntiles) return;
     ti = 0;
-    it += 2;
+    it += stride;
     skip_empty(pv, g);
   }
 };
 
 // Deterministic interleave of the two streams: alternate while both are alive.
+// (nstream = 1 only in the one-WG timing experiment: stream 1 is empty.)
 struct Interleave {
   ItemStream s0, s1;
   int turn = 0;
-  __device__ __forceinline__ void init(const PlanView& pv, int g, int it0, int it1) {
-    s0.init(pv, g, it0, it1);
-    s1.init(pv, g, it0 + 1, it1);
+  __device__ __forceinline__ void init(const PlanView& pv, int g, int it0, int it1, int nstream = 2) {
+    s0.init(pv, g, it0, it1, nstream);
+    s1.init(pv, g, nstream == 2 ? it0 + 1 : it1, it1, nstream);
     turn = 0;
   }
   __device__ __forceinline__ int pick() const {  // -1 when both exhausted
@@ -160,6 +162,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();  // PDL: the next kernel's CTAs may take SMs this grid releases
   const int B = tp.box_tok;
+  const int nstream = (tp.dbg & 4) ? 1 : 2;  // 2 softmax WGs (1 only in a timing experiment)
   const int ps = p.page_size;
   // debug trace (CTA 0): trace[ev * 1024 + i] = clock64() of the i-th event of kind ev
   long long* const trace = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
@@ -170,7 +173,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   if (warp == 3) {
     // ===================== scheduler: interleaved tile descriptors =====================
     Interleave il;
-    il.init(pv, g, it0, it1);
+    il.init(pv, g, it0, it1, nstream);
     const int spp = kTile / B;             // sub-blocks of a full tile (<= 16)
     const int G = min(4, 32 / spp);        // positions per batched index load
     int pos = 0;
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         if (kq == k) D.page[j] = page;
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&desc_full[slot]);
+        if (lane == 0) BSRA_TRACE(10, pos);
         ++pos;
       }
     }
@@ -273,7 +277,9 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       const int kvh = D.kvh, t0 = D.t0, n = D.n;
       const int nsub = (n + B - 1) / B;
       const int page = lane < nsub ? D.page[lane] : 0;
-      const int off = (t0 + lane * B) % ps;
+      // tiles start page-aligned (chunk alignment is a multiple of B), so sub-blocks of pages
+      // <= 128 tokens start at slot 0; only pages > 128 tokens need the in-page offset
+      const int off = ps <= kTile ? 0 : (t0 + lane * B) % ps;
       if (isK && (D.flags & 1) && lane == 0) {  // Q of WG w's next item
         ptx::mbar_wait(&empty_q[w], qphase[w]);
         ptx::mbar_arrive_expect_tx(&full_q[w], kOp);
@@ -294,6 +300,11 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         if (lane == 0) BSRA_TRACE(isK ? 0 : 1, pos);
         ptx::tma_load_4d(dst, tm, &fullx[stage], 0, kvh, off, page);
         ptx::tma_load_4d(dst + kHalf, tm, &fullx[stage], 64, kvh, off, page);
+      }
+      __syncwarp();
+      if ((tp.dbg & 8) && lane == 0) {  // timing experiment: TMA issue -> landed latency
+        ptx::mbar_wait(&fullx[stage], ephase ^ 1);
+        BSRA_TRACE(isK ? 15 : 14, pos);
       }
       __syncwarp();
       if (++stage == nst) {
@@ -347,7 +358,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t step = (uint64_t)((kk >> 2) * (kHalf >> 4) + (kk & 3) * 2);
-            ptx::mma_f16_ss_warp(dS, a0 + step, b0 + step, idS, kk > 0);
+            if (!(tp.dbg & 2)) ptx::mma_f16_ss_warp(dS, a0 + step, b0 + step, idS, kk > 0);
           }
         }
         ptx::mma_commit_warp(&empty_k[kst]);
@@ -389,7 +400,8 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         const uint32_t dO = tmem + 256 + w * 128, aP = tmem + w * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // +128 (2 KB = 16 tokens) per K step of the MN-major V
-          ptx::mma_f16_ts_warp(dO, aP + kk * 8, b0 + (uint64_t)(kk * 128), idO, ((flags & 1) && kk == 0) ? 0u : 1u);
+          if (!(tp.dbg & 2))
+            ptx::mma_f16_ts_warp(dO, aP + kk * 8, b0 + (uint64_t)(kk * 128), idO, ((flags & 1) && kk == 0) ? 0u : 1u);
       }
       ptx::mma_commit_warp(&empty_v[vst]);
       if (flags & 2) ptx::mma_commit_warp(&bar_o[w]);
@@ -412,7 +424,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
     const float sc = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     int tcount = 0;
-    for (int it = it0 + w; it < it1; it += 2) {
+    for (int it = it0 + w; w < nstream && it < it1; it += nstream) {
       const DecItem d = dec_item(pv, it, g);
       const bool row_ok = r < d.nrows;
       const int f = d.row0 + r;
@@ -430,6 +442,12 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         sph ^= 1;
         if (r == 0) BSRA_TRACE(5 + 2 * w, tcount);
         ptx::tc_fence_after();
+        if (tp.dbg & 1) {  // timing experiment: no softmax work (results are garbage)
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&p_ready[w]);
+          ++tcount;
+          continue;
+        }
         // ---- pass 1: raw row max (two 32-column TMEM loads in flight per round trip)
         float mx = -INFINITY;
 #pragma unroll
