@@ -462,6 +462,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prefill", action="store_true")
+    ap.add_argument("--prefill-tile", type=int, default=0, help="force T_q for the prefill line (0 = heuristic)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-composable", action="store_true")
     ap.add_argument("--no-long", action="store_true")
@@ -532,13 +533,13 @@ def main():
         torch.cuda.empty_cache()
         wl3 = synth.c3_prefill_llama70b()
         L3 = Layered(wl3, 2, dev, seed_base=1000 * rank)
-        e3 = L3.engine(num_ctas=148, kernel=args.kernel)
+        e3 = L3.engine(num_ctas=148, kernel=args.kernel, tile_q=args.prefill_tile)
         p_ms = per_launch_ms(L3, e3, reps=3)
         fl = causal_flops(wl3)
         tf = fl / (p_ms * 1e-3) / 1e12
         prefill = {"value": tf, "unit": "TFLOP/s", "workload": "c3_prefill_llama70b (configs[2])",
                    "ms_per_layer": p_ms, "frac": tf / pk["bf16_tflops"], "peak": pk["bf16_tflops"],
-                   "kernel": e3.selected_kernel(), "flops_per_layer": fl}
+                   "kernel": e3.selected_kernel(), "tile_q": int(e3.export_plan()[3]), "flops_per_layer": fl}
         del L3
         torch.cuda.empty_cache()
 

@@ -62,8 +62,10 @@ typedef struct {
   int32_t max_batch;         /* scheduler-metadata bounds supplied up front (App. D.3) */
   int32_t max_total_qo_rows; /* bound on sum_i l_qo(i)                                          */
   int32_t num_ctas;          /* persistent grid size; 0 => 2 x #SM when T_q = 16, else #SM     */
-  int32_t tile_set_mask;     /* allowed query tiles T_q: bit0=16, bit1=64, bit2=128; 0 => all */
-  int32_t tile_q;            /* 0 => heuristic of §3.2.2; else forced T_q in {16,64,128} */
+  int32_t tile_set_mask;     /* allowed query tiles T_q: bit0=16, bit1=64, bit2=128, bit3=256
+                                (256 = two 128-row MMA tiles sharing each K/V tile, R20);
+                                0 => all */
+  int32_t tile_q;            /* 0 => heuristic of §3.2.2; else forced T_q in {16,64,128,256} */
   int64_t cost_alpha;        /* Algorithm 1 cost(l_q, l_kv) = alpha*l_q + beta*l_kv     */
   int64_t cost_beta;         /*   0 => 1                                                        */
   int32_t kv_chunk_align;    /* chunk boundaries aligned to this many tokens; 0 => page_size  */
@@ -124,7 +126,8 @@ bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, c
  *   kv_page_indices  [nnz] device int32: BSR `indices` (page ids); not validated (caller contract)
  *   custom_mask      MASK_CUSTOM: device uint8 bits (see bsra_mask); else NULL
  *   mask_bit_indptr  MASK_CUSTOM: device int64 [batch+1] bit offsets; else NULL
- *   o                [sum l_qo, H_qo, D] device, cfg->o_dtype
+ *   o                [sum l_qo, H_qo, D] device, cfg->o_dtype, 32-byte aligned (the kernels
+ *                    write whole 32-byte sectors of a row with 256-bit stores)
  *   lse              [sum l_qo, H_qo] device fp32, natural log (R2); NULL => not written
  * batch = 0 (or no rows) is a no-op that still launches the fixed kernels (graph stability). */
 bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const void* v_pool,

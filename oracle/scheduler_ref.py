@@ -36,7 +36,7 @@ def ceil_div(a: int, b: int) -> int:
     return -(-a // b)
 
 
-def select_tile(qo_lens, g, tile_set=(16, 64, 128)) -> int:
+def select_tile(qo_lens, g, tile_set=(16, 64, 128, 256)) -> int:
     """§3.2.2 heuristic, integer form: smallest T with T*B >= sum(l_qo*g)."""
     B = len(qo_lens)
     S = int(sum(int(x) for x in qo_lens)) * g
@@ -58,7 +58,7 @@ class Plan:
     image: np.ndarray
 
 
-def plan_ref(qo_lens, kv_lens, *, g, H_kv, mask=MASK_NONE, num_ctas, tile_set=(16, 64, 128),
+def plan_ref(qo_lens, kv_lens, *, g, H_kv, mask=MASK_NONE, num_ctas, tile_set=(16, 64, 128, 256),
              alpha=1, beta=1, align=1, L_min=0, T_q=None, qo_begin=None, page_begin=None) -> Plan:
     qo_lens = [int(x) for x in qo_lens]
     kv_lens = [int(x) for x in kv_lens]

@@ -23,7 +23,7 @@ MASK = {"none": 0, "causal": 1, "custom": 2}
 DTYPE = {"f32": F32, "f16": F16, "bf16": BF16}
 TORCH_DTYPE = {F32: torch.float32, F16: torch.float16, BF16: torch.bfloat16}
 KERNEL = {"auto": 0, "simt": 1, "tc": 2}
-TILE_BIT = {16: 1, 64: 2, 128: 4}
+TILE_BIT = {16: 1, 64: 2, 128: 4, 256: 8}
 
 
 class BsraError(RuntimeError):
@@ -105,7 +105,7 @@ def _i32(a) -> np.ndarray:
 
 
 def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="none", max_batch=1,
-                max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128), tile_q=0, alpha=1, beta=1,
+                max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
                 kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False) -> Config:
     c = Config()
     c.flags = FLAG_PDL if pdl else 0

@@ -46,7 +46,7 @@ struct Layout {
   size_t off_plan = 0, off_part_o = 0, off_part_lse = 0, off_counters = 0, total = 0;
 };
 
-int tile_mask_of(const bsra_config& c) { return c.tile_set_mask ? c.tile_set_mask : 7; }
+int tile_mask_of(const bsra_config& c) { return c.tile_set_mask ? c.tile_set_mask : 15; }
 
 bsra_status validate_config(const bsra_config& c) {
   if (c.num_qo_heads <= 0 || c.num_kv_heads <= 0 || c.num_qo_heads % c.num_kv_heads)
@@ -59,8 +59,9 @@ bsra_status validate_config(const bsra_config& c) {
   if (c.max_batch < 0 || c.max_total_qo_rows < 0) return fail(BSRA_EINVAL, "negative bounds");
   if (c.num_ctas < 0) return fail(BSRA_EINVAL, "num_ctas < 0");
   const int tm = tile_mask_of(c);
-  if (tm & ~7) return fail(BSRA_EINVAL, "tile_set_mask has unknown bits");
-  if (c.tile_q && c.tile_q != 16 && c.tile_q != 64 && c.tile_q != 128) return fail(BSRA_EINVAL, "tile_q not in {16,64,128}");
+  if (tm & ~15) return fail(BSRA_EINVAL, "tile_set_mask has unknown bits");
+  if (c.tile_q && c.tile_q != 16 && c.tile_q != 64 && c.tile_q != 128 && c.tile_q != 256)
+    return fail(BSRA_EINVAL, "tile_q not in {16,64,128,256}");
   if (c.cost_alpha < 0 || c.cost_beta < 0) return fail(BSRA_EINVAL, "negative cost parameters");
   if (c.kv_chunk_align < 0 || c.kv_chunk_min < 0) return fail(BSRA_EINVAL, "negative chunk parameters");
   if (c.kernel < BSRA_KERNEL_AUTO || c.kernel > BSRA_KERNEL_TC) return fail(BSRA_EINVAL, "bad kernel selector");
@@ -81,9 +82,9 @@ int32_t default_num_ctas(const bsra_config& c, int32_t sms) {
 Layout make_layout(const bsra_config& c, int32_t num_ctas) {
   Layout L;
   L.num_ctas = num_ctas;
-  const int tm = c.tile_q ? (c.tile_q == 16 ? 1 : c.tile_q == 64 ? 2 : 4) : tile_mask_of(c);
-  L.T_min = (tm & 1) ? 16 : (tm & 2) ? 64 : 128;
-  L.T_max = (tm & 4) ? 128 : (tm & 2) ? 64 : 16;
+  const int tm = c.tile_q ? (c.tile_q == 16 ? 1 : c.tile_q == 64 ? 2 : c.tile_q == 128 ? 4 : 8) : tile_mask_of(c);
+  L.T_min = (tm & 1) ? 16 : (tm & 2) ? 64 : (tm & 4) ? 128 : 256;
+  L.T_max = (tm & 8) ? 256 : (tm & 4) ? 128 : (tm & 2) ? 64 : 16;
   const int32_t g = c.num_qo_heads / c.num_kv_heads;
   L.plan_words = bsra::plan_capacity_words(num_ctas, c.num_kv_heads, g, c.max_batch, c.max_total_qo_rows, L.T_min);
   size_t off = 0;
@@ -330,8 +331,10 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
     if ((k_strides[i] * es) % 16 || (v_strides[i] * es) % 16 || k_strides[i] < 0 || v_strides[i] < 0)
       return fail(BSRA_EINVAL, "pool strides must be non-negative and 16-byte multiples");
   if (has_rows && ((reinterpret_cast<uintptr_t>(k_pool) | reinterpret_cast<uintptr_t>(v_pool) |
-                    reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(o)) % 16))
-    return fail(BSRA_EINVAL, "q, pools and o must be 16-byte aligned");
+                    reinterpret_cast<uintptr_t>(q)) % 16))
+    return fail(BSRA_EINVAL, "q and the pools must be 16-byte aligned");
+  if (has_rows && reinterpret_cast<uintptr_t>(o) % 32)
+    return fail(BSRA_EINVAL, "o must be 32-byte aligned (256-bit row stores)");
 
   bsra::AttnParams p{};
   p.plan = reinterpret_cast<const int32_t*>(e->ws + e->lay.off_plan);

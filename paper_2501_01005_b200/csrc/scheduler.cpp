@@ -49,12 +49,12 @@ std::string lengths_from_bsr(int32_t batch, const int32_t* qo_indptr, const int3
 }
 
 int32_t select_tile(const std::vector<int32_t>& qo_len, int32_t g, int32_t tile_set_mask) {
-  static const int32_t tiles[3] = {16, 64, 128};
+  static const int32_t tiles[4] = {16, 64, 128, 256};
   const int64_t B = (int64_t)qo_len.size();
   int64_t fused = 0;
   for (int32_t x : qo_len) fused += (int64_t)x * g;
   int32_t largest = 0;
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     if (!(tile_set_mask & (1 << k))) continue;
     largest = tiles[k];
     if ((int64_t)tiles[k] * B >= fused) return tiles[k];

@@ -25,7 +25,7 @@ struct SchedParams {
   int32_t H_qo = 0, H_kv = 0, page_size = 1;
   int32_t mask = 0;            // 0 none, 1 causal, 2 custom
   int32_t num_ctas = 1;
-  int32_t tile_set_mask = 7;   // bit0 = 16, bit1 = 64, bit2 = 128
+  int32_t tile_set_mask = 15;  // bit0 = 16, bit1 = 64, bit2 = 128, bit3 = 256
   int32_t tile_q = 0;          // forced tile (0 = heuristic)
   int64_t alpha = 1, beta = 1;
   int32_t align = 1;           // chunk alignment in tokens

@@ -125,7 +125,7 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     *name = "tc_decode";
     return 1;
   }
-  if (L.T_q == 64 || L.T_q == 128) {
+  if (L.T_q == 64 || L.T_q == 128 || L.T_q == 256) {
     return tc_prefill_launch(p, L, st, name, why, B);
   }
   *why = "no tcgen05 kernel for this tile";

@@ -470,7 +470,13 @@ inline int tc_prefill_launch(const AttnParams& p, const TcLaunch& L, cudaStream_
   }
   cudaError_t e;
   static const bool v1 = getenv("BSRA_PREFILL_V1") != nullptr;  // A/B against the one-warpgroup kernel
-  if (v1) {
+  if (L.T_q == 256) {  // paired: both softmax WGs on one item, every K/V tile feeds 256 rows
+    switch (L.mask) {
+      case 0: e = launch_prefill2_t<0, true>(tp, L.grid, st); break;
+      case 1: e = launch_prefill2_t<1, true>(tp, L.grid, st); break;
+      default: e = launch_prefill2_t<2, true>(tp, L.grid, st); break;
+    }
+  } else if (v1) {
     switch (L.mask) {
       case 0: e = launch_prefill_t<0>(tp, L.grid, st); break;
       case 1: e = launch_prefill_t<1>(tp, L.grid, st); break;
@@ -478,9 +484,9 @@ inline int tc_prefill_launch(const AttnParams& p, const TcLaunch& L, cudaStream_
     }
   } else {
     switch (L.mask) {
-      case 0: e = launch_prefill2_t<0>(tp, L.grid, st); break;
-      case 1: e = launch_prefill2_t<1>(tp, L.grid, st); break;
-      default: e = launch_prefill2_t<2>(tp, L.grid, st); break;
+      case 0: e = launch_prefill2_t<0, false>(tp, L.grid, st); break;
+      case 1: e = launch_prefill2_t<1, false>(tp, L.grid, st); break;
+      default: e = launch_prefill2_t<2, false>(tp, L.grid, st); break;
     }
   }
   if (e != cudaSuccess) return -1;

@@ -26,8 +26,18 @@ namespace bsra {
 
 namespace pre2 {
 constexpr int kTile = 128;
-constexpr int kKStages = 3;
-constexpr int kVStages = 2;
+// K ring depth 2 (not 3): the kernel's shared memory then stays under the 196 KB carve-out step
+// and the SM keeps ~60 KB of L1; with a third K stage (224 KB, carve-out 228 KB) the same kernel
+// measured 7 % slower (A/B on one box: 541 vs 575 us per configs[2] layer without o stores, and
+// 8 KB of unused padding alone costs the same — the ring depth itself is not the limit).
+#ifndef BSRA_PRE2_KSTAGES
+#define BSRA_PRE2_KSTAGES 2
+#endif
+constexpr int kKStages = BSRA_PRE2_KSTAGES;
+#ifndef BSRA_PRE2_VSTAGES
+#define BSRA_PRE2_VSTAGES 2
+#endif
+constexpr int kVStages = BSRA_PRE2_VSTAGES;
 constexpr int kDesc = 12;          // tile-descriptor ring
 constexpr int kHalf = 128 * 128;   // 16 KB: 128 rows x 128 B
 constexpr int kOp = 2 * kHalf;     // 32 KB operand (128 x 128 bf16, two SW128 halves)
@@ -36,7 +46,10 @@ constexpr int kOffK = 2 * kOp;
 constexpr int kOffV = kOffK + kKStages * kOp;
 constexpr int kOffBar = kOffV + kVStages * kOp;
 constexpr int kOffDesc = kOffBar + 512;
-constexpr int kSmemBytes = kOffDesc + kDesc * 96 + 1024;
+#ifndef BSRA_PRE2_PAD
+#define BSRA_PRE2_PAD 0
+#endif
+constexpr int kSmemBytes = kOffDesc + kDesc * 96 + 1024 + BSRA_PRE2_PAD;
 constexpr int kThreads = 384;  // warps 0 Q+K producer, 1 V producer, 2 MMA, 3 scheduler, 4-7 WG0, 8-11 WG1
 constexpr uint32_t kTmemCols = 512;  // S/P_w at w*128, O_w at 256 + w*128
 constexpr float kRescaleThresh = 8.f;
@@ -107,7 +120,11 @@ struct Interleave {
   }
 };
 
-template <int kMask>
+// kPair = false: T_q in {64, 128}; the two WGs run different items (two item streams).
+// kPair = true:  T_q = 256; both WGs run the same item, WG w on fused rows [128w, 128w + 128), so
+//                every K/V tile staged in smem feeds 256 query rows (half the L2->smem bytes per
+//                flop of the streamed form, which the no-compute timing mode showed to be the bound).
+template <int kMask, bool kPair, bool kF16>
 __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __grid_constant__ TcParams tp) {
   using namespace pre2;
   const AttnParams& p = tp.p;
@@ -162,13 +179,16 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();  // PDL: the next kernel's CTAs may take SMs this grid releases
   const int B = tp.box_tok;
-  const int nstream = (tp.dbg & 4) ? 1 : 2;  // 2 softmax WGs (1 only in a timing experiment)
+  // item streams: 2 (one per softmax WG); 1 when paired (both WGs on every item) or in the
+  // one-WG timing experiment
+  const int nstream = (kPair || (tp.dbg & 4)) ? 1 : 2;
   const int ps = p.page_size;
   // debug trace (CTA 0): trace[ev * 1024 + i] = clock64() of the i-th event of kind ev
   long long* const trace = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
 #define BSRA_TRACE(ev, i) \
   if (trace && (i) < 1024) trace[(ev) * 1024 + (i)] = clock64();
   if (threadIdx.x == 0) BSRA_TRACE(9, 0);
+  if (p.trace && threadIdx.x == 0) p.trace[16 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
 
   if (warp == 3) {
     // ===================== scheduler: interleaved tile descriptors =====================
@@ -253,16 +273,12 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
     // ===================== producers: warp 0 = Q + K, warp 1 = V =====================
     const bool isK = warp == 0;
     if (lane == 0) {
-      if (isK) {
-        ptx::tma_prefetch_desc(&tp.tq);
-        ptx::tma_prefetch_desc(&tp.tk);
-      } else {
-        ptx::tma_prefetch_desc(&tp.tv);
-      }
+      if (isK) ptx::tma_prefetch_desc(&tp.tq);
+      ptx::tma_prefetch_desc(isK ? &tp.tk : &tp.tv);
     }
+    uint32_t qphase = 3;  // bit w: phase of empty_q[w] to wait for (first wait passes)
     int stage = 0;
     uint32_t ephase = 1;
-    uint32_t qphase[2] = {1, 1};
     const int nst = isK ? kKStages : kVStages;
     uint64_t* fullx = isK ? full_k : full_v;
     uint64_t* emptyx = isK ? empty_k : empty_v;
@@ -272,22 +288,26 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       const int slot = pos % kDesc;
       ptx::mbar_wait(&desc_full[slot], (pos / kDesc) & 1);
       const TileDesc& D = descs[slot];
-      const int w = D.w;
-      if (w < 0) break;
+      if (D.w < 0) break;
       const int kvh = D.kvh, t0 = D.t0, n = D.n;
       const int nsub = (n + B - 1) / B;
       const int page = lane < nsub ? D.page[lane] : 0;
       // tiles start page-aligned (chunk alignment is a multiple of B), so sub-blocks of pages
       // <= 128 tokens start at slot 0; only pages > 128 tokens need the in-page offset
       const int off = ps <= kTile ? 0 : (t0 + lane * B) % ps;
-      if (isK && (D.flags & 1) && lane == 0) {  // Q of WG w's next item
-        ptx::mbar_wait(&empty_q[w], qphase[w]);
-        ptx::mbar_arrive_expect_tx(&full_q[w], kOp);
-        uint8_t* qdst = smem + kOffQ + w * kOp;
-        ptx::tma_load_3d(qdst, &tp.tq, &full_q[w], 0, D.head0, D.tok0);
-        ptx::tma_load_3d(qdst + kHalf, &tp.tq, &full_q[w], 64, D.head0, D.tok0);
+      if (isK && (D.flags & 1) && lane == 0) {  // Q of the item's WG (paired: both halves)
+        const int w = kPair ? 0 : D.w;
+        for (int h = 0; h < (kPair ? 2 : 1); ++h) {
+          const int wb = w + h;
+          ptx::mbar_wait(&empty_q[wb], (qphase >> wb) & 1);
+          ptx::mbar_arrive_expect_tx(&full_q[wb], kOp);
+          uint8_t* qdst = smem + kOffQ + wb * kOp;
+          const int tok = D.tok0 + h * (128 / g);  // rows [128h, 128h + 128): g <= 128 divides 128
+          ptx::tma_load_3d(qdst, &tp.tq, &full_q[wb], 0, D.head0, tok);
+          ptx::tma_load_3d(qdst + kHalf, &tp.tq, &full_q[wb], 64, D.head0, tok);
+        }
       }
-      if (isK && (D.flags & 1)) qphase[w] ^= 1;
+      if (isK && (D.flags & 1)) qphase ^= kPair ? 3u : (1u << D.w);
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&desc_empty[slot]);  // descriptor fields are in registers
       if (lane == 0) {
@@ -314,104 +334,180 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
     }
   } else if (warp == 2) {
     // ===================== MMA issuer =====================
-    // Two cursors over the descriptor ring: S in order (K ring), PV in order (V ring). A WG has
-    // one S buffer, so its next S is issued only after the PV of its current tile (in-order
-    // tensor pipe => no WAR hazard on TMEM).
     const uint32_t fmt = tp.f16 ? 0u : 1u;
     const uint32_t idS = ptx::idesc_f16(fmt, 128, kTile, 0, 0);  // A = Q (K-major), B = K (K-major)
     const uint32_t idO = ptx::idesc_f16(fmt, 128, 128, 0, 1);    // A = P (TMEM), B = V (MN-major)
     const uint32_t sbase = ptx::smem_u32(smem);
-    int kst = 0, vst = 0;
-    uint32_t kph = 0, vph = 0;
-    uint32_t qph[2] = {0, 0}, pph[2] = {0, 0};
-    int pending[2] = {0, 0};
-    int s_pos = 0, pv_pos = 0;
-    bool s_done = false;
-    for (;;) {
-      // ---- issue S in order while the next tile's WG is not holding its S buffer
-      while (!s_done) {
-        const int slot = s_pos % kDesc;
-        const uint32_t ph = (s_pos / kDesc) & 1;
-        if (pv_pos == s_pos) ptx::mbar_wait(&desc_full[slot], ph);
-        else if (!ptx::mbar_test_wait_warp(&desc_full[slot], ph)) break;
-        const TileDesc& D = descs[slot];
-        const int w = D.w;
-        if (w < 0) {
-          s_done = true;
-          break;
+    // S_w = Q_w K^T from K stage ks; descriptors +2 (32 B) per K step inside a 64-column atom,
+    // +1024 (16 KB) per atom
+    auto issue_s = [&](int w, int ks) {
+      const uint64_t a0 = ptx::smem_desc_sw128(sbase + kOffQ + w * kOp, 16, 1024);
+      const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffK + ks * kOp, 16, 1024);
+      const uint32_t dS = tmem + w * 128;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t step = (uint64_t)((kk >> 2) * (kHalf >> 4) + (kk & 3) * 2);
+        if (!(tp.dbg & 2)) ptx::mma_f16_ss_warp(dS, a0 + step, b0 + step, idS, kk > 0);
+      }
+    };
+    // O_w += P_w V from V stage vs; +128 (2 KB = 16 tokens) per K step of the MN-major V
+    auto issue_pv = [&](int w, int vs, bool first) {
+      const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffV + vs * kOp, kHalf, 1024);
+      const uint32_t dO = tmem + 256 + w * 128, aP = tmem + w * 128;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        if (!(tp.dbg & 2)) ptx::mma_f16_ts_warp(dO, aP + kk * 8, b0 + (uint64_t)(kk * 128), idO, (first && kk == 0) ? 0u : 1u);
+    };
+    // rows past the chunk end -> 0 in the V stage (0 * garbage could be NaN)
+    auto zero_v_tail = [&](int vs, int n) {
+      uint8_t* vS = smem + kOffV + vs * kOp;
+      for (int rr = n + lane; rr < kTile; rr += 32) {
+        uint4* v0 = reinterpret_cast<uint4*>(vS + rr * 128);
+        uint4* v1 = reinterpret_cast<uint4*>(vS + kHalf + rr * 128);
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          v0[jj] = make_uint4(0, 0, 0, 0);
+          v1[jj] = make_uint4(0, 0, 0, 0);
         }
-        if (pending[w]) break;
-        const int flags = D.flags;
-        if (flags & 1) {  // first tile of an item: its Q must have landed
-          ptx::mbar_wait(&full_q[w], qph[w]);
-          qph[w] ^= 1;
-        }
-        ptx::mbar_wait(&full_k[kst], kph);
-        if (lane == 0) BSRA_TRACE(2, s_pos);
+      }
+      ptx::fence_proxy_async();
+      __syncwarp();
+    };
+    if constexpr (kPair) {
+      // Both WGs on every tile t, issued as  S0(t) S1(t) | PV0(t) S0(t+1) PV1(t) S1(t+1) | ...
+      // S_w(t+1) overwrites the columns P_w(t) occupies, so it is issued after PV_w(t) (the tensor
+      // pipe executes one thread's MMAs in order); WG1's softmax of t overlaps PV0(t), S0(t+1).
+      int kst = 0, vst = 0;
+      uint32_t kph = 0, vph = 0, qph = 0, pph[2] = {0, 0};
+      int pos = 0;
+      const TileDesc* D = &descs[0];
+      ptx::mbar_wait(&desc_full[0], 0);
+      bool have = D->w >= 0;
+      int flags = have ? D->flags : 0, n = have ? D->n : 0;
+      int pos_s = 0;  // trace index of the S being issued
+      auto s_pair_half = [&](int w, int fl) {  // S_w of the tile in K stage kst
+        if (fl & 1) ptx::mbar_wait(&full_q[w], qph);
+        if (lane == 0 && w == 0) BSRA_TRACE(13, pos_s);
+        if (w == 0) ptx::mbar_wait(&full_k[kst], kph);
+        if (lane == 0 && w == 0) BSRA_TRACE(2, pos_s);
         ptx::tc_fence_after();
-        {
-          // warp-converged issue (elect inside the asm); descriptors: +2 (32 B) per K step
-          // inside a 64-column atom, +1024 (16 KB) per atom
-          const uint64_t a0 = ptx::smem_desc_sw128(sbase + kOffQ + w * kOp, 16, 1024);
-          const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffK + kst * kOp, 16, 1024);
-          const uint32_t dS = tmem + w * 128;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t step = (uint64_t)((kk >> 2) * (kHalf >> 4) + (kk & 3) * 2);
-            if (!(tp.dbg & 2)) ptx::mma_f16_ss_warp(dS, a0 + step, b0 + step, idS, kk > 0);
-          }
-        }
-        ptx::mma_commit_warp(&empty_k[kst]);
+        issue_s(w, kst);
         ptx::mma_commit_warp(&bar_s[w]);
-        if (flags & 2) ptx::mma_commit_warp(&empty_q[w]);  // last S of the item: Q buffer free
-        if (++kst == kKStages) {
-          kst = 0;
-          kph ^= 1;
-        }
-        pending[w] = 1;
-        ++s_pos;
-      }
-      if (pv_pos == s_pos) break;  // schedule finished and every PV issued
-      // ---- PV of the oldest tile
-      const int slot = pv_pos % kDesc;
-      const TileDesc& D = descs[slot];
-      const int w = D.w, n = D.n, flags = D.flags;
-      ptx::mbar_wait(&full_v[vst], vph);
-      if (n < kTile) {  // rows past the chunk -> 0 (0 * garbage could be NaN)
-        uint8_t* vS = smem + kOffV + vst * kOp;
-        for (int rr = n + lane; rr < kTile; rr += 32) {
-          uint4* v0 = reinterpret_cast<uint4*>(vS + rr * 128);
-          uint4* v1 = reinterpret_cast<uint4*>(vS + kHalf + rr * 128);
-#pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            v0[jj] = make_uint4(0, 0, 0, 0);
-            v1[jj] = make_uint4(0, 0, 0, 0);
+        if (fl & 2) ptx::mma_commit_warp(&empty_q[w]);  // the item's last S: Q_w buffer free
+        if (w == 1) {
+          ++pos_s;
+          ptx::mma_commit_warp(&empty_k[kst]);
+          if (fl & 1) qph ^= 1;
+          if (++kst == kKStages) {
+            kst = 0;
+            kph ^= 1;
           }
         }
-        ptx::fence_proxy_async();
-        __syncwarp();
+      };
+      if (have) {
+        s_pair_half(0, flags);
+        s_pair_half(1, flags);
       }
-      ptx::mbar_wait(&p_ready[w], pph[w]);
-      pph[w] ^= 1;
-      if (lane == 0) BSRA_TRACE(3, pv_pos);
-      ptx::tc_fence_after();
-      {
-        const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffV + vst * kOp, kHalf, 1024);
-        const uint32_t dO = tmem + 256 + w * 128, aP = tmem + w * 128;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // +128 (2 KB = 16 tokens) per K step of the MN-major V
-          if (!(tp.dbg & 2))
-            ptx::mma_f16_ts_warp(dO, aP + kk * 8, b0 + (uint64_t)(kk * 128), idO, ((flags & 1) && kk == 0) ? 0u : 1u);
+      while (have) {
+        const int slot = pos % kDesc;
+        if (lane == 0) BSRA_TRACE(3, pos);
+        ptx::mbar_wait(&full_v[vst], vph);
+        if (n < kTile) zero_v_tail(vst, n);
+        ptx::mbar_wait(&p_ready[0], pph[0]);
+        pph[0] ^= 1;
+        ptx::tc_fence_after();
+        issue_pv(0, vst, flags & 1);
+        if (flags & 2) ptx::mma_commit_warp(&bar_o[0]);
+        // next tile's descriptor (the scheduler runs ahead)
+        const int npos = pos + 1, nslot = npos % kDesc;
+        ptx::mbar_wait(&desc_full[nslot], (npos / kDesc) & 1);
+        const TileDesc* N = &descs[nslot];
+        const bool nhave = N->w >= 0;
+        const int nflags = nhave ? N->flags : 0, nn = nhave ? N->n : 0;
+        if (nhave) s_pair_half(0, nflags);
+        ptx::mbar_wait(&p_ready[1], pph[1]);
+        pph[1] ^= 1;
+        ptx::tc_fence_after();
+        issue_pv(1, vst, flags & 1);
+        ptx::mma_commit_warp(&empty_v[vst]);
+        if (flags & 2) ptx::mma_commit_warp(&bar_o[1]);
+        ptx::mbar_arrive_warp(&desc_empty[slot]);
+        if (++vst == kVStages) {
+          vst = 0;
+          vph ^= 1;
+        }
+        if (nhave) s_pair_half(1, nflags);
+        pos = npos;
+        have = nhave;
+        flags = nflags;
+        n = nn;
       }
-      ptx::mma_commit_warp(&empty_v[vst]);
-      if (flags & 2) ptx::mma_commit_warp(&bar_o[w]);
-      ptx::mbar_arrive_warp(&desc_empty[slot]);
-      if (++vst == kVStages) {
-        vst = 0;
-        vph ^= 1;
+    } else {
+      // Streamed: two cursors over the descriptor ring, S in order (K ring) and PV in order (V
+      // ring). A WG has one S buffer, so its next S is issued only after the PV of its current
+      // tile (in-order tensor pipe => no WAR hazard on TMEM).
+      int kst = 0, vst = 0;
+      uint32_t kph = 0, vph = 0;
+      // per-WG phase bits and the "S buffer held" flags as bitmasks (register-resident; arrays
+      // indexed by the runtime WG would live in local memory on the issue path)
+      uint32_t qph = 0, pph = 0, pending = 0;
+      int s_pos = 0, pv_pos = 0;
+      bool s_done = false;
+      for (;;) {
+        // ---- issue S in order while the next tile's WG is not holding its S buffer
+        while (!s_done) {
+          const int slot = s_pos % kDesc;
+          const uint32_t ph = (s_pos / kDesc) & 1;
+          if (pv_pos == s_pos) ptx::mbar_wait(&desc_full[slot], ph);
+          else if (!ptx::mbar_test_wait_warp(&desc_full[slot], ph)) break;
+          const TileDesc& D = descs[slot];
+          const int w = D.w;
+          if (w < 0) {
+            s_done = true;
+            break;
+          }
+          if ((pending >> w) & 1) break;
+          const int flags = D.flags;
+          if (flags & 1) {  // first tile of an item: its Q must have landed
+            ptx::mbar_wait(&full_q[w], (qph >> w) & 1);
+            qph ^= 1u << w;
+          }
+          ptx::mbar_wait(&full_k[kst], kph);
+          if (lane == 0) BSRA_TRACE(2, s_pos);
+          ptx::tc_fence_after();
+          issue_s(w, kst);
+          ptx::mma_commit_warp(&empty_k[kst]);
+          ptx::mma_commit_warp(&bar_s[w]);
+          if (flags & 2) ptx::mma_commit_warp(&empty_q[w]);  // last S of the item: Q buffer free
+          if (++kst == kKStages) {
+            kst = 0;
+            kph ^= 1;
+          }
+          pending |= 1u << w;
+          ++s_pos;
+        }
+        if (pv_pos == s_pos) break;  // schedule finished and every PV issued
+        // ---- PV of the oldest tile
+        const int slot = pv_pos % kDesc;
+        const TileDesc& D = descs[slot];
+        const int w = D.w, n = D.n, flags = D.flags;
+        ptx::mbar_wait(&full_v[vst], vph);
+        if (n < kTile) zero_v_tail(vst, n);
+        ptx::mbar_wait(&p_ready[w], (pph >> w) & 1);
+        pph ^= 1u << w;
+        if (lane == 0) BSRA_TRACE(3, pv_pos);
+        ptx::tc_fence_after();
+        issue_pv(w, vst, flags & 1);
+        ptx::mma_commit_warp(&empty_v[vst]);
+        if (flags & 2) ptx::mma_commit_warp(&bar_o[w]);
+        ptx::mbar_arrive_warp(&desc_empty[slot]);
+        if (++vst == kVStages) {
+          vst = 0;
+          vph ^= 1;
+        }
+        pending &= ~(1u << w);
+        ++pv_pos;
       }
-      pending[w] = 0;
-      ++pv_pos;
     }
   } else if (warp >= 4) {
     // ===================== softmax warpgroups =====================
@@ -424,10 +520,13 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
     const float sc = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     int tcount = 0;
-    for (int it = it0 + w; w < nstream && it < it1; it += nstream) {
+    const int ri = kPair ? w * 128 + r : r;  // this thread's row within the item
+    const int first_it = kPair ? it0 : it0 + w;
+    for (int it = first_it; (kPair || w < nstream) && it < it1; it += nstream) {
       const DecItem d = dec_item(pv, it, g);
-      const bool row_ok = r < d.nrows;
-      const int f = d.row0 + r;
+      if (r == 0 && w == 0) BSRA_TRACE(14, it - it0);
+      const bool row_ok = ri < d.nrows;
+      const int f = d.row0 + ri;
       const int tok = f / g, head = d.kvh * g + f % g;
       const int64_t lim = kMask == 1 ? d.lk - d.lq + tok : d.ke - 1;
       const int64_t mbase = kMask == 2 ? p.mask_indptr[d.req] + (int64_t)tok * d.lk : 0;
@@ -449,9 +548,9 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           continue;
         }
         // ---- pass 1: raw row max (two 32-column TMEM loads in flight per round trip)
-        float mx = -INFINITY;
+        float mx = (tp.dbg & 16) ? 0.f : -INFINITY;  // dbg 16: timing experiment, no max pass
 #pragma unroll
-        for (int c = 0; c < 4; c += 2) {
+        for (int c = 0; c < ((tp.dbg & 16) ? 0 : 4); c += 2) {
           float s[64];
           ptx::tmem_ld32(tS + c * 32, s);
           ptx::tmem_ld32(tS + c * 32 + 32, s + 32);
@@ -499,8 +598,10 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           }
         }
         // ---- pass 2: P = 2^(s*scale - m) packed to 16-bit pairs, written over the consumed S columns
+        // packed fp32 pairs (FFMA2 / FADD2) for the scale and the row sum; four independent sums
         const float mneg = m == -INFINITY ? 0.f : -m;
-        float rs0 = 0.f, rs1 = 0.f;
+        const float2 sc2 = make_float2(sc, sc), mn2 = make_float2(mneg, mneg);
+        float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         float sbuf[2][32];  // chunk c+1's TMEM load overlaps chunk c's exponentials
         ptx::tmem_ld32(tS, sbuf[0]);
         ptx::tmem_ld_wait();
@@ -519,22 +620,25 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            const float p0 = ptx_ex2(fmaf(s[j], sc, mneg));
-            const float p1 = ptx_ex2(fmaf(s[j + 1], sc, mneg));
-            rs0 += p0;
-            rs1 += p1;
-            if (tp.f16) {
-              __half2 h = __floats2half2_rn(p0, p1);
+            float2 x = __ffma2_rn(make_float2(s[j], s[j + 1]), sc2, mn2);
+            if (!(tp.dbg & 32)) {  // dbg 32: timing experiment, no MUFU
+              x.x = ptx_ex2(x.x);
+              x.y = ptx_ex2(x.y);
+            }
+            rs[(j >> 1) & 3] = __fadd2_rn(rs[(j >> 1) & 3], x);
+            if constexpr (kF16) {
+              __half2 h = __floats2half2_rn(x.x, x.y);
               pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h);
             } else {
-              __nv_bfloat162 h = __floats2bfloat162_rn(p0, p1);
+              __nv_bfloat162 h = __floats2bfloat162_rn(x.x, x.y);
               pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h);
             }
           }
           ptx::tmem_st16(tS + c * 16, pk);
           ptx::tmem_ld_wait();  // chunk c+1 has landed (its columns are >= 32(c+1) > P's 16(c+1))
         }
-        l = l * alpha + (rs0 + rs1);
+        const float2 r01 = __fadd2_rn(rs[0], rs[1]), r23 = __fadd2_rn(rs[2], rs[3]);
+        l = l * alpha + ((r01.x + r01.y) + (r23.x + r23.y));
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_ready[w]);
@@ -543,42 +647,49 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       }
       pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
       // ---- epilogue: wait for the item's last PV, normalise, write
+      if (r == 0 && w == 0) BSRA_TRACE(11, it - it0);
       if (d.ntiles > 0) {
         ptx::mbar_wait(&bar_o[w], oph);
         oph ^= 1;
         ptx::tc_fence_after();
       }
+      if (r == 0 && w == 0) BSRA_TRACE(12, it - it0);
       const bool empty_row = !(l > 0.f);
       const float inv = empty_row ? 0.f : 1.f / l;
       const float lse = empty_row ? -INFINITY : (m + __log2f(l)) * kLn2;
       const int64_t orow = (d.qo_begin + tok) * p.H_qo + head;
-      const int64_t prow = (int64_t)d.slot * p.T_slot + r;
+      const int64_t prow = (int64_t)d.slot * p.T_slot + ri;
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 32) {
         float ov[32];
-        if (d.ntiles > 0) {
+        if (d.ntiles > 0 && !(tp.dbg & 128)) {  // dbg 128: timing experiment, no O read
           ptx::tmem_ld32(tO + c0, ov);
           ptx::tmem_ld_wait();
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) ov[j] = 0.f;
         }
-        if (!row_ok) continue;
+        if (!row_ok || (tp.dbg & 64)) continue;  // dbg 64: timing experiment, no o stores
+        // 256-bit stores: a lane writes whole 32-byte sectors of its row (half the instructions of
+        // 16-byte stores; rows of a warp are scattered, so the instruction count is the cost)
         if (d.slot >= 0 || p.o_f32) {
           float* dstf = d.slot >= 0 ? p.part_o + prow * 128 + c0 : reinterpret_cast<float*>(p.o) + orow * 128 + c0;
-          float4* dst = reinterpret_cast<float4*>(dstf);
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(ov[4 * j] * inv, ov[4 * j + 1] * inv, ov[4 * j + 2] * inv, ov[4 * j + 3] * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.o) + orow * 128 + c0);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            uint32_t wv[4];
+            uint32_t wv[8];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float a0 = ov[8 * j + 2 * e] * inv, a1 = ov[8 * j + 2 * e + 1] * inv;
-              if (tp.f16) {
+            for (int e = 0; e < 8; ++e) wv[e] = __float_as_uint(ov[8 * j + e] * inv);
+            ptx::st_global_v8(dstf + 8 * j, wv);
+          }
+        } else {
+          uint16_t* dsth = reinterpret_cast<uint16_t*>(p.o) + orow * 128 + c0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            uint32_t wv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float a0 = ov[16 * j + 2 * e] * inv, a1 = ov[16 * j + 2 * e + 1] * inv;
+              if constexpr (kF16) {
                 __half2 h = __floats2half2_rn(a0, a1);
                 wv[e] = *reinterpret_cast<uint32_t*>(&h);
               } else {
@@ -586,7 +697,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
                 wv[e] = *reinterpret_cast<uint32_t*>(&h);
               }
             }
-            dst[j] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            ptx::st_global_v8(dsth + 16 * j, wv);
           }
         }
       }
@@ -594,31 +705,38 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         if (d.slot >= 0) p.part_lse[prow] = lse;
         else if (p.lse) p.lse[orow] = lse;
       }
-      if (d.slot >= 0 && p.fused_merge) {  // split item: the WG completing its merge list folds it
+      if (!kPair && d.slot >= 0 && p.fused_merge) {  // split item: the WG completing its merge list folds it
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1 + w);
-        if (tp.f16) fused_contraction<__half, 128>(p, pv, d.slot, r, 128, 2 + w, s_flag);
+        if constexpr (kF16) fused_contraction<__half, 128>(p, pv, d.slot, r, 128, 2 + w, s_flag);
         else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, r, 128, 2 + w, s_flag);
       }
       ptx::tc_fence_before();  // O_w reads done before this WG's next p_ready (next item's PV)
+      if (r == 0 && w == 0) BSRA_TRACE(4, it - it0);
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) BSRA_TRACE(9, 1);
+  if (p.trace && threadIdx.x == 0) p.trace[17 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
 #undef BSRA_TRACE
   if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 
-template <int kMask>
-inline cudaError_t launch_prefill2_t(const TcParams& tp, int grid, cudaStream_t st) {
+template <int kMask, bool kPair, bool kF16>
+inline cudaError_t launch_prefill2_f(const TcParams& tp, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_prefill2_kernel<kMask>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         pre2::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(tc_prefill2_kernel<kMask, kPair, kF16>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, pre2::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_tc(tc_prefill2_kernel<kMask>, grid, pre2::kThreads, pre2::kSmemBytes, st, tp);
+  return launch_tc(tc_prefill2_kernel<kMask, kPair, kF16>, grid, pre2::kThreads, pre2::kSmemBytes, st, tp);
+}
+
+template <int kMask, bool kPair>
+inline cudaError_t launch_prefill2_t(const TcParams& tp, int grid, cudaStream_t st) {
+  return tp.f16 ? launch_prefill2_f<kMask, kPair, true>(tp, grid, st) : launch_prefill2_f<kMask, kPair, false>(tp, grid, st);
 }
 
 }  // namespace bsra

@@ -36,6 +36,7 @@ t0 = t[9, 0]
 out = {}
 for ev in range(16):
     row = t[ev]
-    n = int(np.count_nonzero(row))
+    nz = np.nonzero(row)[0]
+    n = int(nz[-1]) + 1 if len(nz) else 0
     out[ev] = [int(x - t0) if x else None for x in row[:n]]
 print(json.dumps({"total": int(t[9, 1] - t0), "events": out}))

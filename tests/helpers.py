@@ -10,7 +10,7 @@ import synth
 TOL = {"f32": (1e-5, 1e-5), "f16": (1e-2, 1e-3), "bf16": (1e-2, 1e-3)}  # (o, lse): BASELINE north_star
 
 
-def engine_for(wl, *, num_ctas=0, tile_q=0, tile_set=(16, 64, 128), kernel="auto", o_dtype=None, max_batch=None,
+def engine_for(wl, *, num_ctas=0, tile_q=0, tile_set=(16, 64, 128, 256), kernel="auto", o_dtype=None, max_batch=None,
                max_rows=None, device=0):
     cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
                            o_dtype=o_dtype, mask=wl.mask, max_batch=max_batch or max(1, wl.batch),

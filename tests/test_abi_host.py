@@ -39,7 +39,7 @@ def _bsr(qo, kv, ps):
 MASKS = {0: "none", 1: "causal", 2: "custom"}
 
 
-def _compare(qo, kv, *, H_qo, H_kv, ps, mask, num_ctas, tiles=(16, 64, 128), tile_q=0, alpha=1, beta=1,
+def _compare(qo, kv, *, H_qo, H_kv, ps, mask, num_ctas, tiles=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
              align=0, L_min=0):
     qi, ki, last = _bsr(qo, kv, ps)
     cfg = bsra.make_config(H_qo=H_qo, H_kv=H_kv, D=128, page_size=ps, dtype="bf16", mask=MASKS[mask],
@@ -78,7 +78,7 @@ def test_cpp_scheduler_bit_exact_vs_python(seed):
     alpha, beta = (1, 1) if seed % 5 else (int(rng.integers(0, 50)), int(rng.integers(1, 5)))
     align = 0 if seed % 7 else int(rng.choice([1, 8, 32]))
     L_min = 0 if seed % 11 else int(rng.integers(1, 500))
-    tiles = [(16, 64, 128), (16, 128), (64,), (128,), (16,)][seed % 5]
+    tiles = [(16, 64, 128), (16, 128), (64,), (128,), (16,), (16, 64, 128, 256), (256,)][seed % 7]
     _compare(qo, kv, H_qo=H_kv * g, H_kv=H_kv, ps=ps, mask=mask, num_ctas=num_ctas, tiles=tiles, alpha=alpha,
              beta=beta, align=align, L_min=L_min)
 

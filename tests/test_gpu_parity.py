@@ -45,7 +45,7 @@ def test_random_small_workloads(cuda_device, seed):
 
 @pytest.mark.parametrize("kernel", ["simt", "auto"])
 @pytest.mark.parametrize("mask", ["none", "causal", "custom"])
-@pytest.mark.parametrize("tile_q", [16, 64, 128])
+@pytest.mark.parametrize("tile_q", [16, 64, 128, 256])
 def test_tiles_masks_kernels_bf16(cuda_device, kernel, mask, tile_q):
     wl = synth.Workload("t", 32, 8, 128, 16, "bf16", mask, np.array([1, 37, 5, 130, 0], np.int32),
                         np.array([300, 37, 900, 250, 33], np.int32))

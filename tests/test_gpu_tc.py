@@ -88,7 +88,7 @@ def test_tc_decode_deterministic(cuda_device):
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
-# ----------------------------------------------------------------- prefill (T_q = 64 / 128)
+# ----------------------------------------------------------- prefill (T_q = 64 / 128 / 256)
 def _prefill_case(cuda_device, *, H_qo=64, H_kv=8, ps=16, dtype="bf16", mask="causal", qo=None, kv=None, nc=148,
                   tile_q=128, seed=0, layout="NHD", q_scale=1.0):
     qo = np.array(qo if qo is not None else [70, 129, 1, 300], np.int32)
@@ -101,34 +101,40 @@ def _prefill_case(cuda_device, *, H_qo=64, H_kv=8, ps=16, dtype="bf16", mask="ca
 
 
 @pytest.mark.parametrize("mask", ["none", "causal", "custom"])
-@pytest.mark.parametrize("tile_q", [64, 128])
+@pytest.mark.parametrize("tile_q", [64, 128, 256])
 def test_tc_prefill_masks_tiles(cuda_device, mask, tile_q):
     _prefill_case(cuda_device, mask=mask, tile_q=tile_q)
 
 
+@pytest.mark.parametrize("tile_q", [128, 256])
 @pytest.mark.parametrize("nc", [1, 5, 148, 300])
-def test_tc_prefill_num_ctas(cuda_device, nc):
-    _prefill_case(cuda_device, nc=nc, qo=[500, 37, 1000], kv=[700, 37, 1000])
+def test_tc_prefill_num_ctas(cuda_device, nc, tile_q):
+    _prefill_case(cuda_device, nc=nc, qo=[500, 37, 1000], kv=[700, 37, 1000], tile_q=tile_q)
 
 
+@pytest.mark.parametrize("tile_q", [128, 256])
 @pytest.mark.parametrize("H", [(8, 8), (32, 8), (64, 8), (128, 8), (16, 1)])
-def test_tc_prefill_group_sizes(cuda_device, H):
-    _prefill_case(cuda_device, H_qo=H[0], H_kv=H[1], nc=64)
+def test_tc_prefill_group_sizes(cuda_device, H, tile_q):
+    _prefill_case(cuda_device, H_qo=H[0], H_kv=H[1], nc=64, tile_q=tile_q)
 
 
+@pytest.mark.parametrize("tile_q", [128, 256])
 @pytest.mark.parametrize("ps", [8, 32, 128, 256])
-def test_tc_prefill_page_sizes(cuda_device, ps):
-    _prefill_case(cuda_device, ps=ps, nc=40)
+def test_tc_prefill_page_sizes(cuda_device, ps, tile_q):
+    _prefill_case(cuda_device, ps=ps, nc=40, tile_q=tile_q)
 
 
+@pytest.mark.parametrize("tile_q", [128, 256])
 @pytest.mark.parametrize("dtype", ["bf16", "f16"])
 @pytest.mark.parametrize("layout", ["NHD", "HND"])
-def test_tc_prefill_dtypes_layouts(cuda_device, dtype, layout):
-    _prefill_case(cuda_device, dtype=dtype, layout=layout, nc=33)
+def test_tc_prefill_dtypes_layouts(cuda_device, dtype, layout, tile_q):
+    _prefill_case(cuda_device, dtype=dtype, layout=layout, nc=33, tile_q=tile_q)
 
 
-def test_tc_prefill_peaked_and_empty(cuda_device):
-    _prefill_case(cuda_device, q_scale=8.0, qo=[3, 0, 200, 9], kv=[1, 10, 200, 2], mask="causal", nc=17)
+@pytest.mark.parametrize("tile_q", [128, 256])
+def test_tc_prefill_peaked_and_empty(cuda_device, tile_q):
+    _prefill_case(cuda_device, q_scale=8.0, qo=[3, 0, 200, 9], kv=[1, 10, 200, 2], mask="causal", nc=17,
+                  tile_q=tile_q)
 
 
 def test_tc_prefill_decode_rows_agree_with_tc_decode(cuda_device):

@@ -43,6 +43,14 @@ def test_workspace_bound_example():
 @pytest.mark.parametrize("qo,g,expect", [([1] * 128, 4, 16), ([1] * 2, 4, 16), ([5] * 8, 4, 64),
                                          ([64, 2048], 8, 128), ([16] * 4, 1, 16), ([17] * 4, 1, 64)])
 def test_select_tile(qo, g, expect):
+    """The paper's tile set."""
+    assert S.select_tile(qo, g, (16, 64, 128)) == expect
+
+
+@pytest.mark.parametrize("qo,g,expect", [([64, 2048], 8, 256), ([16] * 4, 8, 128), ([17] * 4, 8, 256),
+                                         ([1] * 128, 4, 16), ([4000] * 2, 1, 256)])
+def test_select_tile_with_256(qo, g, expect):
+    """Extended set with the paired 256-row tile (R20): same rule, one more size."""
     assert S.select_tile(qo, g) == expect
 
 
