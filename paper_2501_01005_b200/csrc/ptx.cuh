@@ -299,6 +299,27 @@ __device__ __forceinline__ float poly_ex2(float x) {
   return x <= -126.f ? 0.f : r;
 }
 
+// 2^x for a pair on the FMA pipes (FADD2 / FFMA2 + one IMAD per element), offloading the MUFU,
+// whose 4 ex2/clk/SMSP otherwise bound the prefill softmax (FA4's exp2 emulation). The caller
+// passes xs = x - 1/2 (folded into its scale FFMA). n = rint(xs) = floor(x) except at ties, and
+// f = x - n lies in [0, 1]; 2^f = 1 + f(c1 + f(c2 + f c3)), a minimax cubic with p(0) = 1 and
+// p(1) = 2 exactly (max relative error 1.03e-4, 20x below the bf16 rounding P receives). Then
+// 2^x = bits(p) + n << 23, where t = xs + 1.5*2^23 holds n in its low mantissa bits, so
+// bits(t) * 2^23 = n << 23 (mod 2^32). Clamping xs at -127.5 gives n = -128, f = 1,
+// bits(2.0) - (128 << 23) = 0: masked (-inf) and underflowing inputs give exactly 0.
+__device__ __forceinline__ float2 poly_ex2x2_shifted(float2 xs) {
+  xs.x = fmaxf(xs.x, -127.5f);
+  xs.y = fmaxf(xs.y, -127.5f);
+  const float2 t = __fadd2_rn(xs, make_float2(12582912.f, 12582912.f));
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(n, make_float2(-1.f, -1.f), __fadd2_rn(xs, make_float2(0.5f, 0.5f)));
+  float2 p = __ffma2_rn(f, make_float2(0.0782674694f, 0.0782674694f), make_float2(0.226308357f, 0.226308357f));
+  p = __ffma2_rn(p, f, make_float2(0.695424173f, 0.695424173f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  return make_float2(__int_as_float(__float_as_int(t.x) * (1 << 23) + __float_as_int(p.x)),
+                     __int_as_float(__float_as_int(t.y) * (1 << 23) + __float_as_int(p.y)));
+}
+
 namespace ptx {
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;

@@ -53,6 +53,12 @@ constexpr int kSmemBytes = kOffDesc + kDesc * 96 + 1024 + BSRA_PRE2_PAD;
 constexpr int kThreads = 384;  // warps 0 Q+K producer, 1 V producer, 2 MMA, 3 scheduler, 4-7 WG0, 8-11 WG1
 constexpr uint32_t kTmemCols = 512;  // S/P_w at w*128, O_w at 256 + w*128
 constexpr float kRescaleThresh = 8.f;
+// exp2 split between the MUFU (4/clk/SMSP) and a cubic on the FMA pipes: kEmuPairs of every 8
+// element pairs take the polynomial (FA4's exp2 emulation)
+#ifndef BSRA_PRE2_EMU
+#define BSRA_PRE2_EMU 2
+#endif
+constexpr int kEmuPairs = BSRA_PRE2_EMU;
 }  // namespace pre2
 
 // One KV tile of the interleaved order, as published by the scheduler warp.
@@ -601,6 +607,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         // packed fp32 pairs (FFMA2 / FADD2) for the scale and the row sum; four independent sums
         const float mneg = m == -INFINITY ? 0.f : -m;
         const float2 sc2 = make_float2(sc, sc), mn2 = make_float2(mneg, mneg);
+        const float2 mn2h = make_float2(mneg - 0.5f, mneg - 0.5f);  // poly_ex2x2_shifted takes x - 1/2
         float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         float sbuf[2][32];  // chunk c+1's TMEM load overlaps chunk c's exponentials
         ptx::tmem_ld32(tS, sbuf[0]);
@@ -620,8 +627,11 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           uint32_t pk[16];
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            float2 x = __ffma2_rn(make_float2(s[j], s[j + 1]), sc2, mn2);
-            if (!(tp.dbg & 32)) {  // dbg 32: timing experiment, no MUFU
+            float2 x;
+            if (((j >> 1) & 7) < kEmuPairs) {  // kEmuPairs of every 8 pairs on the FMA pipes
+              x = poly_ex2x2_shifted(__ffma2_rn(make_float2(s[j], s[j + 1]), sc2, mn2h));
+            } else {
+              x = __ffma2_rn(make_float2(s[j], s[j + 1]), sc2, mn2);
               x.x = ptx_ex2(x.x);
               x.y = ptx_ex2(x.y);
             }
