@@ -81,6 +81,12 @@ typedef struct {
  * run() (q, pools, indices, mask) are NOT produced by the kernel immediately preceding it on
  * the stream — e.g. consecutive layers' attention captured back to back. */
 #define BSRA_FLAG_PDL 1
+/* flags: BSRA_FLAG_RAGGED_KV makes a contiguous-KV engine (the KV layout
+ * the paper's App. B compares the page table against): K/V are ragged tensors
+ * [sum l_kv, H_kv, D] indexed by kv_indptr, with no page table. Such an engine is planned with
+ * bsra_plan_ragged and run with bsra_run_ragged, and requires page_size = 128 (the KV tile and
+ * the default chunk alignment). */
+#define BSRA_FLAG_RAGGED_KV 2
 
 typedef struct bsra_engine bsra_engine;
 
@@ -134,6 +140,26 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
                      const int64_t* k_strides, const int64_t* v_strides, const int32_t* kv_page_indices,
                      const uint8_t* custom_mask, const int64_t* mask_bit_indptr, void* o, float* lse,
                      void* stream);
+
+/* Contiguous-KV inspector (engine created with BSRA_FLAG_RAGGED_KV): as bsra_plan, with the KV
+ * lengths given by a ragged indptr instead of a page table.
+ *   qo_indptr  [batch+1] host int32; [0] = 0; nondecreasing
+ *   kv_indptr  [batch+1] host int32; [0] = 0; nondecreasing; request i's keys are rows
+ *              kv_indptr[i] .. kv_indptr[i+1]-1 of k / v
+ * Errors: EINVAL (malformed arrays, paged engine), EBOUNDS (bounds). */
+bsra_status bsra_plan_ragged(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, const int32_t* kv_indptr,
+                             float sm_scale, void* stream);
+
+/* Contiguous-KV executor: as bsra_run, with
+ *   k, v       [kv_indptr[batch], H_kv, D] device, cfg->dtype; row t at t*strides[0], head h at
+ *              h*strides[1] (ELEMENTS, host int64[2]; dim stride 1); base 16-byte aligned, strides
+ *              16-byte multiples. Tiles are read with one TMA box per 128 tokens at a token
+ *              coordinate (no gather); the tensor map's extent is kv_indptr[batch], so the last
+ *              tile never reads past k / v.
+ * q, custom_mask, mask_bit_indptr, o, lse, stream: as bsra_run. Graph-capturable. */
+bsra_status bsra_run_ragged(bsra_engine* e, const void* q, const void* k, const void* v, const int64_t* k_strides,
+                            const int64_t* v_strides, const uint8_t* custom_mask, const int64_t* mask_bit_indptr,
+                            void* o, float* lse, void* stream);
 
 /* ⊕ of two attention-state tensors, max-shifted, fp32 arithmetic; the empty state
  * (o = 0, lse = -inf) is the identity. rows x heads states of head_dim values each.

@@ -41,11 +41,13 @@ class Config(ctypes.Structure):
 
 
 FLAG_PDL = 1  # BSRA_FLAG_PDL (include/bsra.h)
+FLAG_RAGGED_KV = 2  # BSRA_FLAG_RAGGED_KV: contiguous (ragged) K/V, no page table
 
 
 _lib = None
 EXPORTS = ["bsra_version", "bsra_num_sms", "bsra_workspace_bytes", "bsra_engine_create", "bsra_engine_destroy",
-           "bsra_plan", "bsra_run", "bsra_merge_states", "bsra_merge_many", "bsra_plan_host", "bsra_plan_export",
+           "bsra_plan", "bsra_run", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
+           "bsra_plan_host", "bsra_plan_export",
            "bsra_plan_stats", "bsra_last_run_launches", "bsra_selected_kernel", "bsra_last_error",
            "bsra_dist_unique_id", "bsra_dist_create", "bsra_dist_destroy", "bsra_dist_scratch_bytes",
            "bsra_dist_allgather_merge", "bsra_dist_last_error"]
@@ -68,6 +70,8 @@ def lib():
             "bsra_engine_destroy": (None, [P]),
             "bsra_plan": (I32, [P, I32, P, P, P, ctypes.c_float, P]),
             "bsra_run": (I32, [P, P, P, P, P, P, P, P, P, P, P, P]),
+            "bsra_plan_ragged": (I32, [P, I32, P, P, ctypes.c_float, P]),
+            "bsra_run_ragged": (I32, [P, P, P, P, P, P, P, P, P, P, P]),
             "bsra_merge_states": (I32, [P, P, P, P, I32, I64, I32, I32, P, I32, P, P]),
             "bsra_merge_many": (I32, [P, P, I32, I64, I32, I32, P, I32, P, P]),
             "bsra_plan_host": (I32, [CP, I32, I32, P, P, P, P, SZ, ctypes.POINTER(SZ)]),
@@ -106,9 +110,9 @@ def _i32(a) -> np.ndarray:
 
 def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="none", max_batch=1,
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
-                kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False) -> Config:
+                kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False) -> Config:
     c = Config()
-    c.flags = FLAG_PDL if pdl else 0
+    c.flags = (FLAG_PDL if pdl else 0) | (FLAG_RAGGED_KV if ragged_kv else 0)
     c.num_qo_heads, c.num_kv_heads, c.head_dim, c.page_size = H_qo, H_kv, D, page_size
     c.dtype = DTYPE[dtype] if isinstance(dtype, str) else dtype
     od = o_dtype if o_dtype is not None else dtype
@@ -186,6 +190,21 @@ class Engine:
         _check(lib().bsra_run(self._h, _p(q), _p(k_pool), _p(v_pool), ctypes.cast(ks, ctypes.c_void_p),
                               ctypes.cast(vs, ctypes.c_void_p), _p(kv_page_indices), _p(custom_mask),
                               _p(mask_bit_indptr), _p(o), _p(lse), self._stream(stream)))
+
+    def plan_ragged(self, qo_indptr, kv_indptr, sm_scale: float = 0.0, stream=None):
+        """Contiguous-KV inspector (engine made with ragged_kv=True): kv_indptr[batch+1] token offsets."""
+        qi, ki = _i32(qo_indptr), _i32(kv_indptr)
+        self._keep = [qi, ki]
+        _check(lib().bsra_plan_ragged(self._h, len(qi) - 1, _p(qi), _p(ki), float(sm_scale), self._stream(stream)))
+
+    def run_ragged(self, q, k, v, k_strides, v_strides, o, lse=None, custom_mask=None, mask_bit_indptr=None,
+                   stream=None):
+        """Contiguous-KV executor: k, v [N, H_kv, D]; strides (token, head) in elements."""
+        ks = (ctypes.c_int64 * 2)(*[int(x) for x in k_strides])
+        vs = (ctypes.c_int64 * 2)(*[int(x) for x in v_strides])
+        _check(lib().bsra_run_ragged(self._h, _p(q), _p(k), _p(v), ctypes.cast(ks, ctypes.c_void_p),
+                                     ctypes.cast(vs, ctypes.c_void_p), _p(custom_mask), _p(mask_bit_indptr), _p(o),
+                                     _p(lse), self._stream(stream)))
 
     def export_plan(self, from_device=False, stream=None) -> np.ndarray:
         L = lib()

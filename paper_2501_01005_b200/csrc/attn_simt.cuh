@@ -36,8 +36,8 @@ __device__ __forceinline__ void simt_load_tile(const AttnParams& p, uint8_t* sk,
   for (int c = threadIdx.x; c < n * kChunks; c += blockDim.x) {
     const int tt = c / kChunks, ch = c % kChunks;
     const int64_t t = t0 + tt;
-    const int64_t page = __ldg(p.page_indices + page_begin + t / p.page_size);
-    const int64_t slot = t % p.page_size;
+    const int64_t page = p.kv_ragged ? 0 : __ldg(p.page_indices + page_begin + t / p.page_size);
+    const int64_t slot = p.kv_ragged ? page_begin + t : t % p.page_size;
     const T* ksrc = kp + page * p.ks0 + slot * p.ks1 + kvh * p.ks2 + ch * (16 / (int)sizeof(T));
     const T* vsrc = vp + page * p.vs0 + slot * p.vs1 + kvh * p.vs2 + ch * (16 / (int)sizeof(T));
     cp_async16(sk + tt * S::kRowBytes + ch * 16, ksrc);

@@ -29,6 +29,10 @@ struct AttnParams {
   int32_t* counters;  // per-merge-list arrival counters (fused contraction)
   long long* trace;   // optional pipeline trace (CTA 0 event clocks), NULL in production
   int32_t fused_merge;  // 1: split items are merged in-kernel (decode engines); 0: contraction kernel
+  // 1: contiguous (ragged) KV: token t of request i is row page_begin_i + t of
+  // k/v [N, H_kv, D] (page_begin = kv_indptr[i]); no page table. The tcgen05 kernels address it
+  // through a pool map whose token dimension is N (TMA clips at the buffer end).
+  int32_t kv_ragged;
   int32_t H_qo, H_kv, g, page_size, mask_mode, o_f32, T_slot, D;
   float scale_log2;  // sm_scale * log2(e)
 };

@@ -65,7 +65,9 @@ bsra_status validate_config(const bsra_config& c) {
   if (c.cost_alpha < 0 || c.cost_beta < 0) return fail(BSRA_EINVAL, "negative cost parameters");
   if (c.kv_chunk_align < 0 || c.kv_chunk_min < 0) return fail(BSRA_EINVAL, "negative chunk parameters");
   if (c.kernel < BSRA_KERNEL_AUTO || c.kernel > BSRA_KERNEL_TC) return fail(BSRA_EINVAL, "bad kernel selector");
-  if (c.flags & ~BSRA_FLAG_PDL) return fail(BSRA_EINVAL, "unknown flag bits");
+  if (c.flags & ~(BSRA_FLAG_PDL | BSRA_FLAG_RAGGED_KV)) return fail(BSRA_EINVAL, "unknown flag bits");
+  if ((c.flags & BSRA_FLAG_RAGGED_KV) && c.page_size != 128)
+    return fail(BSRA_EINVAL, "BSRA_FLAG_RAGGED_KV engines take page_size = 128 (the KV tile)");
   for (int i = 0; i < 6; ++i)
     if (c.reserved[i]) return fail(BSRA_EINVAL, "reserved fields must be zero");
   return BSRA_OK;
@@ -122,6 +124,7 @@ struct bsra_engine {
   bool counters_zeroed = false;
   float sm_scale = 0.f;
   int64_t total_qo = 0;
+  int64_t total_kv = 0;  // ragged KV: token extent of k / v (kv_indptr[batch])
   int32_t max_qo = 0;
   long long* trace = nullptr;  // debug: device buffer for kernel pipeline traces
   int32_t last_launches = 0;
@@ -241,20 +244,19 @@ bsra_status bsra_plan_host(const bsra_config* cfg, int32_t num_ctas, int32_t bat
   return BSRA_OK;
 }
 
-bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, const int32_t* kv_page_indptr,
-                      const int32_t* kv_last_page_len, float sm_scale, void* stream) {
-  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+namespace {
+
+// Shared inspector core: Algorithm 1 over (qo, kv) lengths; `page_begin` gives each request's
+// first BSR page (paged) or first token row (contiguous KV) for the plan's request table.
+bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* page_begin,
+                      const std::vector<int32_t>& qo, const std::vector<int32_t>& kv, float sm_scale, void* stream) {
   const bsra_config& c = e->cfg;
-  if (batch > c.max_batch) return fail(BSRA_EBOUNDS, "batch exceeds max_batch");
-  std::vector<int32_t> qo, kv;
-  std::string err = bsra::lengths_from_bsr(batch, qo_indptr, kv_page_indptr, kv_last_page_len, c.page_size, qo, kv);
-  if (!err.empty()) return fail(BSRA_EINVAL, err);
   int64_t rows = 0;
   for (int32_t x : qo) rows += x;
   if (rows > c.max_total_qo_rows) return fail(BSRA_EBOUNDS, "sum of qo lengths exceeds max_total_qo_rows");
   std::vector<int32_t> im;
   bsra::PlanSummary sum;
-  err = bsra::build_plan(sched_params(c, c.num_ctas), qo, kv, qo_indptr, kv_page_indptr, im, sum);
+  std::string err = bsra::build_plan(sched_params(c, c.num_ctas), qo, kv, qo_indptr, page_begin, im, sum);
   if (!err.empty()) return fail(BSRA_EINVAL, err);
   if (im.size() > e->lay.plan_words) return fail(BSRA_EBOUNDS, "plan image exceeds the workspace plan section");
   if (sum.T_q > e->lay.T_max) return fail(BSRA_EBOUNDS, "tile larger than the workspace partial slots");
@@ -276,6 +278,42 @@ bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, c
   e->total_qo = rows;
   e->max_qo = 0;
   for (int32_t x : qo) e->max_qo = std::max(e->max_qo, x);
+  return BSRA_OK;
+}
+
+}  // namespace
+
+bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, const int32_t* kv_page_indptr,
+                      const int32_t* kv_last_page_len, float sm_scale, void* stream) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  const bsra_config& c = e->cfg;
+  if (c.flags & BSRA_FLAG_RAGGED_KV) return fail(BSRA_EINVAL, "contiguous-KV engine: use bsra_plan_ragged");
+  if (batch > c.max_batch) return fail(BSRA_EBOUNDS, "batch exceeds max_batch");
+  std::vector<int32_t> qo, kv;
+  std::string err = bsra::lengths_from_bsr(batch, qo_indptr, kv_page_indptr, kv_last_page_len, c.page_size, qo, kv);
+  if (!err.empty()) return fail(BSRA_EINVAL, err);
+  return plan_core(e, qo_indptr, kv_page_indptr, qo, kv, sm_scale, stream);
+}
+
+bsra_status bsra_plan_ragged(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, const int32_t* kv_indptr,
+                             float sm_scale, void* stream) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  const bsra_config& c = e->cfg;
+  if (!(c.flags & BSRA_FLAG_RAGGED_KV)) return fail(BSRA_EINVAL, "paged engine: use bsra_plan (or create with BSRA_FLAG_RAGGED_KV)");
+  if (batch < 0) return fail(BSRA_EINVAL, "batch < 0");
+  if (batch > c.max_batch) return fail(BSRA_EBOUNDS, "batch exceeds max_batch");
+  if (batch > 0 && (!qo_indptr || !kv_indptr)) return fail(BSRA_EINVAL, "NULL indptr");
+  std::vector<int32_t> qo(batch), kv(batch);
+  if (batch > 0 && (qo_indptr[0] != 0 || kv_indptr[0] != 0)) return fail(BSRA_EINVAL, "indptr[0] != 0");
+  for (int32_t i = 0; i < batch; ++i) {
+    qo[i] = qo_indptr[i + 1] - qo_indptr[i];
+    kv[i] = kv_indptr[i + 1] - kv_indptr[i];
+    if (qo[i] < 0) return fail(BSRA_EINVAL, "qo_indptr not nondecreasing at " + std::to_string(i));
+    if (kv[i] < 0) return fail(BSRA_EINVAL, "kv_indptr not nondecreasing at " + std::to_string(i));
+  }
+  bsra_status s = plan_core(e, qo_indptr, kv_indptr, qo, kv, sm_scale, stream);
+  if (s) return s;
+  e->total_kv = batch > 0 ? kv_indptr[batch] : 0;
   return BSRA_OK;
 }
 
@@ -313,16 +351,19 @@ bsra_status launch_contraction_d(const bsra::AttnParams& p, int D, int grid, cud
 
 }  // namespace
 
-bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const void* v_pool, const int64_t* k_strides,
-                     const int64_t* v_strides, const int32_t* kv_page_indices, const uint8_t* custom_mask,
+namespace {
+
+// Shared executor core. Paged: k_strides = (page, slot, head) and the BSR page ids. Contiguous KV
+// (ragged): k_strides = (token, token, head), no page ids; token t of request i is row
+// kv_indptr[i] + t (the plan's page_begin).
+bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const void* v_pool, const int64_t* k_strides,
+                     const int64_t* v_strides, const int32_t* kv_page_indices, bool ragged, const uint8_t* custom_mask,
                      const int64_t* mask_bit_indptr, void* o, float* lse, void* stream) {
-  if (!e) return fail(BSRA_EINVAL, "NULL engine");
   if (!e->planned) return fail(BSRA_EINVAL, "run() before plan()");
   const bsra_config& c = e->cfg;
   e->last_launches = 0;
-  if (!k_strides || !v_strides) return fail(BSRA_EINVAL, "NULL strides");
   const bool has_rows = e->summary.n_items > 0;
-  if (has_rows && (!q || !k_pool || !v_pool || !kv_page_indices || !o))
+  if (has_rows && (!q || !k_pool || !v_pool || (!ragged && !kv_page_indices) || !o))
     return fail(BSRA_EINVAL, "NULL tensor pointer");
   if (c.mask == BSRA_MASK_CUSTOM && has_rows && (!custom_mask || !mask_bit_indptr))
     return fail(BSRA_EINVAL, "MASK_CUSTOM needs custom_mask and mask_bit_indptr");
@@ -348,6 +389,7 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
   p.vs1 = v_strides[1];
   p.vs2 = v_strides[2];
   p.page_indices = kv_page_indices;
+  p.kv_ragged = ragged ? 1 : 0;
   p.mask = custom_mask;
   p.mask_indptr = mask_bit_indptr;
   p.o = o;
@@ -386,6 +428,8 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
     tl.max_qo = e->max_qo;
     tl.mask = c.mask;
     tl.pdl = (c.flags & BSRA_FLAG_PDL) != 0;
+    tl.ragged = ragged;
+    tl.total_kv = e->total_kv;
     const char* why = "";
     int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
     if (rc < 0)
@@ -413,6 +457,29 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
     e->last_launches = 2;
   }
   return BSRA_OK;
+}
+
+}  // namespace
+
+bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const void* v_pool, const int64_t* k_strides,
+                     const int64_t* v_strides, const int32_t* kv_page_indices, const uint8_t* custom_mask,
+                     const int64_t* mask_bit_indptr, void* o, float* lse, void* stream) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  if (e->cfg.flags & BSRA_FLAG_RAGGED_KV) return fail(BSRA_EINVAL, "contiguous-KV engine: use bsra_run_ragged");
+  if (!k_strides || !v_strides) return fail(BSRA_EINVAL, "NULL strides");
+  return run_core(e, q, k_pool, v_pool, k_strides, v_strides, kv_page_indices, false, custom_mask, mask_bit_indptr, o,
+                  lse, stream);
+}
+
+bsra_status bsra_run_ragged(bsra_engine* e, const void* q, const void* k, const void* v, const int64_t* k_strides,
+                            const int64_t* v_strides, const uint8_t* custom_mask, const int64_t* mask_bit_indptr,
+                            void* o, float* lse, void* stream) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  if (!(e->cfg.flags & BSRA_FLAG_RAGGED_KV)) return fail(BSRA_EINVAL, "paged engine: use bsra_run");
+  if (!k_strides || !v_strides) return fail(BSRA_EINVAL, "NULL strides");
+  const int64_t ks[3] = {k_strides[0], k_strides[0], k_strides[1]};
+  const int64_t vs[3] = {v_strides[0], v_strides[0], v_strides[1]};
+  return run_core(e, q, k, v, ks, vs, nullptr, true, custom_mask, mask_bit_indptr, o, lse, stream);
 }
 
 int32_t bsra_last_run_launches(const bsra_engine* e) { return e ? e->last_launches : 0; }

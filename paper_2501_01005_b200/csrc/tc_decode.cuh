@@ -152,6 +152,8 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();  // PDL: the next kernel's CTAs may take SMs this grid releases
+  // debug (p.trace set): per-CTA start / end time, globaltimer ns (scripts/cta_balance.py)
+  if (p.trace && threadIdx.x == 0) p.trace[16 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
 
   if (warp == 0) {
     // ============================ TMA producer ============================
@@ -187,8 +189,12 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         int page = 0, off = 0;
         if (lane < nsub) {
           const int64_t tok = t0 + (int64_t)lane * B;
-          page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
-          off = (int)(tok % p.page_size);
+          if (p.kv_ragged) {  // contiguous KV: token coordinate, no page table
+            off = (int)(d.page_begin + tok);
+          } else {
+            page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
+            off = (int)(tok % p.page_size);
+          }
         }
         if (lane == 0) {
           ptx::mbar_wait(&empty[stage], ephase);
@@ -448,6 +454,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (p.trace && threadIdx.x == 0) p.trace[17 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
   if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 

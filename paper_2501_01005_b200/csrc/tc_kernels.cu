@@ -43,11 +43,12 @@ bool make_q_map(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, in
 
 // paged pool: element (page, slot, head, d) at page*s0 + slot*s1 + head*s2 + d (elements).
 // 4-D view ordered (d, head, slot, page) — coordinates in that order — box (64, 1, B, 1).
-bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int page_size, int64_t s0, int64_t s1,
-                   int64_t s2, int B) {
+// Contiguous KV uses the same view with slot = token (extent N, clipped there) and one page.
+bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int64_t page_size, int64_t s0, int64_t s1,
+                   int64_t s2, int B, int64_t npages = 0x7fffffff) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[4] = {128, (cuuint64_t)H_kv, (cuuint64_t)page_size, (cuuint64_t)0x7fffffff};
+  cuuint64_t dims[4] = {128, (cuuint64_t)H_kv, (cuuint64_t)std::max<int64_t>(page_size, 1), (cuuint64_t)npages};
   cuuint64_t strides[3] = {(cuuint64_t)s2 * 2, (cuuint64_t)s1 * 2, (cuuint64_t)s0 * 2};
   cuuint32_t box[4] = {64, 1, (cuuint32_t)B, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
@@ -90,9 +91,13 @@ cudaError_t launch_decode(int kc, int mask, const TcParams& tp, int grid, cudaSt
 bool make_q_map_ext(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, int hb, int tb) {
   return make_q_map(m, q, f16, H_qo, N, hb, tb);
 }
-bool make_pool_map_ext(CUtensorMap* m, const void* pool, bool f16, int H_kv, int page_size, int64_t s0, int64_t s1,
-                       int64_t s2, int B) {
-  return make_pool_map(m, pool, f16, H_kv, page_size, s0, s1, s2, B);
+// K and V maps for a launch: paged pools, or contiguous KV (token extent L.total_kv, one page)
+bool make_kv_maps(TcParams& tp, const AttnParams& p, const TcLaunch& L, int B) {
+  if (L.ragged)
+    return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.total_kv, p.ks1, p.ks1, p.ks2, B, 1) &&
+           make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.total_kv, p.vs1, p.vs1, p.vs2, B, 1);
+  return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.page_size, p.ks0, p.ks1, p.ks2, B) &&
+         make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.page_size, p.vs0, p.vs1, p.vs2, B);
 }
 
 int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const char** name, const char** why) {
@@ -101,9 +106,12 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
   const int g = p.g;
   if (!is_pow2(g)) { *why = "group size not a power of two"; return 0; }
   const int ps = L.page_size;
-  const int B = std::min(ps, 128);
-  if (!(ps >= 8 && (128 % ps == 0 || ps % 128 == 0))) { *why = "page size must divide 128 (>= 8) or be a multiple of 128"; return 0; }
-  if (L.align % B) { *why = "chunk alignment not a multiple of the page box"; return 0; }
+  // contiguous KV: any tile start is one 128-token box at a token coordinate
+  const int B = L.ragged ? 128 : std::min(ps, 128);
+  if (!L.ragged) {
+    if (!(ps >= 8 && (128 % ps == 0 || ps % 128 == 0))) { *why = "page size must divide 128 (>= 8) or be a multiple of 128"; return 0; }
+    if (L.align % B) { *why = "chunk alignment not a multiple of the page box"; return 0; }
+  }
   if (L.T_q == 16) {
     TcParams tp;
     std::memset(&tp, 0, sizeof(tp));
@@ -113,9 +121,7 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     tp.q_tb = g <= 16 ? 16 / g : 1;
     tp.f16 = L.f16;
     tp.pdl = L.pdl;
-    if (!make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) ||
-        !make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, ps, p.ks0, p.ks1, p.ks2, B) ||
-        !make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, ps, p.vs0, p.vs1, p.vs2, B)) {
+    if (!make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) || !make_kv_maps(tp, p, L, B)) {
       *why = "cuTensorMapEncodeTiled failed";
       return -1;
     }

@@ -16,6 +16,8 @@ struct TcLaunch {
   int max_qo = 0;          // max l_qo of the current plan (live fused columns)
   int mask = 0;
   bool pdl = false;        // programmatic dependent launch (BSRA_FLAG_PDL)
+  bool ragged = false;     // contiguous KV [N, H_kv, D] (p.kv_ragged)
+  int64_t total_kv = 0;    // ragged: N, the token extent of k / v
 };
 
 // Launches the tcgen05 kernel for this plan if one applies (bf16/f16, D = 128, supported page

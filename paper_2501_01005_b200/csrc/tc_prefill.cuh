@@ -52,8 +52,12 @@ __device__ __forceinline__ void kv_tile_coords(const AttnParams& p, const DecIte
   off = 0;
   if (lane < nsub) {
     const int64_t tok = t0 + (int64_t)lane * B;
-    page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
-    off = (int)(tok % p.page_size);
+    if (p.kv_ragged) {  // contiguous KV: token coordinate, no page table
+      off = (int)(d.page_begin + tok);
+    } else {
+      page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
+      off = (int)(tok % p.page_size);
+    }
   }
 }
 __device__ __forceinline__ void load_kv_tile(const CUtensorMap* tm, uint8_t* dst, uint64_t* bar, const DecItem& d,
@@ -442,8 +446,7 @@ inline cudaError_t launch_prefill_t(const TcParams& tp, int grid, cudaStream_t s
 }
 
 bool make_q_map_ext(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, int hb, int tb);
-bool make_pool_map_ext(CUtensorMap* m, const void* pool, bool f16, int H_kv, int page_size, int64_t s0, int64_t s1,
-                       int64_t s2, int B);
+bool make_kv_maps(TcParams& tp, const AttnParams& p, const TcLaunch& L, int B);
 
 inline int tc_prefill_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const char** name,
                              const char** why, int B) {
@@ -462,9 +465,7 @@ inline int tc_prefill_launch(const AttnParams& p, const TcLaunch& L, cudaStream_
   tp.pdl = L.pdl;
   static const int dbg = getenv("BSRA_DEBUG_PREFILL") ? atoi(getenv("BSRA_DEBUG_PREFILL")) : 0;
   tp.dbg = dbg;  // timing experiments only (never set in tests / bench)
-  if (!make_q_map_ext(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) ||
-      !make_pool_map_ext(&tp.tk, p.k, L.f16, p.H_kv, L.page_size, p.ks0, p.ks1, p.ks2, B) ||
-      !make_pool_map_ext(&tp.tv, p.v, L.f16, p.H_kv, L.page_size, p.vs0, p.vs1, p.vs2, B)) {
+  if (!make_q_map_ext(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) || !make_kv_maps(tp, p, L, B)) {
     *why = "cuTensorMapEncodeTiled failed";
     return -1;
   }

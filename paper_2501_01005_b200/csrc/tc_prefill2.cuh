@@ -243,7 +243,8 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
             n = cn[k];
             pb = cpb[k];
           }
-        if (j * B < n) page = __ldg(p.page_indices + pb + (t0 + j * B) / ps);
+        // paged: the sub-block's page id; contiguous KV: its token coordinate
+        if (j * B < n) page = p.kv_ragged ? (int)(pb + t0 + j * B) : __ldg(p.page_indices + pb + (t0 + j * B) / ps);
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -297,10 +298,12 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       if (D.w < 0) break;
       const int kvh = D.kvh, t0 = D.t0, n = D.n;
       const int nsub = (n + B - 1) / B;
-      const int page = lane < nsub ? D.page[lane] : 0;
+      const int pg = lane < nsub ? D.page[lane] : 0;
       // tiles start page-aligned (chunk alignment is a multiple of B), so sub-blocks of pages
-      // <= 128 tokens start at slot 0; only pages > 128 tokens need the in-page offset
-      const int off = ps <= kTile ? 0 : (t0 + lane * B) % ps;
+      // <= 128 tokens start at slot 0; only pages > 128 tokens need the in-page offset.
+      // Contiguous KV: the descriptor holds the token coordinate, the page coordinate is 0.
+      const int off = p.kv_ragged ? pg : ps <= kTile ? 0 : (t0 + lane * B) % ps;
+      const int page = p.kv_ragged ? 0 : pg;
       if (isK && (D.flags & 1) && lane == 0) {  // Q of the item's WG (paired: both halves)
         const int w = kPair ? 0 : D.w;
         for (int h = 0; h < (kPair ? 2 : 1); ++h) {

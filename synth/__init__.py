@@ -215,6 +215,42 @@ def make_inputs(wl: Workload, *, device="cpu", seed_base=0, permute=True, layout
                   float(sm_scale) if sm_scale is not None else 1.0 / float(np.sqrt(wl.D)))
 
 
+@dataclasses.dataclass
+class RaggedKV:
+    """The same keys / values as a paged Inputs, laid out contiguously:
+    request i's tokens are rows kv_indptr[i] .. kv_indptr[i+1]-1 of k / v [N, H_kv, D]."""
+    kv_indptr: np.ndarray  # int32 [B+1]
+    k: torch.Tensor
+    v: torch.Tensor
+    k_strides: tuple       # elements (token, head)
+    v_strides: tuple
+
+
+def ragged_kv(inp: Inputs) -> RaggedKV:
+    """Gathers a paged Inputs' K/V into contiguous ragged tensors (data movement only): token t
+    of request i is slot t mod B_c of page indices[kv_page_indptr[i] + t // B_c]."""
+    wl = inp.wl
+    ps = wl.page_size
+    kv_indptr = np.concatenate([[0], np.cumsum(wl.kv_lens.astype(np.int64))]).astype(np.int32)
+    idx = inp.kv_page_indices.cpu().numpy().astype(np.int64)
+    pages, slots = [], []
+    for i in range(wl.batch):
+        t = np.arange(int(wl.kv_lens[i]), dtype=np.int64)
+        pages.append(idx[inp.kv_page_indptr[i] + t // ps])
+        slots.append(t % ps)
+    pg = torch.from_numpy(np.concatenate(pages) if pages else np.zeros(0, np.int64)).to(inp.k_pool.device)
+    sl = torch.from_numpy(np.concatenate(slots) if slots else np.zeros(0, np.int64)).to(inp.k_pool.device)
+
+    def gather(pool, strides):
+        view = torch.as_strided(pool, (pool.numel() // max(1, strides[0]), ps, wl.H_kv, wl.D),
+                                (strides[0], strides[1], strides[2], 1))
+        return view[pg, sl].contiguous()
+
+    k, v = gather(inp.k_pool, inp.k_strides), gather(inp.v_pool, inp.v_strides)
+    st = (wl.H_kv * wl.D, wl.D)
+    return RaggedKV(kv_indptr, k, v, st, st)
+
+
 def raw_bits(t: torch.Tensor) -> np.ndarray:
     """Host numpy view of a tensor's storage: float32 stays float32, 16-bit types as uint16 bits."""
     t = t.detach().cpu().contiguous()
