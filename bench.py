@@ -29,8 +29,18 @@ import torch
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-# stdout carries exactly one JSON line: keep NCCL's version banner / info off it
 os.environ["NCCL_DEBUG"] = os.environ.get("BSRA_NCCL_DEBUG", "WARN")
+# stdout carries exactly one JSON line. Anything a library prints to the process's stdout (NCCL's
+# version banner is printed at WARN level) goes to stderr: fd 1 is pointed at fd 2, and the JSON
+# line is written through a duplicate of the original stdout.
+_JSON_OUT = os.fdopen(os.dup(1), "w")
+sys.stdout.flush()
+os.dup2(2, 1)
+
+
+def emit(obj) -> None:
+    _JSON_OUT.write(json.dumps(obj) + "\n")
+    _JSON_OUT.flush()
 
 import synth  # noqa: E402
 
@@ -292,6 +302,47 @@ def time_graph(fn, s, reps, warmup=3):
     return a.elapsed_time(b) / reps
 
 
+def bench_contiguous(dev, pk, reps=9):
+    """the page table's cost. The same keys / values as a paged pool
+    (permuted 16-token pages, the workload) and as contiguous ragged tensors (BSRA_FLAG_RAGGED_KV),
+    per-launch CUDA events (median), configs[1] decode and configs[2] prefill."""
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts)) * 1e3
+
+    import paper_2501_01005_b200 as bsra
+    out = {"unit": "us per launch", "paper": "App. B (P:443-447): <= 1 % decode, ~10 % prefill on H100/FA3"}
+    for key, wl, tq in (("decode_c2", synth.c2_decode_llama8b(), 16), ("prefill_c3", synth.c3_prefill_llama70b(), 0)):
+        inp = synth.make_inputs(wl, device=dev)
+        nq = int(wl.qo_lens.sum())
+        kw = dict(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, dtype=wl.dtype, mask=wl.mask, max_batch=wl.batch,
+                  max_total_qo_rows=nq, num_ctas=148, tile_q=tq)
+        o = torch.empty((nq, wl.H_qo, wl.D), device=dev, dtype=torch.bfloat16)
+        lse = torch.empty((nq, wl.H_qo), device=dev)
+        pe = bsra.Engine(bsra.make_config(page_size=wl.page_size, **kw), torch.cuda.current_device())
+        pe.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+        paged = timed(lambda: pe.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides,
+                                     inp.kv_page_indices, o, lse))
+        rk = synth.ragged_kv(inp)
+        re_ = bsra.Engine(bsra.make_config(page_size=128, ragged_kv=True, **kw), torch.cuda.current_device())
+        re_.plan_ragged(inp.qo_indptr, rk.kv_indptr, inp.sm_scale)
+        contig = timed(lambda: re_.run_ragged(inp.q, rk.k, rk.v, rk.k_strides, rk.v_strides, o, lse))
+        out[key] = {"paged_us": paged, "contiguous_us": contig,
+                    "page_table_overhead_pct": 100.0 * (paged / contig - 1.0)}
+        del inp, rk, pe, re_, o, lse
+        torch.cuda.empty_cache()
+    return out
+
+
 def bench_composable(dev, pk, layers=16, reps=20):
     """configs[3]: 8K shared prefix + 64 branches x 256-token suffixes, one decode step per layer
     through ComposableDecode (prefix engine on tensor-core tiles + suffix engine + ⊕), every layer
@@ -440,14 +491,14 @@ def run_reference(args, world, rank):
     el = (time.perf_counter() - t0) / args.steps
     val = by / el / 1e12
     sample = f"requests 0,4,...,124 (32 of 128) of configs[1], one layer per step"
-    print(json.dumps({
+    emit({
         "impl": "reference", "metric": "paged decode HBM TB/s (configs[1], Llama-3-8B shape, batch 128)",
         "value": val, "unit": "TB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": "c2_decode_llama8b (sampled)", "global_batch": 32},
         "cpu_baseline": {"value": val, "unit": "TB/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": val, "unit": "TB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    })
 
 
 def main():
@@ -465,6 +516,7 @@ def main():
     ap.add_argument("--prefill-tile", type=int, default=0, help="force T_q for the prefill line (0 = heuristic)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-composable", action="store_true")
+    ap.add_argument("--no-contiguous", action="store_true", help="skip the paged-vs-contiguous KV line")
     ap.add_argument("--no-long", action="store_true")
     ap.add_argument("--no-pdl", action="store_true")
     args = ap.parse_args()
@@ -553,6 +605,11 @@ def main():
         composable = bench_composable(dev, pk)
         torch.cuda.empty_cache()
 
+    contiguous = None
+    if not args.no_contiguous and world == 1:
+        torch.cuda.empty_cache()
+        contiguous = bench_contiguous(dev, pk)
+
     long_ctx = None
     if not args.no_long:
         try:
@@ -582,10 +639,10 @@ def main():
                        "graph": not args.no_graph},
             "frac_of_hbm_peak": value / world * 1e3 / pk["hbm_gbs"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "prefill": prefill,
-            "composable": composable, "long_context": long_ctx,
+            "composable": composable, "long_context": long_ctx, "contiguous_kv": contiguous,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         }
-        print(json.dumps(out))
+        emit(out)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
