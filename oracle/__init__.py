@@ -53,8 +53,8 @@ def _load():
         lib.orc_paged_attention.restype = ctypes.c_int
         lib.orc_paged_attention.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P,
-                                            ctypes.c_int, P, P, ctypes.c_double, P, ctypes.c_int, P, P,
-                                            ctypes.c_int]
+                                            ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                            P, ctypes.c_int, P, P, ctypes.c_int]
         lib.orc_merge.restype = None
         lib.orc_merge.argtypes = [ctypes.c_int64, ctypes.c_int, P, P, P, P, P, P]
         lib.orc_decode.restype = ctypes.c_double
@@ -73,8 +73,8 @@ def decode_scalar(dtype: str, bits: int) -> float:
 
 def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
                     k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
-                    mask_bit_indptr=None, sm_scale, req_list: Optional[Sequence[int]] = None,
-                    num_threads: int = 0, out=None):
+                    mask_bit_indptr=None, sm_scale, window: int = 0, soft_cap: float = 0.0,
+                    req_list: Optional[Sequence[int]] = None, num_threads: int = 0, out=None):
     """float64 oracle (C). Array arguments are host numpy arrays; ``q``/pools hold raw
     element bits (float32, or uint16 bits for f16/bf16). Returns (o, lse) float64 with
     shapes [sum l_qo, H_qo, D] and [sum l_qo, H_qo]. With ``req_list`` only those requests
@@ -102,7 +102,8 @@ def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indi
     rc = lib.orc_paged_attention(batch, _ptr(qo_indptr), _ptr(kv_page_indptr), _ptr(kv_last_page_len),
                                  _ptr(kv_page_indices), H_qo, H_kv, D, page_size, DT_CODE[dtype], _ptr(q),
                                  _ptr(k_pool), _ptr(v_pool), _ptr(ks), _ptr(vs), MASK_CODE[mask], _ptr(cm),
-                                 _ptr(mb), float(sm_scale), _ptr(rl), 0 if rl is None else len(rl), _ptr(o),
+                                 _ptr(mb), float(sm_scale), int(window), float(soft_cap), _ptr(rl),
+                                 0 if rl is None else len(rl), _ptr(o),
                                  _ptr(lse), int(num_threads))
     if rc != 0:
         raise ValueError(f"orc_paged_attention failed with code {rc}")
@@ -119,8 +120,8 @@ def attention_from_inputs(inp, req_list=None, num_threads=0):
         v_pool=raw_bits(inp.v_pool), k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo,
         H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
         custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
-        mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, req_list=req_list,
-        num_threads=num_threads)
+        mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap,
+        req_list=req_list, num_threads=num_threads)
 
 
 # ------------------------------------------------------------- brute force ---
@@ -136,9 +137,11 @@ def to_float64(bits: np.ndarray, dtype: str) -> np.ndarray:
 
 def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
                 k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
-                mask_bit_indptr=None, sm_scale):
+                mask_bit_indptr=None, sm_scale, window=0, soft_cap=0.0):
     """NumPy brute force (tiny inputs): dense un-paged K/V per request, the full masked
-    score matrix, float64 softmax. Same definition as the C oracle, different code."""
+    score matrix, float64 softmax. Same definition as the C oracle, different code.
+    Variants (PAPER.md:228): window W > 0 keeps keys t >= l_kv - l_qo + r - W + 1 (R26);
+    soft_cap c > 0 maps the scaled scores through c * tanh(S / c) (R27)."""
     qf = to_float64(q, dtype).reshape(-1, H_qo, D)
     kflat = to_float64(k_pool, dtype).reshape(-1)
     vflat = to_float64(v_pool, dtype).reshape(-1)
@@ -170,6 +173,8 @@ def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices,
         Kr = np.repeat(Kd, g, axis=1)  # GQA: head h uses kv head h // g
         Vr = np.repeat(Vd, g, axis=1)
         S = sm_scale * np.einsum("rhd,thd->hrt", qf[q0:q1], Kr)  # [H, lq, lk]
+        if soft_cap > 0:
+            S = soft_cap * np.tanh(S / soft_cap)
         if mask == "none":
             vis = np.ones((lq, lk), bool)
         elif mask == "causal":
@@ -177,6 +182,8 @@ def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices,
         else:
             b0 = int(mask_bit_indptr[i])
             vis = bits[b0:b0 + lq * lk].reshape(lq, lk)
+        if window > 0:
+            vis = vis & (np.arange(lk)[None, :] >= (lk - lq + np.arange(lq) - window + 1)[:, None])
         S = np.where(vis[None], S, -np.inf)
         m = S.max(axis=2, initial=-np.inf, keepdims=True)
         msafe = np.where(np.isfinite(m), m, 0.0)
@@ -199,7 +206,7 @@ def brute_force_from_inputs(inp):
         v_pool=raw_bits(inp.v_pool), k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo,
         H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
         custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
-        mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale)
+        mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap)
 
 
 # --------------------------------------------------------------------- ⊕ ---

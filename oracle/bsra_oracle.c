@@ -18,6 +18,10 @@
  *   - Visible set vis(r): NONE: all t; CAUSAL (right aligned, R4):
  *     t <= l_kv - l_qo + r; CUSTOM (R9): bit mask_bit_indptr[i] + r*l_kv + t,
  *     LSB-first in bytes. Masked pairs are skipped, not -inf arithmetic (R10).
+ *   - LogitsMask variant, sliding window (§3.2.3; R26): window W > 0
+ *     additionally hides t < l_kv - l_qo + r - W + 1 (W keys up to the row's own position).
+ *   - LogitsTransform variant, logits soft-cap (R27): cap c > 0 replaces
+ *     the scaled logit s by c * tanh(s / c) before Eq. 1-2.
  *   - Eq. 1: lse = log sum_{t in vis} exp(s_t), s_t = sm_scale * q.k_t
  *     (R1: the logits are scaled by sm_scale; R2: natural log).
  *   - Eq. 2: o = sum_{t in vis} exp(s_t) / exp(lse) * v_t
@@ -95,8 +99,9 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
                         int H_qo, int H_kv, int D, int page_size, int dtype, const void* q,
                         const void* k_pool, const void* v_pool, const int64_t* k_strides,
                         const int64_t* v_strides, int mask_mode, const uint8_t* custom_mask,
-                        const int64_t* mask_bit_indptr, double sm_scale, const int32_t* req_list,
-                        int n_req_list, double* o_out, double* lse_out, int num_threads) {
+                        const int64_t* mask_bit_indptr, double sm_scale, int window, double soft_cap,
+                        const int32_t* req_list, int n_req_list, double* o_out, double* lse_out,
+                        int num_threads) {
   if (batch < 0 || H_qo <= 0 || H_kv <= 0 || H_qo % H_kv != 0 || D <= 0 || page_size <= 0) return 1;
   if (mask_mode == ORC_MASK_CUSTOM && (!custom_mask || !mask_bit_indptr)) return 2;
   const int g = H_qo / H_kv;
@@ -159,6 +164,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
           int64_t j = mask_bit_indptr[i] + (int64_t)r * l_kv + t;
           visible = (custom_mask[j >> 3] >> (j & 7)) & 1;
         }
+        if (window > 0 && t < l_kv - l_qo + r - window + 1) visible = 0;
         if (visible) vis[nv++] = (int32_t)t;
       }
       const int64_t row = (int64_t)qo_indptr[i] + r;
@@ -180,6 +186,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
           double dot = 0.0;
           for (int d = 0; d < D; ++d) dot += orc_load(q, dtype, qbase + d) * orc_load(k_pool, dtype, kb + d);
           s[a] = sm_scale * dot;
+          if (soft_cap > 0.0) s[a] = soft_cap * tanh(s[a] / soft_cap);
           if (s[a] > m) m = s[a];
         }
         /* pass 2: normaliser, lse, output (Eq. 1-2) */

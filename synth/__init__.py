@@ -43,6 +43,8 @@ class Workload:
     mask: str
     qo_lens: np.ndarray  # int32 [B]
     kv_lens: np.ndarray  # int32 [B]
+    window: int = 0       # sliding window W (0 = off), R26
+    soft_cap: float = 0.0  # logits soft-cap c (0 = off), R27
 
     @property
     def batch(self) -> int:

@@ -392,3 +392,85 @@ def test_negative_control_dropped_page_is_detected():
         v_strides=bad.v_strides, H_qo=4, H_kv=1, D=32, page_size=4, dtype="f32", sm_scale=bad.sm_scale)
     assert np.max(np.abs(ob - o)) > 1e-2 or np.max(np.abs(lb - l)) > 1e-3
     del wl2
+
+
+# ------------------------------------------- attention variants (NEXT-3)
+def _with_variant(wl, window=0, soft_cap=0.0):
+    import dataclasses
+    return dataclasses.replace(wl, window=window, soft_cap=soft_cap)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_variants_c_oracle_matches_numpy_brute_force(seed):
+    """Sliding window (R26) and logits soft-cap (R27) in the C oracle against the NumPy brute
+    force (dense scores, different code), every mask mode."""
+    rng = np.random.default_rng(5000 + seed)
+    wl = synth.random_workload(rng, dtype=["f32", "bf16"][seed % 2], mask=synth.MASKS[seed % 3])
+    wl = _with_variant(wl, window=int(rng.integers(1, 40)) if seed % 4 != 3 else 0,
+                       soft_cap=[0.0, 1.5, 7.0, 30.0][seed % 4])
+    inp = _inp(wl, seed_base=seed, q_scale=[1.0, 4.0][seed % 2])
+    _cmp(_run(inp), oracle.brute_force_from_inputs(inp), 1e-12)
+
+
+@pytest.mark.parametrize("mask", ["none", "causal"])
+def test_window_covering_everything_is_no_window(mask):
+    """W >= l_kv + l_qo hides nothing: bit-identical to the plain oracle."""
+    wl = synth.random_workload(np.random.default_rng(7), dtype="f32", mask=mask)
+    big = int(wl.kv_lens.max() + wl.qo_lens.max() + 1)
+    a = _run(_inp(wl))
+    b = _run(_inp(_with_variant(wl, window=big)))
+    assert np.array_equal(a[0], b[0], equal_nan=True) and np.array_equal(a[1], b[1], equal_nan=True)
+
+
+def test_causal_window_one_is_the_diagonal():
+    """Causal + W = 1: row r sees only its own position p = l_kv - l_qo + r, so o = v_p and
+    lse = sm_scale * q.k_p (closed form)."""
+    rng = np.random.default_rng(11)
+    lq, lk, H, D = 5, 9, 2, 16
+    q = rng.standard_normal((lq, H, D))
+    K = rng.standard_normal((lk, H, D))
+    V = rng.uniform(-1, 1, (lk, H, D))
+    args = _single_request(q, K, V, page_size=4, mask="causal", sm_scale=0.3)
+    o, lse = oracle.paged_attention(**args, window=1)
+    qf, Kf, Vf = (x.astype(np.float32).astype(np.float64) for x in (q, K, V))
+    for r in range(lq):
+        p = lk - lq + r
+        for h in range(H):
+            assert np.allclose(o[r, h], Vf[p, h], atol=1e-15)
+            assert abs(lse[r, h] - 0.3 * float(qf[r, h] @ Kf[p, h])) < 1e-12
+
+
+def test_window_equals_custom_mask_bits():
+    """A window is a LogitsMask: NONE + window W equals CUSTOM with the bits
+    t >= l_kv - l_qo + r - W + 1 (the oracle's custom-mask path, a different branch)."""
+    wl = synth.Workload("w", 8, 2, 32, 4, "f32", "none", np.array([3, 7, 1], np.int32),
+                        np.array([10, 7, 30], np.int32))
+    W = 4
+    inp_w = _inp(_with_variant(wl, window=W))
+    bits, indptr = [], [0]
+    for lq, lk in zip(wl.qo_lens, wl.kv_lens):
+        m = np.arange(lk)[None, :] >= (lk - lq + np.arange(lq) - W + 1)[:, None]
+        bits.append(m.reshape(-1))
+        indptr.append(indptr[-1] + lq * lk)
+    packed = np.packbits(np.concatenate(bits).astype(np.uint8), bitorder="little")
+    inp_c = _inp(synth.Workload("w", 8, 2, 32, 4, "f32", "custom", wl.qo_lens, wl.kv_lens),
+                 mask_bits=(packed, np.array(indptr, np.int64)))
+    a, b = _run(inp_w), _run(inp_c)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_soft_cap_closed_forms():
+    """Two keys with scaled logits s1, s2 and cap c: lse = ln(e^{c tanh(s1/c)} + e^{c tanh(s2/c)})
+    and o the matching convex combination; a cap far above the logits changes nothing."""
+    q = np.array([[[1.0, 0.0, 0.0, 0.0]]])
+    K = np.array([[[0.5, 0, 0, 0]], [[-2.0, 0, 0, 0]]])
+    V = np.array([[[1.0, 2.0, 3.0, 4.0]], [[-1.0, 0.5, 0.0, 2.0]]])
+    for c in (0.7, 3.0):
+        o, lse = oracle.paged_attention(**_single_request(q, K, V, sm_scale=1.0), soft_cap=c)
+        z1, z2 = c * math.tanh(0.5 / c), c * math.tanh(-2.0 / c)
+        assert abs(lse[0, 0] - math.log(math.exp(z1) + math.exp(z2))) < 1e-14
+        w1 = math.exp(z1) / (math.exp(z1) + math.exp(z2))
+        assert np.allclose(o[0, 0], w1 * V[0, 0] + (1 - w1) * V[1, 0], atol=1e-14)
+    a = oracle.paged_attention(**_single_request(q, K, V, sm_scale=1.0), soft_cap=1e9)
+    b = oracle.paged_attention(**_single_request(q, K, V, sm_scale=1.0))
+    assert np.allclose(a[0], b[0], atol=1e-15) and abs(a[1][0, 0] - b[1][0, 0]) < 1e-15
