@@ -72,7 +72,13 @@ typedef struct {
   int32_t kv_chunk_min;      /* floor for the chunk size L_kv; 0 => none                        */
   int32_t kernel;            /* bsra_kernel                                                     */
   int32_t flags;             /* BSRA_FLAG_* bits                                                */
-  int32_t reserved[6];       /* must be zero                                                    */
+  /* Attention variants (the paper's LogitsMask / LogitsTransform functors; compiled
+   * in, no JIT). 0 = off. */
+  int32_t sliding_window;    /* W > 0: row at position p = l_kv - l_qo + r also hides keys
+                                t < p - W + 1 (W keys up to its own position; R26).
+                                Algorithm 1 then starts each row's KV range at its window       */
+  float logits_soft_cap;     /* c > 0: scaled logit s -> c * tanh(s / c) (R27)        */
+  int32_t reserved[4];       /* must be zero                                                    */
 } bsra_config;
 
 /* flags: BSRA_FLAG_PDL launches the tcgen05 kernels with programmatic dependent launch: a run()

@@ -59,7 +59,7 @@ class Plan:
 
 
 def plan_ref(qo_lens, kv_lens, *, g, H_kv, mask=MASK_NONE, num_ctas, tile_set=(16, 64, 128, 256),
-             alpha=1, beta=1, align=1, L_min=0, T_q=None, qo_begin=None, page_begin=None) -> Plan:
+             alpha=1, beta=1, align=1, L_min=0, T_q=None, qo_begin=None, page_begin=None, window=0) -> Plan:
     qo_lens = [int(x) for x in qo_lens]
     kv_lens = [int(x) for x in kv_lens]
     B = len(qo_lens)
@@ -67,8 +67,10 @@ def plan_ref(qo_lens, kv_lens, *, g, H_kv, mask=MASK_NONE, num_ctas, tile_set=(1
         raise ValueError("num_ctas >= 1")
     if T_q is None:
         T_q = select_tile(qo_lens, g, tile_set)
-    # --- rows (request, kv head, q tile) and their effective kv length
-    rows = []  # (i, h, t, e)
+    # --- rows (request, kv head, q tile) and their effective kv range [b, e): e is the causal-
+    # effective end (R13); with a sliding window W (R26) the tile's first row sees nothing
+    # before p - W + 1, so b is that bound rounded down to the chunk alignment
+    rows = []  # (i, h, t, b, e)
     for i in range(B):
         lq, lk = qo_lens[i], kv_lens[i]
         fused = lq * g
@@ -80,16 +82,21 @@ def plan_ref(qo_lens, kv_lens, *, g, H_kv, mask=MASK_NONE, num_ctas, tile_set=(1
                     e = min(max(lk - lq + last_tok + 1, 0), lk)
                 else:
                     e = lk
-                rows.append((i, h, t, e))
-    total = sum(r[3] for r in rows)
+                b = 0
+                if window > 0:
+                    first_tok = (t * T_q) // g
+                    b = max(0, lk - lq + first_tok - window + 1)
+                    b = min((b // align) * align, e)
+                rows.append((i, h, t, b, e))
+    total = sum(r[4] - r[3] for r in rows)
     L = max(ceil_div(total, num_ctas), L_min, 1)
     L = ceil_div(L, align) * align
     # --- chunks, work index w in (row, j) order
     chunks = []  # (w, row_idx, j, begin, end)
-    for ri, (i, h, t, e) in enumerate(rows):
-        n = max(1, ceil_div(e, L))
+    for ri, (i, h, t, b, e) in enumerate(rows):
+        n = max(1, ceil_div(e - b, L))
         for j in range(n):
-            chunks.append((len(chunks), ri, j, j * L, min((j + 1) * L, e)))
+            chunks.append((len(chunks), ri, j, b + j * L, min(b + (j + 1) * L, e)))
     # --- slots: DIRECT for unsplit rows, consecutive slots (j asc) for split rows
     nchunk_of_row = [0] * len(rows)
     for c in chunks:
@@ -98,7 +105,7 @@ def plan_ref(qo_lens, kv_lens, *, g, H_kv, mask=MASK_NONE, num_ctas, tile_set=(1
     lists = []
     nslot = 0
     first_chunk = 0
-    for ri, (i, h, t, e) in enumerate(rows):
+    for ri, (i, h, t, _b, _e) in enumerate(rows):
         n = nchunk_of_row[ri]
         if n > 1:
             sl = []
@@ -122,7 +129,7 @@ def plan_ref(qo_lens, kv_lens, *, g, H_kv, mask=MASK_NONE, num_ctas, tile_set=(1
     for c in range(num_ctas):
         for w in queues[c]:
             _, ri, j, b, e = chunks[w]
-            i, h, t, _ = rows[ri]
+            i, h, t, _, _ = rows[ri]
             items.append((i, h, t, b, e, slot_of[w]))
         cta_indptr.append(len(items))
     image = encode_image(num_ctas, T_q, L, items, cta_indptr, lists, nslot, B, g, H_kv, mask, qo_lens,

@@ -37,7 +37,8 @@ class Config(ctypes.Structure):
                 ("num_ctas", ctypes.c_int32), ("tile_set_mask", ctypes.c_int32), ("tile_q", ctypes.c_int32),
                 ("cost_alpha", ctypes.c_int64), ("cost_beta", ctypes.c_int64), ("kv_chunk_align", ctypes.c_int32),
                 ("kv_chunk_min", ctypes.c_int32), ("kernel", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 6)]
+                ("sliding_window", ctypes.c_int32), ("logits_soft_cap", ctypes.c_float),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 FLAG_PDL = 1  # BSRA_FLAG_PDL (include/bsra.h)
@@ -110,8 +111,11 @@ def _i32(a) -> np.ndarray:
 
 def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="none", max_batch=1,
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
-                kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False) -> Config:
+                kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False, window=0,
+                soft_cap=0.0) -> Config:
+    """window: sliding window W (0 = off, R26); soft_cap: logits soft-cap c (0 = off, R27)."""
     c = Config()
+    c.sliding_window, c.logits_soft_cap = int(window), float(soft_cap)
     c.flags = (FLAG_PDL if pdl else 0) | (FLAG_RAGGED_KV if ragged_kv else 0)
     c.num_qo_heads, c.num_kv_heads, c.head_dim, c.page_size = H_qo, H_kv, D, page_size
     c.dtype = DTYPE[dtype] if isinstance(dtype, str) else dtype

@@ -68,7 +68,10 @@ bsra_status validate_config(const bsra_config& c) {
   if (c.flags & ~(BSRA_FLAG_PDL | BSRA_FLAG_RAGGED_KV)) return fail(BSRA_EINVAL, "unknown flag bits");
   if ((c.flags & BSRA_FLAG_RAGGED_KV) && c.page_size != 128)
     return fail(BSRA_EINVAL, "BSRA_FLAG_RAGGED_KV engines take page_size = 128 (the KV tile)");
-  for (int i = 0; i < 6; ++i)
+  if (c.sliding_window < 0) return fail(BSRA_EINVAL, "sliding_window < 0");
+  if (!(c.logits_soft_cap >= 0.f) || !std::isfinite(c.logits_soft_cap))
+    return fail(BSRA_EINVAL, "logits_soft_cap must be finite and >= 0");
+  for (int i = 0; i < 4; ++i)
     if (c.reserved[i]) return fail(BSRA_EINVAL, "reserved fields must be zero");
   return BSRA_OK;
 }
@@ -220,6 +223,7 @@ static bsra::SchedParams sched_params(const bsra_config& c, int32_t num_ctas) {
   sp.beta = c.cost_beta ? c.cost_beta : 1;
   sp.align = c.kv_chunk_align ? c.kv_chunk_align : c.page_size;
   sp.L_min = c.kv_chunk_min;
+  sp.window = c.sliding_window;
   return sp;
 }
 

@@ -89,7 +89,7 @@ std::string build_plan(const SchedParams& p, const std::vector<int32_t>& qo_len,
   const int64_t alpha = p.alpha, beta = p.beta;
 
   // ---- rows (request, kv head, q tile) and their effective KV length e
-  struct Row { int32_t i, h, t; int64_t e; };
+  struct Row { int32_t i, h, t; int64_t b, e; };
   std::vector<Row> rows;
   for (int32_t i = 0; i < B; ++i) {
     const int64_t lq = qo_len[i], lk = kv_len[i];
@@ -103,12 +103,20 @@ std::string build_plan(const SchedParams& p, const std::vector<int32_t>& qo_len,
           const int64_t last_tok = cdiv(hi, g) - 1;
           e = std::min(std::max(lk - lq + last_tok + 1, (int64_t)0), lk);
         }
-        rows.push_back({i, h, (int32_t)t, e});
+        // sliding window (R26): nothing before the first row's p - W + 1 is visible;
+        // the range starts there, rounded down to the chunk alignment (page-aligned tiles)
+        int64_t b = 0;
+        if (p.window > 0) {
+          const int64_t first_tok = (t * T_q) / g;
+          b = std::max<int64_t>(0, lk - lq + first_tok - p.window + 1);
+          b = std::min(b / std::max(1, p.align) * std::max(1, p.align), e);
+        }
+        rows.push_back({i, h, (int32_t)t, b, e});
       }
     }
   }
   int64_t total = 0;
-  for (const Row& r : rows) total += r.e;
+  for (const Row& r : rows) total += r.e - r.b;
   int64_t L = std::max<int64_t>(std::max<int64_t>(cdiv(total, p.num_ctas), p.L_min), 1);
   const int64_t align = std::max(1, p.align);
   L = cdiv(L, align) * align;
@@ -119,10 +127,12 @@ std::string build_plan(const SchedParams& p, const std::vector<int32_t>& qo_len,
   std::vector<Chunk> chunks;
   std::vector<int32_t> row_first(rows.size()), row_n(rows.size());
   for (size_t r = 0; r < rows.size(); ++r) {
-    const int64_t n = std::max<int64_t>(1, cdiv(rows[r].e, L));
+    const int64_t b = rows[r].b;
+    const int64_t n = std::max<int64_t>(1, cdiv(rows[r].e - b, L));
     row_first[r] = (int32_t)chunks.size();
     row_n[r] = (int32_t)n;
-    for (int64_t j = 0; j < n; ++j) chunks.push_back({(int32_t)r, (int32_t)j, j * L, std::min((j + 1) * L, rows[r].e)});
+    for (int64_t j = 0; j < n; ++j)
+      chunks.push_back({(int32_t)r, (int32_t)j, b + j * L, std::min(b + (j + 1) * L, rows[r].e)});
   }
 
   // ---- writethrough (App. D.2) and partial slots / merge lists for split rows

@@ -30,6 +30,7 @@ struct SchedParams {
   int64_t alpha = 1, beta = 1;
   int32_t align = 1;           // chunk alignment in tokens
   int32_t L_min = 0;
+  int32_t window = 0;          // sliding window W (0 = off): rows start at p - W + 1, aligned down
 };
 
 struct PlanSummary {

@@ -40,15 +40,16 @@ MASKS = {0: "none", 1: "causal", 2: "custom"}
 
 
 def _compare(qo, kv, *, H_qo, H_kv, ps, mask, num_ctas, tiles=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
-             align=0, L_min=0):
+             align=0, L_min=0, window=0):
     qi, ki, last = _bsr(qo, kv, ps)
     cfg = bsra.make_config(H_qo=H_qo, H_kv=H_kv, D=128, page_size=ps, dtype="bf16", mask=MASKS[mask],
                            max_batch=len(qo), max_total_qo_rows=int(sum(qo)), num_ctas=num_ctas, tile_set=tiles,
-                           tile_q=tile_q, alpha=alpha, beta=beta, kv_chunk_align=align, kv_chunk_min=L_min)
+                           tile_q=tile_q, alpha=alpha, beta=beta, kv_chunk_align=align, kv_chunk_min=L_min,
+                           window=window)
     img_c = bsra.plan_host(cfg, num_ctas, qi, ki, last)
     ref = S.plan_ref(qo, kv, g=H_qo // H_kv, H_kv=H_kv, mask=mask, num_ctas=num_ctas, tile_set=tiles,
                      alpha=alpha, beta=beta, align=align or ps, L_min=L_min, T_q=tile_q or None,
-                     qo_begin=qi[:-1], page_begin=ki[:-1])
+                     qo_begin=qi[:-1], page_begin=ki[:-1], window=window)
     assert img_c.dtype == np.int32
     assert np.array_equal(img_c, ref.image), (len(img_c), len(ref.image))
     return img_c
@@ -79,8 +80,9 @@ def test_cpp_scheduler_bit_exact_vs_python(seed):
     align = 0 if seed % 7 else int(rng.choice([1, 8, 32]))
     L_min = 0 if seed % 11 else int(rng.integers(1, 500))
     tiles = [(16, 64, 128), (16, 128), (64,), (128,), (16,), (16, 64, 128, 256), (256,)][seed % 7]
+    window = 0 if seed % 3 else int(rng.choice([1, 7, 64, 1000, 5000]))  # sliding window (R26)
     _compare(qo, kv, H_qo=H_kv * g, H_kv=H_kv, ps=ps, mask=mask, num_ctas=num_ctas, tiles=tiles, alpha=alpha,
-             beta=beta, align=align, L_min=L_min)
+             beta=beta, align=align, L_min=L_min, window=window)
 
 
 @pytest.mark.parametrize("name,qo,kv,H,ps,mask,nc", [

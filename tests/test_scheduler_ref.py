@@ -143,3 +143,42 @@ def test_image_header_and_layout():
     assert im[5] == len(p.items) and im[6] == len(p.lists) and im[7] == p.n_slots
     expect = S.HEADER_WORDS + 4 + 6 * len(p.items) + len(p.lists) + 1 + p.n_slots + 3 * len(p.lists) + 4 * 2
     assert im.size == expect
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_window_plan_covers_every_visible_key(seed):
+    """Sliding window (R26) in Algorithm 1, checked from the definition: for every fused row of
+    every (request, kv head, q tile), the keys it can see (mask AND t >= p - W + 1) lie inside the
+    union of the tile's items; each tile's items are disjoint, contiguous, at most L long, start
+    on the chunk alignment, and cost the scheduler no more than the windowless plan."""
+    rng = np.random.default_rng(9000 + seed)
+    B = int(rng.integers(1, 12))
+    g = int(rng.choice([1, 4, 8]))
+    H_kv = int(rng.choice([1, 2]))
+    mask = int(rng.integers(0, 3))
+    kv = rng.integers(0, 3000, B)
+    qo = rng.integers(0, 3, B) if seed % 2 else rng.integers(1, 200, B)
+    if mask == S.MASK_CAUSAL:
+        kv = np.maximum(kv, qo)
+    W = int(rng.choice([1, 5, 64, 500, 4000]))
+    align = int(rng.choice([1, 16, 128]))
+    nc = int(rng.choice([1, 8, 148]))
+    p = S.plan_ref(qo, kv, g=g, H_kv=H_kv, mask=mask, num_ctas=nc, align=align, window=W)
+    by_row = {}
+    for it in p.items:
+        by_row.setdefault(it[:3], []).append(it)
+    for (i, h, t), its in by_row.items():
+        its = sorted(its, key=lambda x: x[3])
+        for a, b in zip(its, its[1:]):
+            assert a[4] == b[3]
+        assert its[0][3] % align == 0 and all(x[4] - x[3] <= p.L for x in its)
+        lo_cov, hi_cov = its[0][3], its[-1][4]
+        lq, lk = int(qo[i]), int(kv[i])
+        for f in range(t * p.T_q, min((t + 1) * p.T_q, lq * g)):
+            pos = lk - lq + f // g
+            vis_lo = max(0, pos - W + 1)
+            vis_hi = min(pos + 1, lk) if mask == S.MASK_CAUSAL else lk
+            if vis_hi > vis_lo:
+                assert lo_cov <= vis_lo and vis_hi <= hi_cov, (i, h, t, f, lo_cov, hi_cov, vis_lo, vis_hi)
+    full = S.plan_ref(qo, kv, g=g, H_kv=H_kv, mask=mask, num_ctas=nc, align=align)
+    assert sum(x[4] - x[3] for x in p.items) <= sum(x[4] - x[3] for x in full.items)
