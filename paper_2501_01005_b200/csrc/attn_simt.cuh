@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
         bool vis = valid && lane < n;
         if (vis && p.mask_mode == 1) vis = t <= causal_lim;
         if (vis && p.mask_mode == 2) vis = mask_bit(p.mask, mbase + t);
+        if (vis && p.window > 0) vis = t >= causal_lim - p.window + 1;  // sliding window (R26)
         float s = -INFINITY;
         if (vis) {
           const uint4* krow = reinterpret_cast<const uint4*>(sk[st] + lane * S::kRowBytes);
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
 #pragma unroll
             for (int e = 0; e < kVecN; ++e) dot = fmaf(qv[c * kVecN + e], kf[e], dot);
           }
-          s = dot * p.scale_log2;
+          s = (p.soft_cap > 0.f ? soft_cap_raw(p, dot) : dot) * p.scale_log2;  // soft-cap (R27)
         }
         const float mt = warp_max(s);
         const float mnew = fmaxf(m, mt);

@@ -33,9 +33,25 @@ struct AttnParams {
   // k/v [N, H_kv, D] (page_begin = kv_indptr[i]); no page table. The tcgen05 kernels address it
   // through a pool map whose token dimension is N (TMA clips at the buffer end).
   int32_t kv_ragged;
+  // Attention variants (R26 / R27), 0 = off. window: sliding window W, a
+  // row at position p hides keys t < p - W + 1. soft_cap: c / sm_scale, the cap in raw q.k units,
+  // so the transformed raw score cap * tanh(s / cap) goes through the same scale-and-exp path.
+  int32_t window;
+  float soft_cap, inv_soft_cap;
   int32_t H_qo, H_kv, g, page_size, mask_mode, o_f32, T_slot, D;
   float scale_log2;  // sm_scale * log2(e)
 };
+
+// LogitsTransform soft-cap on a raw score (R27): s -> c * tanh(s / c), c in raw units.
+// tanh x = 1 - 2 / (2^(2x log2 e) + 1): one ex2 and one rcp (absolute error ~1e-7, i.e. ~c*1e-7
+// in the logit; tanh.approx.f32's 2^-11 relative error would exceed the lse tolerance at c = 50).
+// Saturates correctly: x -> +inf gives 1, x -> -inf gives -1.
+__device__ __forceinline__ float soft_cap_raw(const AttnParams& p, float s) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(s * p.inv_soft_cap * 2.8853900817779268f));  // 2 log2(e)
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.f));
+  return p.soft_cap * fmaf(-2.f, r, 1.f);
+}
 
 struct PlanView {
   int32_t num_ctas, T_q, L, n_items, n_lists, n_slots, batch, g, H_kv, mask;

@@ -394,6 +394,10 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   p.vs2 = v_strides[2];
   p.page_indices = kv_page_indices;
   p.kv_ragged = ragged ? 1 : 0;
+  p.window = c.sliding_window;
+  // soft-cap in raw q.k units: c * tanh(sm_scale*s / c) = sm_scale * c' tanh(s / c'), c' = c / sm_scale
+  p.soft_cap = c.logits_soft_cap > 0.f ? c.logits_soft_cap / e->sm_scale : 0.f;
+  p.inv_soft_cap = c.logits_soft_cap > 0.f ? e->sm_scale / c.logits_soft_cap : 0.f;
   p.mask = custom_mask;
   p.mask_indptr = mask_bit_indptr;
   p.o = o;

@@ -317,7 +317,9 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           bool vis = tok_ok && c < d.nrows;
           if (kMask == 1) vis = vis && t <= lim[c];
           if (kMask == 2) vis = vis && mask_bit(p.mask, lim[c] + t);
-          s[c] = vis ? s[c] * p.scale_log2 : -INFINITY;
+          if (p.window > 0) vis = vis && t >= d.lk - d.lq + (d.row0 + c) / g - p.window + 1;  // R26
+          const float sc = p.soft_cap > 0.f ? soft_cap_raw(p, s[c]) : s[c];                // R27
+          s[c] = vis ? sc * p.scale_log2 : -INFINITY;
         }
         float mx[kC];
 #pragma unroll

@@ -130,7 +130,9 @@ struct Interleave {
 // kPair = true:  T_q = 256; both WGs run the same item, WG w on fused rows [128w, 128w + 128), so
 //                every K/V tile staged in smem feeds 256 query rows (half the L2->smem bytes per
 //                flop of the streamed form, which the no-compute timing mode showed to be the bound).
-template <int kMask, bool kPair, bool kF16>
+// kVar: attention variants on (sliding window / soft-cap, read from p at run time); the default
+// instantiation compiles them out so the plain path carries none of their per-tile work.
+template <int kMask, bool kPair, bool kF16, bool kVar>
 __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __grid_constant__ TcParams tp) {
   using namespace pre2;
   const AttnParams& p = tp.p;
@@ -539,13 +541,18 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       const int tok = f / g, head = d.kvh * g + f % g;
       const int64_t lim = kMask == 1 ? d.lk - d.lq + tok : d.ke - 1;
       const int64_t mbase = kMask == 2 ? p.mask_indptr[d.req] + (int64_t)tok * d.lk : 0;
+      // variants: sliding-window lower bound of this row (R26), soft-cap (R27) — both go through
+      // the general (per-element) path; plain tiles keep the fast path
+      const int64_t wlo = kVar && p.window > 0 ? d.lk - d.lq + tok - p.window + 1 : INT64_MIN / 2;
+      const bool capped = kVar && p.soft_cap > 0.f;
       float m = -INFINITY, l = 0.f;
       for (int ti = 0; ti < d.ntiles; ++ti) {
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
         const int n = (int)imin64(kTile, d.ke - t0);
         const int64_t vis_end = row_ok ? (kMask == 1 ? imin64(lim + 1, t0 + n) : t0 + n) : t0;
         const int nvis = (int)(vis_end > t0 ? vis_end - t0 : 0);
-        const bool need_mask = kMask == 2 || nvis < kTile;
+        const int vbeg = kVar && wlo > t0 ? (int)imin64(wlo - t0, kTile) : 0;  // first visible column
+        const bool need_mask = kMask == 2 || nvis < kTile || vbeg > 0 || capped;
         ptx::mbar_wait(&bar_s[w], sph);
         sph ^= 1;
         if (r == 0) BSRA_TRACE(5 + 2 * w, tcount);
@@ -567,7 +574,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           if (need_mask) {
 #pragma unroll
             for (int j = 0; j < 64; ++j) {
-              bool vis = c * 32 + j < nvis;
+              bool vis = c * 32 + j < nvis && c * 32 + j >= vbeg;
               if (kMask == 2) vis = vis && mask_bit(p.mask, mbase + t0 + c * 32 + j);
               s[j] = vis ? s[j] : -INFINITY;
             }
@@ -582,7 +589,8 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           }
           mx = fmaxf(mx, fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
         }
-        const float mt = mx * sc;
+        // soft-cap is monotone, so the capped max is the cap of the raw max (-inf stays -inf)
+        const float mt = (capped && mx != -INFINITY ? soft_cap_raw(p, mx) : mx) * sc;
         float alpha = 1.f;
         bool rescale = false;
         if (mt > m + kRescaleThresh) {
@@ -622,9 +630,9 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           if (need_mask) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              bool vis = c * 32 + j < nvis;
+              bool vis = c * 32 + j < nvis && c * 32 + j >= vbeg;
               if (kMask == 2) vis = vis && mask_bit(p.mask, mbase + t0 + c * 32 + j);
-              s[j] = vis ? s[j] : -INFINITY;
+              s[j] = vis ? (capped ? soft_cap_raw(p, s[j]) : s[j]) : -INFINITY;
             }
           }
           uint32_t pk[16];
@@ -735,21 +743,28 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 
-template <int kMask, bool kPair, bool kF16>
+template <int kMask, bool kPair, bool kF16, bool kVar>
 inline cudaError_t launch_prefill2_f(const TcParams& tp, int grid, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_prefill2_kernel<kMask, kPair, kF16>,
+    cudaError_t e = cudaFuncSetAttribute(tc_prefill2_kernel<kMask, kPair, kF16, kVar>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, pre2::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_tc(tc_prefill2_kernel<kMask, kPair, kF16>, grid, pre2::kThreads, pre2::kSmemBytes, st, tp);
+  return launch_tc(tc_prefill2_kernel<kMask, kPair, kF16, kVar>, grid, pre2::kThreads, pre2::kSmemBytes, st, tp);
+}
+
+template <int kMask, bool kPair, bool kF16>
+inline cudaError_t launch_prefill2_v(const TcParams& tp, int grid, cudaStream_t st) {
+  const bool var = tp.p.window > 0 || tp.p.soft_cap > 0.f;
+  return var ? launch_prefill2_f<kMask, kPair, kF16, true>(tp, grid, st)
+             : launch_prefill2_f<kMask, kPair, kF16, false>(tp, grid, st);
 }
 
 template <int kMask, bool kPair>
 inline cudaError_t launch_prefill2_t(const TcParams& tp, int grid, cudaStream_t st) {
-  return tp.f16 ? launch_prefill2_f<kMask, kPair, true>(tp, grid, st) : launch_prefill2_f<kMask, kPair, false>(tp, grid, st);
+  return tp.f16 ? launch_prefill2_v<kMask, kPair, true>(tp, grid, st) : launch_prefill2_v<kMask, kPair, false>(tp, grid, st);
 }
 
 }  // namespace bsra
