@@ -53,6 +53,19 @@ constexpr int kSmemBytes = kOffDesc + kDesc * 96 + 1024 + BSRA_PRE2_PAD;
 constexpr int kThreads = 384;  // warps 0 Q+K producer, 1 V producer, 2 MMA, 3 scheduler, 4-7 WG0, 8-11 WG1
 constexpr uint32_t kTmemCols = 512;  // S/P_w at w*128, O_w at 256 + w*128
 constexpr float kRescaleThresh = 8.f;
+#ifndef BSRA_PRE2_REGS_LOW
+#define BSRA_PRE2_REGS_LOW 96
+#endif
+constexpr int kRegsLow = BSRA_PRE2_REGS_LOW;         // warpgroup 0 (producers, MMA, scheduler)
+// The pool is what the CTA was launched with (168 per thread x 384 threads), not the SM's 64K:
+// an inc the released registers cannot cover blocks forever.
+constexpr int kRegsLaunch = 168;
+// one-pass softmax (S held in registers, one TMEM read per tile) — needs the register split
+#ifndef BSRA_PRE2_ONEPASS
+#define BSRA_PRE2_ONEPASS 1
+#endif
+constexpr int kRegsHigh = (3 * kRegsLaunch - kRegsLow) / 2 / 8 * 8;  // each softmax warpgroup
+static_assert(128 * kRegsLow + 256 * kRegsHigh <= 384 * kRegsLaunch, "register split exceeds the CTA's pool");
 // exp2 split between the MUFU (4/clk/SMSP) and a cubic on the FMA pipes: kEmuPairs of every 8
 // element pairs take the polynomial (FA4's exp2 emulation)
 #ifndef BSRA_PRE2_EMU
@@ -186,6 +199,8 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();  // PDL: the next kernel's CTAs may take SMs this grid releases
+  // register split (each role branch below): warpgroup 0 (producers, MMA issuer, scheduler)
+  // gives registers to the two softmax warpgroups (128 x kRegsLow + 256 x kRegsHigh = 64K)
   const int B = tp.box_tok;
   // item streams: 2 (one per softmax WG); 1 when paired (both WGs on every item) or in the
   // one-WG timing experiment
@@ -199,6 +214,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   if (p.trace && threadIdx.x == 0) p.trace[16 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
 
   if (warp == 3) {
+    ptx::setmaxnreg_dec<kRegsLow>();
     // ===================== scheduler: interleaved tile descriptors =====================
     Interleave il;
     il.init(pv, g, it0, it1, nstream);
@@ -279,6 +295,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       ptx::mbar_arrive(&desc_full[slot]);
     }
   } else if (warp == 0 || warp == 1) {
+    ptx::setmaxnreg_dec<kRegsLow>();
     // ===================== producers: warp 0 = Q + K, warp 1 = V =====================
     const bool isK = warp == 0;
     if (lane == 0) {
@@ -344,6 +361,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       }
     }
   } else if (warp == 2) {
+    ptx::setmaxnreg_dec<kRegsLow>();
     // ===================== MMA issuer =====================
     const uint32_t fmt = tp.f16 ? 0u : 1u;
     const uint32_t idS = ptx::idesc_f16(fmt, 128, kTile, 0, 0);  // A = Q (K-major), B = K (K-major)
@@ -521,6 +539,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       }
     }
   } else if (warp >= 4) {
+    ptx::setmaxnreg_inc<kRegsHigh>();
     // ===================== softmax warpgroups =====================
     const int w = (warp - 4) >> 2;        // WG index
     const int q4 = warp & 3;              // TMEM lane quarter
@@ -563,6 +582,89 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           ++tcount;
           continue;
         }
+        // the variant instantiation keeps the two-pass form (the soft-cap needs the registers)
+        constexpr bool kOnePass = BSRA_PRE2_ONEPASS && !kVar;
+        if constexpr (kOnePass) {
+        // ---- one pass (registers from setmaxnreg): all 128 S columns in one TMEM round trip,
+        // mask / soft-cap, row max, P = 2^(s*scale - m) packed to 16-bit pairs over the consumed
+        // S columns; the rare O rescale goes after P (O_w is quiescent until p_ready)
+        float s[128];
+        ptx::tmem_ld32(tS, s);
+        ptx::tmem_ld32(tS + 32, s + 32);
+        ptx::tmem_ld32(tS + 64, s + 64);
+        ptx::tmem_ld32(tS + 96, s + 96);
+        ptx::tmem_ld_wait();
+        if (need_mask) {
+#pragma unroll
+          for (int j = 0; j < 128; ++j) {
+            bool vis = j < nvis && j >= vbeg;
+            if (kMask == 2) vis = vis && mask_bit(p.mask, mbase + t0 + j);
+            s[j] = vis ? (capped ? soft_cap_raw(p, s[j]) : s[j]) : -INFINITY;
+          }
+        }
+        float a0 = fmaxf(s[0], s[1]), a1 = fmaxf(s[2], s[3]), a2 = fmaxf(s[4], s[5]), a3 = fmaxf(s[6], s[7]);
+#pragma unroll
+        for (int j = 8; j < 128; j += 4) {
+          a0 = fmaxf(a0, s[j]);
+          a1 = fmaxf(a1, s[j + 1]);
+          a2 = fmaxf(a2, s[j + 2]);
+          a3 = fmaxf(a3, s[j + 3]);
+        }
+        const float mt = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)) * sc;
+        float alpha = 1.f;
+        bool rescale = false;
+        if (mt > m + kRescaleThresh) {
+          if (m != -INFINITY) {
+            alpha = ptx_ex2(m - mt);
+            rescale = true;
+          }
+          m = mt;
+        }
+        const float mneg = m == -INFINITY ? 0.f : -m;
+        const float2 sc2 = make_float2(sc, sc), mn2 = make_float2(mneg, mneg);
+        const float2 mn2h = make_float2(mneg - 0.5f, mneg - 0.5f);  // poly_ex2x2_shifted takes x - 1/2
+        float2 rs[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            float2 x;
+            const float2 sv = make_float2(s[c * 32 + j], s[c * 32 + j + 1]);
+            if (((j >> 1) & 7) < kEmuPairs) {  // kEmuPairs of every 8 pairs on the FMA pipes
+              x = poly_ex2x2_shifted(__ffma2_rn(sv, sc2, mn2h));
+            } else {
+              x = __ffma2_rn(sv, sc2, mn2);
+              x.x = ptx_ex2(x.x);
+              x.y = ptx_ex2(x.y);
+            }
+            rs[(j >> 1) & 3] = __fadd2_rn(rs[(j >> 1) & 3], x);
+            if constexpr (kF16) {
+              __half2 h = __floats2half2_rn(x.x, x.y);
+              pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h);
+            } else {
+              __nv_bfloat162 h = __floats2bfloat162_rn(x.x, x.y);
+              pk[j >> 1] = *reinterpret_cast<uint32_t*>(&h);
+            }
+          }
+          ptx::tmem_st16(tS + c * 16, pk);
+        }
+        if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float ov[32];
+            ptx::tmem_ld32(tO + c * 32, ov);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ov[j] *= alpha;
+            uint32_t* ou = reinterpret_cast<uint32_t*>(ov);
+            ptx::tmem_st16(tO + c * 32, ou);
+            ptx::tmem_st16(tO + c * 32 + 16, ou + 16);
+          }
+        }
+        const float2 r01 = __fadd2_rn(rs[0], rs[1]), r23 = __fadd2_rn(rs[2], rs[3]);
+        l = l * alpha + ((r01.x + r01.y) + (r23.x + r23.y));
+        } else {
         // ---- pass 1: raw row max (two 32-column TMEM loads in flight per round trip)
         float mx = (tp.dbg & 16) ? 0.f : -INFINITY;  // dbg 16: timing experiment, no max pass
 #pragma unroll
@@ -660,6 +762,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         }
         const float2 r01 = __fadd2_rn(rs[0], rs[1]), r23 = __fadd2_rn(rs[2], rs[3]);
         l = l * alpha + ((r01.x + r01.y) + (r23.x + r23.y));
+        }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_ready[w]);
