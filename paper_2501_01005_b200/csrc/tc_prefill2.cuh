@@ -69,7 +69,7 @@ static_assert(128 * kRegsLow + 256 * kRegsHigh <= 384 * kRegsLaunch, "register s
 // exp2 split between the MUFU (4/clk/SMSP) and a cubic on the FMA pipes: kEmuPairs of every 8
 // element pairs take the polynomial (FA4's exp2 emulation)
 #ifndef BSRA_PRE2_EMU
-#define BSRA_PRE2_EMU 2
+#define BSRA_PRE2_EMU 0
 #endif
 constexpr int kEmuPairs = BSRA_PRE2_EMU;
 }  // namespace pre2
