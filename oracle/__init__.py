@@ -14,6 +14,10 @@ Contents
   * ``merge`` / ``merge_all``   ⊕ of attention states, float64.
   * ``split_attention``   P contiguous KV shards, each through the oracle, merged in order.
   * ``scheduler_ref``     Algorithm 1 re-implemented in Python.
+  * fp8 KV cache          (App. F): K/V stored as OCP E4M3 bytes, q/o in
+                          fp16/bf16; element value = scale * E4M3(byte) (R28). Both the
+                          C oracle (own decoder) and the brute force (NumPy decoder written from
+                          the format definition) take ``kv_dtype="e4m3"``, ``k_scale``, ``v_scale``.
 
 Every function that has no independent pin says so ("parity unpinned") in its
 docstring; see DESIGN.md §Oracle.
@@ -32,7 +36,7 @@ _SO = os.path.join(_HERE, "liborc.so")
 _SRC = os.path.join(_HERE, "bsra_oracle.c")
 _lib = None
 
-DT_CODE = {"f32": 0, "f16": 1, "bf16": 2}
+DT_CODE = {"f32": 0, "f16": 1, "bf16": 2, "e4m3": 3}
 MASK_CODE = {"none": 0, "causal": 1, "custom": 2}
 
 
@@ -52,7 +56,8 @@ def _load():
         P = ctypes.c_void_p
         lib.orc_paged_attention.restype = ctypes.c_int
         lib.orc_paged_attention.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, ctypes.c_int,
-                                            ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, P, P,
+                                            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_double, ctypes.c_double, P, P, P, P, P,
                                             ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                             P, ctypes.c_int, P, P, ctypes.c_int]
         lib.orc_merge.restype = None
@@ -74,9 +79,12 @@ def decode_scalar(dtype: str, bits: int) -> float:
 def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
                     k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
                     mask_bit_indptr=None, sm_scale, window: int = 0, soft_cap: float = 0.0,
+                    kv_dtype: Optional[str] = None, k_scale: float = 1.0, v_scale: float = 1.0,
                     req_list: Optional[Sequence[int]] = None, num_threads: int = 0, out=None):
     """float64 oracle (C). Array arguments are host numpy arrays; ``q``/pools hold raw
-    element bits (float32, or uint16 bits for f16/bf16). Returns (o, lse) float64 with
+    element bits (float32, uint16 bits for f16/bf16, uint8 bytes for e4m3 pools).
+    ``kv_dtype`` (default: ``dtype``) is the pools' dtype; K/V values are scaled by
+    ``k_scale`` / ``v_scale`` (the fp8 KV cache). Returns (o, lse) float64 with
     shapes [sum l_qo, H_qo, D] and [sum l_qo, H_qo]. With ``req_list`` only those requests
     are computed (other rows stay NaN)."""
     lib = _load()
@@ -100,7 +108,8 @@ def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indi
     k_pool = np.asarray(k_pool)
     v_pool = np.asarray(v_pool)
     rc = lib.orc_paged_attention(batch, _ptr(qo_indptr), _ptr(kv_page_indptr), _ptr(kv_last_page_len),
-                                 _ptr(kv_page_indices), H_qo, H_kv, D, page_size, DT_CODE[dtype], _ptr(q),
+                                 _ptr(kv_page_indices), H_qo, H_kv, D, page_size, DT_CODE[dtype],
+                                 DT_CODE[kv_dtype or dtype], float(k_scale), float(v_scale), _ptr(q),
                                  _ptr(k_pool), _ptr(v_pool), _ptr(ks), _ptr(vs), MASK_CODE[mask], _ptr(cm),
                                  _ptr(mb), float(sm_scale), int(window), float(soft_cap), _ptr(rl),
                                  0 if rl is None else len(rl), _ptr(o),
@@ -121,12 +130,28 @@ def attention_from_inputs(inp, req_list=None, num_threads=0):
         H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
         custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
         mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap,
+        kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale,
         req_list=req_list, num_threads=num_threads)
 
 
 # ------------------------------------------------------------- brute force ---
+def e4m3_to_float64(bits: np.ndarray) -> np.ndarray:
+    """OCP FP8 E4M3 bytes -> float64, vectorised from the format definition (R28):
+    bias 7; exponent field 0 is subnormal (m/8 * 2^-6); S.1111.111 is NaN; no infinities.
+    Independent of the C decoder (table-free, different code)."""
+    b = np.asarray(bits, np.uint8).astype(np.int64)
+    sign = np.where(b & 0x80, -1.0, 1.0)
+    e = (b >> 3) & 0xF
+    m = (b & 0x7).astype(np.float64)
+    mag = np.where(e == 0, (m / 8.0) * 2.0 ** -6, (1.0 + m / 8.0) * np.exp2(e.astype(np.float64) - 7.0))
+    mag = np.where((e == 15) & ((b & 7) == 7), np.nan, mag)
+    return sign * mag
+
+
 def to_float64(bits: np.ndarray, dtype: str) -> np.ndarray:
     """Exact upcast via numpy's own float types (independent of the C decoders)."""
+    if dtype == "e4m3":
+        return e4m3_to_float64(bits)
     if dtype == "f32":
         return np.asarray(bits, np.float32).astype(np.float64)
     if dtype == "f16":
@@ -137,14 +162,15 @@ def to_float64(bits: np.ndarray, dtype: str) -> np.ndarray:
 
 def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
                 k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
-                mask_bit_indptr=None, sm_scale, window=0, soft_cap=0.0):
+                mask_bit_indptr=None, sm_scale, window=0, soft_cap=0.0, kv_dtype=None, k_scale=1.0, v_scale=1.0):
     """NumPy brute force (tiny inputs): dense un-paged K/V per request, the full masked
     score matrix, float64 softmax. Same definition as the C oracle, different code.
+    fp8 KV: pools of ``kv_dtype`` scaled by k_scale / v_scale.
     Variants (PAPER.md:228): window W > 0 keeps keys t >= l_kv - l_qo + r - W + 1 (R26);
     soft_cap c > 0 maps the scaled scores through c * tanh(S / c) (R27)."""
     qf = to_float64(q, dtype).reshape(-1, H_qo, D)
-    kflat = to_float64(k_pool, dtype).reshape(-1)
-    vflat = to_float64(v_pool, dtype).reshape(-1)
+    kflat = k_scale * to_float64(k_pool, kv_dtype or dtype).reshape(-1)
+    vflat = v_scale * to_float64(v_pool, kv_dtype or dtype).reshape(-1)
     g = H_qo // H_kv
     nq = int(qo_indptr[-1])
     o = np.zeros((nq, H_qo, D))
@@ -206,7 +232,8 @@ def brute_force_from_inputs(inp):
         v_pool=raw_bits(inp.v_pool), k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo,
         H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
         custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
-        mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap)
+        mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap,
+        kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale)
 
 
 # --------------------------------------------------------------------- ⊕ ---
@@ -260,6 +287,7 @@ def split_attention(inp, P: int, num_threads=0):
             kv_last_page_len=np.array(last, np.int32), kv_page_indices=np.concatenate(sel).astype(np.int32),
             q=raw_bits(inp.q), k_pool=raw_bits(inp.k_pool), v_pool=raw_bits(inp.v_pool),
             k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D,
-            page_size=wl.page_size, dtype=wl.dtype, sm_scale=inp.sm_scale, num_threads=num_threads)
+            page_size=wl.page_size, dtype=wl.dtype, sm_scale=inp.sm_scale, kv_dtype=wl.kv_dtype or wl.dtype,
+            k_scale=inp.k_scale, v_scale=inp.v_scale, num_threads=num_threads)
         states.append((o, lse))
     return merge_all(states)

@@ -27,6 +27,10 @@
  *   - Eq. 2: o = sum_{t in vis} exp(s_t) / exp(lse) * v_t
  *     (evaluated max-shifted: m = max s_t, Z = sum exp(s_t - m), lse = m + ln Z).
  *   - Empty vis: o = 0, lse = -inf (R3).
+ *   - FP8-FP16 mixed precision (App. F): "the query and output remain in
+ *     fp16, while the KV-Cache is stored in fp8". K/V may be stored as OCP FP8 E4M3 (kv_dtype 3;
+ *     DESIGN.md R28): element value = k_scale * E4M3(byte) (v_scale for V), a per-tensor scale
+ *     (1 = the plain format). Nothing else changes: Eq. 1-2 run on the dequantised values.
  *
  * Inputs are the same arrays given to bsra_plan / bsra_run, copied to the host.
  * fp32 / fp16 / bf16 values are upcast exactly to double here (own decoders).
@@ -39,7 +43,7 @@
 #include <omp.h>
 #endif
 
-enum { ORC_F32 = 0, ORC_F16 = 1, ORC_BF16 = 2 };
+enum { ORC_F32 = 0, ORC_F16 = 1, ORC_BF16 = 2, ORC_E4M3 = 3 };
 enum { ORC_MASK_NONE = 0, ORC_MASK_CAUSAL = 1, ORC_MASK_CUSTOM = 2 };
 
 /* IEEE binary16 -> double, exact (normal, subnormal, inf, nan). */
@@ -66,10 +70,28 @@ static double orc_bf16_to_double(uint16_t b) {
   return (double)f;
 }
 
+/* OCP FP8 E4M3 ("E4M3FN") -> double, exact: 1 sign, 4 exponent (bias 7), 3 mantissa bits; no
+ * infinities, S.1111.111 is NaN, largest finite 448 (R28). */
+static double orc_e4m3_to_double(uint8_t b) {
+  int sign = (b >> 7) & 1;
+  int exp = (b >> 3) & 0xf;
+  int man = b & 0x7;
+  double v;
+  if (exp == 0) {
+    v = ldexp((double)man, -9); /* subnormal: (man / 8) * 2^(1-7) */
+  } else if (exp == 15 && man == 7) {
+    v = NAN;
+  } else {
+    v = ldexp((double)(man | 0x8), exp - 10); /* (1.man) * 2^(exp-7) */
+  }
+  return sign ? -v : v;
+}
+
 static double orc_load(const void* base, int dtype, int64_t idx) {
   switch (dtype) {
     case ORC_F32: return (double)((const float*)base)[idx];
     case ORC_F16: return orc_f16_to_double(((const uint16_t*)base)[idx]);
+    case ORC_E4M3: return orc_e4m3_to_double(((const uint8_t*)base)[idx]);
     default: return orc_bf16_to_double(((const uint16_t*)base)[idx]);
   }
 }
@@ -83,20 +105,23 @@ double orc_decode(int dtype, uint32_t bits) {
     memcpy(&f, &bits, sizeof f);
     return (double)f;
   }
+  if (dtype == ORC_E4M3) return orc_e4m3_to_double((uint8_t)bits);
   return dtype == ORC_F16 ? orc_f16_to_double((uint16_t)bits) : orc_bf16_to_double((uint16_t)bits);
 }
 
 /*
  * orc_paged_attention — returns 0 on success, nonzero on invalid input.
  *   q            [sum l_qo, H_qo, D] contiguous, dtype
- *   k_pool/v_pool element strides {page, token, head}; dim stride 1
+ *   k_pool/v_pool element strides {page, token, head}; dim stride 1; kv_dtype (pools' dtype,
+ *                ORC_E4M3 for the fp8 KV cache), values scaled by k_scale / v_scale
  *   req_list     optional list of request ids to compute (NULL => all); rows of
  *                other requests in o_out/lse_out are left untouched
  *   o_out        [sum l_qo, H_qo, D] double;  lse_out [sum l_qo, H_qo] double
  */
 int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_page_indptr,
                         const int32_t* kv_last_page_len, const int32_t* kv_page_indices,
-                        int H_qo, int H_kv, int D, int page_size, int dtype, const void* q,
+                        int H_qo, int H_kv, int D, int page_size, int dtype, int kv_dtype,
+                        double k_scale, double v_scale, const void* q,
                         const void* k_pool, const void* v_pool, const int64_t* k_strides,
                         const int64_t* v_strides, int mask_mode, const uint8_t* custom_mask,
                         const int64_t* mask_bit_indptr, double sm_scale, int window, double soft_cap,
@@ -184,7 +209,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
           const int64_t p = kv_page_indices[kv_page_indptr[i] + t / page_size];
           const int64_t kb = p * k_strides[0] + (t % page_size) * k_strides[1] + hk * k_strides[2];
           double dot = 0.0;
-          for (int d = 0; d < D; ++d) dot += orc_load(q, dtype, qbase + d) * orc_load(k_pool, dtype, kb + d);
+          for (int d = 0; d < D; ++d) dot += orc_load(q, dtype, qbase + d) * (k_scale * orc_load(k_pool, kv_dtype, kb + d));
           s[a] = sm_scale * dot;
           if (soft_cap > 0.0) s[a] = soft_cap * tanh(s[a] / soft_cap);
           if (s[a] > m) m = s[a];
@@ -199,7 +224,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
           const int64_t p = kv_page_indices[kv_page_indptr[i] + t / page_size];
           const int64_t vb = p * v_strides[0] + (t % page_size) * v_strides[1] + hk * v_strides[2];
           const double wgt = exp(s[a] - m) / Z;
-          for (int d = 0; d < D; ++d) o[d] += wgt * orc_load(v_pool, dtype, vb + d);
+          for (int d = 0; d < D; ++d) o[d] += wgt * (v_scale * orc_load(v_pool, kv_dtype, vb + d));
         }
       }
     }

@@ -26,7 +26,11 @@ from typing import Optional
 import numpy as np
 import torch
 
-DTYPES = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}
+DTYPES = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16, "e4m3": torch.float8_e4m3fn}
+# fp8 KV cache: per-tensor scales of the synthetic e4m3 pools. The stored byte is
+# the e4m3 rounding of value / scale, so the dequantised values keep the bf16 recipe's ranges
+# (k ~ N(0,1), v in [-1, 1]); deliberately not powers of two.
+KV_SCALE_E4M3 = (0.03, 0.011)
 MASKS = ("none", "causal", "custom")
 
 SEED_LEN, SEED_Q, SEED_K, SEED_V, SEED_PERM, SEED_MASK = 0, 1, 2, 3, 4, 5
@@ -45,6 +49,7 @@ class Workload:
     kv_lens: np.ndarray  # int32 [B]
     window: int = 0       # sliding window W (0 = off), R26
     soft_cap: float = 0.0  # logits soft-cap c (0 = off), R27
+    kv_dtype: str = ""     # "" = dtype; "e4m3" = fp8 KV cache with fp16/bf16 q and o (R28)
 
     @property
     def batch(self) -> int:
@@ -122,6 +127,8 @@ class Inputs:
     custom_mask: Optional[torch.Tensor]  # uint8 packed bits, LSB first
     mask_bit_indptr: Optional[np.ndarray]  # int64 [B+1]
     sm_scale: float
+    k_scale: float = 1.0        # K value = k_scale * stored element (fp8 KV cache, R28)
+    v_scale: float = 1.0
 
     @property
     def device(self):
@@ -199,22 +206,26 @@ def make_inputs(wl: Workload, *, device="cpu", seed_base=0, permute=True, layout
         strides = (wl.page_size * wl.H_kv * wl.D, wl.D, wl.page_size * wl.D)
     else:
         raise ValueError(layout)
-    k = torch.empty(shape, device=device, dtype=dt)
-    v = torch.empty(shape, device=device, dtype=dt)
+    kvt = DTYPES[wl.kv_dtype or wl.dtype]
+    ks, vs = KV_SCALE_E4M3 if wl.kv_dtype == "e4m3" else (1.0, 1.0)
+    k = torch.empty(shape, device=device, dtype=kvt)
+    v = torch.empty(shape, device=device, dtype=kvt)
     # generate in slabs to bound fp32 temporaries on large pools
     slab = max(1, (1 << 26) // max(1, int(np.prod(shape[1:]))))
     gk, gv = _gen(device, SEED_K + seed_base), _gen(device, SEED_V + seed_base)
     for s in range(0, total_pages, slab):
         e = min(total_pages, s + slab)
-        k[s:e] = torch.randn((e - s,) + shape[1:], generator=gk, device=device).to(dt)
-        v[s:e] = (torch.rand((e - s,) + shape[1:], generator=gv, device=device) * 2 - 1).to(dt)
+        kf = torch.randn((e - s,) + shape[1:], generator=gk, device=device)
+        vf = torch.rand((e - s,) + shape[1:], generator=gv, device=device) * 2 - 1
+        k[s:e] = (kf / ks if ks != 1.0 else kf).to(kvt)
+        v[s:e] = (vf / vs if vs != 1.0 else vf).to(kvt)
     cm, mbi = None, None
     if wl.mask == "custom":
         packed, mbi = mask_bits if mask_bits is not None else custom_mask_bits(wl, seed_base=seed_base)
         cm = torch.from_numpy(packed).to(device)
     return Inputs(wl, qo_indptr, kv_indptr, last, torch.from_numpy(kv_indices).to(device), q, k, v,
                   strides, strides, cm, mbi,
-                  float(sm_scale) if sm_scale is not None else 1.0 / float(np.sqrt(wl.D)))
+                  float(sm_scale) if sm_scale is not None else 1.0 / float(np.sqrt(wl.D)), ks, vs)
 
 
 @dataclasses.dataclass
@@ -254,10 +265,13 @@ def ragged_kv(inp: Inputs) -> RaggedKV:
 
 
 def raw_bits(t: torch.Tensor) -> np.ndarray:
-    """Host numpy view of a tensor's storage: float32 stays float32, 16-bit types as uint16 bits."""
+    """Host numpy view of a tensor's storage: float32 stays float32, 16-bit types as uint16 bits,
+    fp8 as uint8 bytes."""
     t = t.detach().cpu().contiguous()
     if t.dtype == torch.float32:
         return t.numpy()
+    if t.element_size() == 1:
+        return t.view(torch.uint8).numpy()
     return t.view(torch.int16).numpy().view(np.uint16)
 
 

@@ -474,3 +474,75 @@ def test_soft_cap_closed_forms():
     a = oracle.paged_attention(**_single_request(q, K, V, sm_scale=1.0), soft_cap=1e9)
     b = oracle.paged_attention(**_single_request(q, K, V, sm_scale=1.0))
     assert np.allclose(a[0], b[0], atol=1e-15) and abs(a[1][0, 0] - b[1][0, 0]) < 1e-15
+
+
+# ------------------------------------------- fp8 KV cache (NEXT-2, App. F)
+def _fp8(wl):
+    import dataclasses
+    return dataclasses.replace(wl, kv_dtype="e4m3")
+
+
+@pytest.mark.parametrize("bits,val", [
+    (0x00, 0.0), (0x38, 1.0), (0xB8, -1.0), (0x7E, 448.0), (0xFE, -448.0), (0x01, 2.0 ** -9),
+    (0x07, 7 * 2.0 ** -9), (0x08, 2.0 ** -6), (0x3C, 1.5), (0x40, 2.0), (0x34, 0.75), (0x77, 240.0),
+])
+def test_e4m3_decoder_closed_forms(bits, val):
+    """OCP E4M3 (R28): bias 7, 3 mantissa bits, subnormals below 2^-6, max 448."""
+    assert oracle.decode_scalar("e4m3", bits) == val
+
+
+def test_e4m3_decoder_all_codes_vs_torch_and_numpy():
+    """All 256 codes: the C decoder equals torch's float8_e4m3fn upcast (a library routine) and
+    the NumPy decoder (different code); the two NaN codes are exactly 0x7F and 0xFF; -0 is -0."""
+    codes = np.arange(256, dtype=np.uint8)
+    c = np.array([oracle.decode_scalar("e4m3", int(b)) for b in codes])
+    t = torch.from_numpy(codes.copy()).view(torch.float8_e4m3fn).to(torch.float64).numpy()
+    n = oracle.e4m3_to_float64(codes)
+    assert set(np.nonzero(np.isnan(c))[0]) == {0x7F, 0xFF}
+    assert np.array_equal(c, t, equal_nan=True) and np.array_equal(c, n, equal_nan=True)
+    assert math.copysign(1.0, c[0x80]) == -1.0
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_fp8_kv_c_oracle_matches_numpy_brute_force(seed):
+    """e4m3 pools with (non-power-of-two) scales, fp16/bf16 q, every mask, windows and caps."""
+    rng = np.random.default_rng(7000 + seed)
+    wl = synth.random_workload(rng, dtype=["bf16", "f16"][seed % 2], mask=synth.MASKS[seed % 3])
+    wl = _with_variant(_fp8(wl), window=int(rng.integers(1, 40)) if seed % 4 == 1 else 0,
+                       soft_cap=7.0 if seed % 4 == 2 else 0.0)
+    inp = _inp(wl, seed_base=seed, layout="NHD" if seed % 2 else "HND")
+    assert inp.k_pool.dtype == torch.float8_e4m3fn and inp.k_scale != 1.0
+    _cmp(_run(inp), oracle.brute_force_from_inputs(inp), 1e-12)
+
+
+def test_fp8_kv_equals_bf16_pool_of_the_same_values():
+    """Every e4m3 value is exact in bf16, so an e4m3 pool (scale 1) and a bf16 pool holding the
+    same values give a bit-identical oracle: the fp8 path changes only how bytes are decoded."""
+    wl = _fp8(synth.random_workload(np.random.default_rng(3), dtype="bf16", mask="causal"))
+    inp = _inp(wl)
+    args = dict(qo_indptr=inp.qo_indptr, kv_page_indptr=inp.kv_page_indptr, kv_last_page_len=inp.kv_last_page_len,
+                kv_page_indices=inp.kv_page_indices.numpy(), q=raw_bits(inp.q), k_strides=inp.k_strides,
+                v_strides=inp.v_strides, H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype="bf16",
+                mask="causal", sm_scale=inp.sm_scale)
+    a = oracle.paged_attention(**args, k_pool=raw_bits(inp.k_pool), v_pool=raw_bits(inp.v_pool), kv_dtype="e4m3")
+    b = oracle.paged_attention(**args, k_pool=raw_bits(inp.k_pool.to(torch.bfloat16)),
+                               v_pool=raw_bits(inp.v_pool.to(torch.bfloat16)))
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_fp8_kv_scales_closed_forms():
+    """k_scale multiplies every logit (== sm_scale * k_scale with unit k_scale); v_scale
+    multiplies o and leaves lse unchanged."""
+    wl = _fp8(synth.random_workload(np.random.default_rng(4), dtype="bf16", mask="none"))
+    inp = _inp(wl)
+    args = dict(qo_indptr=inp.qo_indptr, kv_page_indptr=inp.kv_page_indptr, kv_last_page_len=inp.kv_last_page_len,
+                kv_page_indices=inp.kv_page_indices.numpy(), q=raw_bits(inp.q), k_pool=raw_bits(inp.k_pool),
+                v_pool=raw_bits(inp.v_pool), k_strides=inp.k_strides, v_strides=inp.v_strides, H_qo=wl.H_qo,
+                H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype="bf16", kv_dtype="e4m3")
+    base = oracle.paged_attention(**args, sm_scale=0.2)
+    ks = oracle.paged_attention(**args, sm_scale=0.2 / 0.37, k_scale=0.37)
+    vs = oracle.paged_attention(**args, sm_scale=0.2, v_scale=-2.5)
+    _cmp(base, ks, 1e-10)  # raw logits reach ~1e3 (bytes up to ~180): rounding of the two scalings
+    fin = np.isfinite(base[1])
+    assert np.max(np.abs(vs[0] - (-2.5) * base[0])) < 1e-12
+    assert np.array_equal(vs[1][fin], base[1][fin])
