@@ -117,7 +117,8 @@ def decode_bytes(wl) -> dict:
     """Algorithmic bytes of one decode layer: every KV byte once per kv head,
     plus q, o (dtype), lse (fp32) and the BSR arrays (int32)."""
     es = 2 if wl.dtype in ("bf16", "f16") else 4
-    kv = int(wl.kv_lens.astype(np.int64).sum()) * wl.H_kv * wl.D * 2 * es
+    kv_es = 1 if wl.kv_dtype == "e4m3" else es  # fp8 KV cache: one byte per element (NEXT-2)
+    kv = int(wl.kv_lens.astype(np.int64).sum()) * wl.H_kv * wl.D * 2 * kv_es
     nq = int(wl.qo_lens.sum())
     qo = 2 * nq * wl.H_qo * wl.D * es + nq * wl.H_qo * 4
     idx = int(wl.num_pages().sum()) * 4 + 3 * (wl.batch + 1) * 4
@@ -154,6 +155,8 @@ class Layered:
 
     def engine(self, **kw):
         wl = self.wl
+        if wl.kv_dtype:
+            kw = dict(kw, kv_dtype=wl.kv_dtype, k_scale=self.inp0.k_scale, v_scale=self.inp0.v_scale)
         cfg = self.bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
                                     mask=wl.mask, max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()), **kw)
         return self.bsra.Engine(cfg, torch.cuda.current_device())
@@ -343,6 +346,35 @@ def bench_contiguous(dev, pk, reps=9):
     return out
 
 
+def bench_fp8_decode(dev, pk, args, world, rank, bf16_ms):
+    """the configs[1] decode step with an E4M3 KV cache: same
+    lengths, layers, graph and timing as the headline line; bytes counted at one byte per KV
+    element. `speedup` = bf16 step time / fp8 step time (same tokens)."""
+    import dataclasses
+    wl = dataclasses.replace(synth.c2_decode_llama8b(), kv_dtype="e4m3")
+    L = Layered(wl, args.layers, dev, seed_base=1000 * rank)
+    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel, pdl=not args.no_pdl)
+    s, one_step, _ = time_device_steps(L, eng, args.steps, args.warmup, not args.no_graph)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        a.record(s)
+        for _ in range(args.steps):
+            one_step()
+        b.record(s)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b) / args.steps, world)
+    by = decode_bytes(wl)
+    launch_ms = per_launch_ms(L, eng)
+    tokens = int(wl.kv_lens.sum()) * args.layers * world
+    return {"workload": "c2_decode_llama8b (configs[1]) with an E4M3 KV cache, bf16 q/o", "unit": "TB/s",
+            "value": world * by["total"] * args.layers / (ms * 1e-3) / 1e12, "ms_per_step": ms,
+            "kv_tokens_per_s": tokens / (ms * 1e-3), "speedup_vs_bf16_kv": bf16_ms / ms,
+            "launch_ms": launch_ms, "frac": by["total"] / (launch_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+            "kernel": eng.selected_kernel(), "algorithmic_bytes_per_launch": by["total"]}
+
+
 def bench_composable(dev, pk, layers=16, reps=20):
     """configs[3]: 8K shared prefix + 64 branches x 256-token suffixes, one decode step per layer
     through ComposableDecode (prefix engine on tensor-core tiles + suffix engine + ⊕), every layer
@@ -518,6 +550,7 @@ def main():
     ap.add_argument("--no-composable", action="store_true")
     ap.add_argument("--no-contiguous", action="store_true", help="skip the paged-vs-contiguous KV line")
     ap.add_argument("--no-long", action="store_true")
+    ap.add_argument("--no-fp8", action="store_true", help="skip the fp8 (E4M3) KV-cache decode line")
     ap.add_argument("--no-pdl", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -578,10 +611,21 @@ def main():
         e2e = {"value": world * step_bytes / (e2e_ms * 1e-3) / 1e12, "unit": "TB/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
 
+    # ---- secondary: the same decode step with an fp8 (E4M3) KV cache (NEXT-2)
+    fp8 = None
+    if not args.no_fp8:
+        del L
+        torch.cuda.empty_cache()
+        fp8 = bench_fp8_decode(dev, pk, args, world, rank, ms)
+        torch.cuda.empty_cache()
+
     # ---- secondary: configs[2] ragged causal prefill TFLOP/s (one layer, per-launch events)
     prefill = None
     if not args.no_prefill:
-        del L
+        try:
+            del L
+        except NameError:
+            pass
         torch.cuda.empty_cache()
         wl3 = synth.c3_prefill_llama70b()
         L3 = Layered(wl3, 2, dev, seed_base=1000 * rank)
@@ -639,7 +683,7 @@ def main():
                        "graph": not args.no_graph},
             "frac_of_hbm_peak": value / world * 1e3 / pk["hbm_gbs"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "prefill": prefill,
-            "composable": composable, "long_context": long_ctx, "contiguous_kv": contiguous,
+            "composable": composable, "long_context": long_ctx, "contiguous_kv": contiguous, "decode_fp8": fp8,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         }
         emit(out)

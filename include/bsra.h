@@ -37,7 +37,11 @@ typedef enum {
   BSRA_ENCCL = 6         /* NCCL error (bsra_dist.h) */
 } bsra_status;
 
-typedef enum { BSRA_F32 = 0, BSRA_F16 = 1, BSRA_BF16 = 2 } bsra_dtype;
+/* BSRA_E4M3: OCP FP8 E4M3 ("E4M3FN": bias 7, no infinities, S.1111.111 = NaN, max 448), valid
+ * only as bsra_config.kv_dtype — the fp8 KV cache of the paper's FP8-FP16 mixed-precision
+ * attention, where "the query and output remain in fp16, while the KV-Cache is stored in fp8"
+ * (App. F; R28). */
+typedef enum { BSRA_F32 = 0, BSRA_F16 = 1, BSRA_BF16 = 2, BSRA_E4M3 = 3 } bsra_dtype;
 
 /* LogitsMask. CAUSAL is right-aligned: query row r of a request with lengths
  * (l_qo, l_kv) sees token t iff t <= l_kv - l_qo + r (R4). CUSTOM: per request a
@@ -56,7 +60,7 @@ typedef struct {
   int32_t num_kv_heads;      /* H_kv                                                            */
   int32_t head_dim;          /* D in {64, 128}                                                  */
   int32_t page_size;         /* B_c >= 1 ("B_c is specified by KV-Cache management")   */
-  bsra_dtype dtype;          /* dtype of q, k_pool, v_pool                                      */
+  bsra_dtype dtype;          /* dtype of q (and of k_pool, v_pool unless kv_dtype says otherwise) */
   bsra_dtype o_dtype;        /* = dtype, or BSRA_F32 (raw attention state for a later ⊕)      */
   bsra_mask mask;            /* fixed per engine                                                */
   int32_t max_batch;         /* scheduler-metadata bounds supplied up front (App. D.3) */
@@ -78,7 +82,15 @@ typedef struct {
                                 t < p - W + 1 (W keys up to its own position; R26).
                                 Algorithm 1 then starts each row's KV range at its window       */
   float logits_soft_cap;     /* c > 0: scaled logit s -> c * tanh(s / c) (R27)        */
-  int32_t reserved[4];       /* must be zero                                                    */
+  /* fp8 KV cache (App. F; R28). kv_dtype: 0 or == dtype => K/V in dtype;
+   * BSRA_E4M3 => K/V pools hold one byte per element (dtype must be F16 or BF16; q and o stay in
+   * dtype). Element values are k_scale * E4M3(byte) and v_scale * E4M3(byte): per-tensor
+   * dequantisation scales (0 => 1), changeable per run with bsra_set_kv_scales. The kernels
+   * dequantise exactly (every E4M3 value is exact in fp16 and bf16) and compute as for dtype. */
+  int32_t kv_dtype;
+  float k_scale;
+  float v_scale;
+  int32_t reserved[1];       /* must be zero                                                    */
 } bsra_config;
 
 /* flags: BSRA_FLAG_PDL launches the tcgen05 kernels with programmatic dependent launch: a run()
@@ -134,7 +146,8 @@ bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, c
  *   k_pool, v_pool   device pools; element (page p, slot s, kv head h, dim d) lives at
  *                    p*strides[0] + s*strides[1] + h*strides[2] + d  (strides in ELEMENTS, host
  *                    int64[3]; dim stride 1). Default NHD: [pages, page_size, H_kv, D].
- *                    Base addresses and strides must be 16-byte aligned.
+ *                    Base addresses and strides must be 16-byte aligned. With kv_dtype =
+ *                    BSRA_E4M3 the pools hold bytes (strides still in elements = bytes).
  *   kv_page_indices  [nnz] device int32: BSR `indices` (page ids); not validated (caller contract)
  *   custom_mask      MASK_CUSTOM: device uint8 bits (see bsra_mask); else NULL
  *   mask_bit_indptr  MASK_CUSTOM: device int64 [batch+1] bit offsets; else NULL
@@ -146,6 +159,11 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
                      const int64_t* k_strides, const int64_t* v_strides, const int32_t* kv_page_indices,
                      const uint8_t* custom_mask, const int64_t* mask_bit_indptr, void* o, float* lse,
                      void* stream);
+
+/* Dequantisation scales of an fp8 KV cache for subsequent run() calls on `e` (e.g. per layer);
+ * 0 => 1. A captured graph keeps the scales of the run() it captured. Host only.
+ * Errors: EINVAL (NULL engine, negative or non-finite scale). */
+bsra_status bsra_set_kv_scales(bsra_engine* e, float k_scale, float v_scale);
 
 /* Contiguous-KV inspector (engine created with BSRA_FLAG_RAGGED_KV): as bsra_plan, with the KV
  * lengths given by a ragged indptr instead of a page table.

@@ -18,10 +18,10 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BSRA_LIB") or os.path.join(_HERE, "libbsra.so")  # override: A/B builds
 
-F32, F16, BF16 = 0, 1, 2
+F32, F16, BF16, E4M3 = 0, 1, 2, 3
 MASK = {"none": 0, "causal": 1, "custom": 2}
-DTYPE = {"f32": F32, "f16": F16, "bf16": BF16}
-TORCH_DTYPE = {F32: torch.float32, F16: torch.float16, BF16: torch.bfloat16}
+DTYPE = {"f32": F32, "f16": F16, "bf16": BF16, "e4m3": E4M3}
+TORCH_DTYPE = {F32: torch.float32, F16: torch.float16, BF16: torch.bfloat16, E4M3: torch.float8_e4m3fn}
 KERNEL = {"auto": 0, "simt": 1, "tc": 2}
 TILE_BIT = {16: 1, 64: 2, 128: 4, 256: 8}
 
@@ -38,7 +38,8 @@ class Config(ctypes.Structure):
                 ("cost_alpha", ctypes.c_int64), ("cost_beta", ctypes.c_int64), ("kv_chunk_align", ctypes.c_int32),
                 ("kv_chunk_min", ctypes.c_int32), ("kernel", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("sliding_window", ctypes.c_int32), ("logits_soft_cap", ctypes.c_float),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("kv_dtype", ctypes.c_int32), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float),
+                ("reserved", ctypes.c_int32 * 1)]
 
 
 FLAG_PDL = 1  # BSRA_FLAG_PDL (include/bsra.h)
@@ -47,7 +48,7 @@ FLAG_RAGGED_KV = 2  # BSRA_FLAG_RAGGED_KV: contiguous (ragged) K/V, no page tabl
 
 _lib = None
 EXPORTS = ["bsra_version", "bsra_num_sms", "bsra_workspace_bytes", "bsra_engine_create", "bsra_engine_destroy",
-           "bsra_plan", "bsra_run", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
+           "bsra_plan", "bsra_run", "bsra_set_kv_scales", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
            "bsra_plan_host", "bsra_plan_export",
            "bsra_plan_stats", "bsra_last_run_launches", "bsra_selected_kernel", "bsra_last_error",
            "bsra_dist_unique_id", "bsra_dist_create", "bsra_dist_destroy", "bsra_dist_scratch_bytes",
@@ -71,6 +72,7 @@ def lib():
             "bsra_engine_destroy": (None, [P]),
             "bsra_plan": (I32, [P, I32, P, P, P, ctypes.c_float, P]),
             "bsra_run": (I32, [P, P, P, P, P, P, P, P, P, P, P, P]),
+            "bsra_set_kv_scales": (I32, [P, ctypes.c_float, ctypes.c_float]),
             "bsra_plan_ragged": (I32, [P, I32, P, P, ctypes.c_float, P]),
             "bsra_run_ragged": (I32, [P, P, P, P, P, P, P, P, P, P, P]),
             "bsra_merge_states": (I32, [P, P, P, P, I32, I64, I32, I32, P, I32, P, P]),
@@ -112,9 +114,13 @@ def _i32(a) -> np.ndarray:
 def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="none", max_batch=1,
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
                 kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False, window=0,
-                soft_cap=0.0) -> Config:
-    """window: sliding window W (0 = off, R26); soft_cap: logits soft-cap c (0 = off, R27)."""
+                soft_cap=0.0, kv_dtype=None, k_scale=0.0, v_scale=0.0) -> Config:
+    """window: sliding window W (0 = off, DESIGN.md R26); soft_cap: logits soft-cap c (0 = off, R27);
+    kv_dtype "e4m3": fp8 KV cache with per-tensor scales k_scale / v_scale (0 = 1; R28)."""
     c = Config()
+    if kv_dtype:
+        c.kv_dtype = DTYPE[kv_dtype] if isinstance(kv_dtype, str) else kv_dtype
+    c.k_scale, c.v_scale = float(k_scale), float(v_scale)
     c.sliding_window, c.logits_soft_cap = int(window), float(soft_cap)
     c.flags = (FLAG_PDL if pdl else 0) | (FLAG_RAGGED_KV if ragged_kv else 0)
     c.num_qo_heads, c.num_kv_heads, c.head_dim, c.page_size = H_qo, H_kv, D, page_size
@@ -194,6 +200,10 @@ class Engine:
         _check(lib().bsra_run(self._h, _p(q), _p(k_pool), _p(v_pool), ctypes.cast(ks, ctypes.c_void_p),
                               ctypes.cast(vs, ctypes.c_void_p), _p(kv_page_indices), _p(custom_mask),
                               _p(mask_bit_indptr), _p(o), _p(lse), self._stream(stream)))
+
+    def set_kv_scales(self, k_scale: float, v_scale: float):
+        """fp8 KV dequantisation scales for the following run() calls (0 = 1)."""
+        _check(lib().bsra_set_kv_scales(self._h, float(k_scale), float(v_scale)))
 
     def plan_ragged(self, qo_indptr, kv_indptr, sm_scale: float = 0.0, stream=None):
         """Contiguous-KV inspector (engine made with ragged_kv=True): kv_indptr[batch+1] token offsets."""

@@ -26,6 +26,7 @@ struct SimtSmem {
   static constexpr int kBytes = 2 /*stages*/ * 2 /*K,V*/ * kTileBytes;
 };
 
+// TKV = element type of the pools (T, or __nv_fp8_e4m3 for the fp8 KV cache, R28)
 template <typename T, int D>
 __device__ __forceinline__ void simt_load_tile(const AttnParams& p, uint8_t* sk, uint8_t* sv, int64_t t0, int n,
                                                int64_t page_begin, int kvh) {
@@ -45,11 +46,12 @@ __device__ __forceinline__ void simt_load_tile(const AttnParams& p, uint8_t* sk,
   }
 }
 
-template <typename T, int D>
+template <typename T, typename TKV, int D>
 __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid_constant__ AttnParams p) {
-  using S = SimtSmem<T, D>;
+  using S = SimtSmem<TKV, D>;
   constexpr int kPer = D / 32;               // output dims owned per lane
-  constexpr int kVecN = Vec<T>::N;           // elements per 16-byte vector
+  constexpr int kVecN = Vec<T>::N;           // q elements per 16-byte vector
+  constexpr int kVecK = Vec<TKV>::N;         // K elements per 16-byte vector
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* sk[2] = {smem, smem + 2 * S::kTileBytes};
   uint8_t* sv[2] = {smem + S::kTileBytes, smem + 3 * S::kTileBytes};
@@ -96,7 +98,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
 
       const int ntiles = (int)((ke - kb + kSimtTile - 1) / kSimtTile);
       __syncthreads();  // previous users of the stage buffers are done
-      if (ntiles > 0) simt_load_tile<T, D>(p, sk[0], sv[0], kb, (int)imin64(kSimtTile, ke - kb), page_begin, kvh);
+      if (ntiles > 0) simt_load_tile<TKV, D>(p, sk[0], sv[0], kb, (int)imin64(kSimtTile, ke - kb), page_begin, kvh);
       cp_async_commit();
       for (int ti = 0; ti < ntiles; ++ti) {
         const int st = ti & 1;
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
         const int n = (int)imin64(kSimtTile, ke - t0);
         if (ti + 1 < ntiles) {
           const int64_t t1 = t0 + kSimtTile;
-          simt_load_tile<T, D>(p, sk[st ^ 1], sv[st ^ 1], t1, (int)imin64(kSimtTile, ke - t1), page_begin, kvh);
+          simt_load_tile<TKV, D>(p, sk[st ^ 1], sv[st ^ 1], t1, (int)imin64(kSimtTile, ke - t1), page_begin, kvh);
         }
         cp_async_commit();
         cp_async_wait<1>();
@@ -121,11 +123,11 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
           const uint4* krow = reinterpret_cast<const uint4*>(sk[st] + lane * S::kRowBytes);
           float dot = 0.f;
 #pragma unroll
-          for (int c = 0; c < D / kVecN; ++c) {
-            float kf[kVecN];
-            Vec<T>::to_float(krow[c], kf);
+          for (int c = 0; c < D / kVecK; ++c) {
+            float kf[kVecK];
+            Vec<TKV>::to_float(krow[c], kf);
 #pragma unroll
-            for (int e = 0; e < kVecN; ++e) dot = fmaf(qv[c * kVecN + e], kf[e], dot);
+            for (int e = 0; e < kVecK; ++e) dot = fmaf(qv[c * kVecK + e], kf[e], dot);
           }
           s = (p.soft_cap > 0.f ? soft_cap_raw(p, dot) : dot) * p.scale_log2;  // soft-cap (R27)
         }
@@ -141,9 +143,9 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
           // ---- O += P V: lane owns dims [lane*kPer, lane*kPer + kPer)
           for (int tt = 0; tt < n; ++tt) {
             const float pt = __shfl_sync(0xffffffffu, pr, tt);
-            const T* vrow = reinterpret_cast<const T*>(sv[st] + tt * S::kRowBytes) + lane * kPer;
+            const TKV* vrow = reinterpret_cast<const TKV*>(sv[st] + tt * S::kRowBytes) + lane * kPer;
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) acc[j] = fmaf(pt, to_f<T>(vrow[j]), acc[j]);
+            for (int j = 0; j < kPer; ++j) acc[j] = fmaf(pt, to_f<TKV>(vrow[j]), acc[j]);
           }
         }
         __syncthreads();  // stage st is free for the load issued in the next iteration
@@ -153,7 +155,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
       // ---- epilogue
       if (valid) {
         const bool empty = dsum == 0.f;
-        const float inv = empty ? 0.f : 1.f / dsum;
+        const float inv = empty ? 0.f : p.v_scale / dsum;  // v_scale: fp8 KV (R28), else 1
         const float lse = empty ? -INFINITY : (m + __log2f(dsum)) * kLn2;
         if (slot < 0) {
           const int64_t orow = (qo_begin + tok) * p.H_qo + head;

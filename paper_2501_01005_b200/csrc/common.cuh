@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 namespace bsra {
 
@@ -39,7 +40,10 @@ struct AttnParams {
   int32_t window;
   float soft_cap, inv_soft_cap;
   int32_t H_qo, H_kv, g, page_size, mask_mode, o_f32, T_slot, D;
-  float scale_log2;  // sm_scale * log2(e)
+  float scale_log2;  // sm_scale * log2(e) (fp8 KV: sm_scale * k_scale * log2(e))
+  // fp8 KV cache (R28): pools hold E4M3 bytes; v_scale multiplies o
+  int32_t kv_f8;
+  float v_scale;
 };
 
 // LogitsTransform soft-cap on a raw score (R27): s -> c * tanh(s / c), c in raw units.
@@ -160,6 +164,25 @@ struct Vec<__half> {
   }
 };
 
+// OCP E4M3 (R28): 16 bytes -> 16 floats via the exact fp8x2 -> f16x2 converter
+template <>
+struct Vec<__nv_fp8_e4m3> {
+  static constexpr int N = 16;
+  __device__ __forceinline__ static void to_float(const uint4& u, float* f) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const __half2_raw r = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[i] >> (16 * h)), __NV_E4M3);
+        const float2 x = __half22float2(*reinterpret_cast<const __half2*>(&r));
+        f[4 * i + 2 * h] = x.x;
+        f[4 * i + 2 * h + 1] = x.y;
+      }
+    }
+  }
+};
+
 template <typename T>
 __device__ __forceinline__ T from_float(float x);
 template <>
@@ -177,6 +200,8 @@ template <>
 __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
 template <>
 __device__ __forceinline__ float to_f<__half>(__half x) { return __half2float(x); }
+template <>
+__device__ __forceinline__ float to_f<__nv_fp8_e4m3>(__nv_fp8_e4m3 x) { return float(x); }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);

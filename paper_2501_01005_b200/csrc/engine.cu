@@ -38,7 +38,11 @@ bsra_status fail(bsra_status s, const std::string& msg) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-int dtype_size(bsra_dtype t) { return t == BSRA_F32 ? 4 : 2; }
+int dtype_size(bsra_dtype t) { return t == BSRA_F32 ? 4 : t == BSRA_E4M3 ? 1 : 2; }
+
+// fp8 KV cache (R28): kv_dtype 0 or == dtype means K/V in dtype
+bool kv_is_f8(const bsra_config& c) { return c.kv_dtype == BSRA_E4M3; }
+bsra_dtype kv_dtype_of(const bsra_config& c) { return kv_is_f8(c) ? BSRA_E4M3 : c.dtype; }
 
 struct Layout {
   int32_t num_ctas = 0, T_max = 0, T_min = 0;
@@ -71,8 +75,12 @@ bsra_status validate_config(const bsra_config& c) {
   if (c.sliding_window < 0) return fail(BSRA_EINVAL, "sliding_window < 0");
   if (!(c.logits_soft_cap >= 0.f) || !std::isfinite(c.logits_soft_cap))
     return fail(BSRA_EINVAL, "logits_soft_cap must be finite and >= 0");
-  for (int i = 0; i < 4; ++i)
-    if (c.reserved[i]) return fail(BSRA_EINVAL, "reserved fields must be zero");
+  if (c.kv_dtype != 0 && c.kv_dtype != c.dtype && c.kv_dtype != BSRA_E4M3) return fail(BSRA_EINVAL, "bad kv_dtype");
+  if (kv_is_f8(c) && c.dtype != BSRA_F16 && c.dtype != BSRA_BF16)
+    return fail(BSRA_EINVAL, "an E4M3 KV cache takes F16 or BF16 q / o (P:499)");
+  if (!(c.k_scale >= 0.f) || !std::isfinite(c.k_scale) || !(c.v_scale >= 0.f) || !std::isfinite(c.v_scale))
+    return fail(BSRA_EINVAL, "k_scale / v_scale must be finite and >= 0");
+  if (c.reserved[0]) return fail(BSRA_EINVAL, "reserved fields must be zero");
   return BSRA_OK;
 }
 
@@ -80,7 +88,7 @@ int32_t default_num_ctas(const bsra_config& c, int32_t sms) {
   // one persistent CTA per SM (App. D.3: k = 1 "persistent kernel"); the SIMT decode
   // path fits two per SM, the tcgen05 kernels one.
   const bool decode = c.tile_q == 16 || (c.tile_q == 0 && tile_mask_of(c) == 1);
-  const bool simt = c.kernel == BSRA_KERNEL_SIMT || c.dtype == BSRA_F32;
+  const bool simt = c.kernel == BSRA_KERNEL_SIMT || c.dtype == BSRA_F32 || (kv_is_f8(c) && c.head_dim != 128);
   return decode && simt ? 2 * sms : sms;
 }
 
@@ -129,6 +137,7 @@ struct bsra_engine {
   int64_t total_qo = 0;
   int64_t total_kv = 0;  // ragged KV: token extent of k / v (kv_indptr[batch])
   int32_t max_qo = 0;
+  float k_scale = 1.f, v_scale = 1.f;  // fp8 KV dequantisation scales (bsra_set_kv_scales)
   long long* trace = nullptr;  // debug: device buffer for kernel pipeline traces
   int32_t last_launches = 0;
   const char* selected = "none";
@@ -182,6 +191,8 @@ bsra_status bsra_engine_create(const bsra_config* cfg, int32_t device, void* d_w
   if (!e) return fail(BSRA_ENOMEM, "host allocation failed");
   e->cfg = *cfg;
   e->cfg.num_ctas = nc;
+  e->k_scale = cfg->k_scale > 0.f ? cfg->k_scale : 1.f;
+  e->v_scale = cfg->v_scale > 0.f ? cfg->v_scale : 1.f;
   e->device = device;
   e->lay = lay;
   e->ws = static_cast<uint8_t*>(d_workspace);
@@ -323,22 +334,23 @@ bsra_status bsra_plan_ragged(bsra_engine* e, int32_t batch, const int32_t* qo_in
 
 namespace {
 
-template <typename T, int D>
+template <typename T, typename TKV, int D>
 bsra_status launch_simt(const bsra::AttnParams& p, int grid, cudaStream_t st) {
-  using S = bsra::SimtSmem<T, D>;
+  using S = bsra::SimtSmem<TKV, D>;
   static bool attr = false;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(bsra::attn_simt_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kBytes));
+    CUDA_TRY(cudaFuncSetAttribute(bsra::attn_simt_kernel<T, TKV, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  S::kBytes));
     attr = true;
   }
-  bsra::attn_simt_kernel<T, D><<<grid, bsra::kSimtWarps * 32, S::kBytes, st>>>(p);
+  bsra::attn_simt_kernel<T, TKV, D><<<grid, bsra::kSimtWarps * 32, S::kBytes, st>>>(p);
   CUDA_TRY(cudaGetLastError());
   return BSRA_OK;
 }
 
-template <typename T>
+template <typename T, typename TKV = T>
 bsra_status launch_simt_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st) {
-  return D == 64 ? launch_simt<T, 64>(p, grid, st) : launch_simt<T, 128>(p, grid, st);
+  return D == 64 ? launch_simt<T, TKV, 64>(p, grid, st) : launch_simt<T, TKV, 128>(p, grid, st);
 }
 
 template <typename TO, int D>
@@ -371,7 +383,7 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     return fail(BSRA_EINVAL, "NULL tensor pointer");
   if (c.mask == BSRA_MASK_CUSTOM && has_rows && (!custom_mask || !mask_bit_indptr))
     return fail(BSRA_EINVAL, "MASK_CUSTOM needs custom_mask and mask_bit_indptr");
-  const int es = dtype_size(c.dtype);
+  const int es = dtype_size(kv_dtype_of(c));
   for (int i = 0; i < 3; ++i)
     if ((k_strides[i] * es) % 16 || (v_strides[i] * es) % 16 || k_strides[i] < 0 || v_strides[i] < 0)
       return fail(BSRA_EINVAL, "pool strides must be non-negative and 16-byte multiples");
@@ -395,9 +407,13 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   p.page_indices = kv_page_indices;
   p.kv_ragged = ragged ? 1 : 0;
   p.window = c.sliding_window;
+  // fp8 KV (R28): k = k_scale * E4M3(byte) folds into the logit scale; v_scale scales o
+  const float logit_scale = e->sm_scale * (kv_is_f8(c) ? e->k_scale : 1.f);
+  p.kv_f8 = kv_is_f8(c) ? 1 : 0;
+  p.v_scale = kv_is_f8(c) ? e->v_scale : 1.f;
   // soft-cap in raw q.k units: c * tanh(sm_scale*s / c) = sm_scale * c' tanh(s / c'), c' = c / sm_scale
-  p.soft_cap = c.logits_soft_cap > 0.f ? c.logits_soft_cap / e->sm_scale : 0.f;
-  p.inv_soft_cap = c.logits_soft_cap > 0.f ? e->sm_scale / c.logits_soft_cap : 0.f;
+  p.soft_cap = c.logits_soft_cap > 0.f ? c.logits_soft_cap / logit_scale : 0.f;
+  p.inv_soft_cap = c.logits_soft_cap > 0.f ? logit_scale / c.logits_soft_cap : 0.f;
   p.mask = custom_mask;
   p.mask_indptr = mask_bit_indptr;
   p.o = o;
@@ -418,7 +434,7 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   p.o_f32 = c.o_dtype == BSRA_F32;
   p.T_slot = e->lay.T_max;
   p.D = c.head_dim;
-  p.scale_log2 = e->sm_scale * bsra::kLog2e;
+  p.scale_log2 = logit_scale * bsra::kLog2e;
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = c.num_ctas;
@@ -438,6 +454,7 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     tl.pdl = (c.flags & BSRA_FLAG_PDL) != 0;
     tl.ragged = ragged;
     tl.total_kv = e->total_kv;
+    tl.f8kv = kv_is_f8(c);
     const char* why = "";
     int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
     if (rc < 0)
@@ -448,10 +465,15 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   }
   if (!used_tc) {
     e->selected = "simt";
-    switch (c.dtype) {
-      case BSRA_F32: s = launch_simt_d<float>(p, c.head_dim, grid, st); break;
-      case BSRA_F16: s = launch_simt_d<__half>(p, c.head_dim, grid, st); break;
-      default: s = launch_simt_d<__nv_bfloat16>(p, c.head_dim, grid, st); break;
+    if (kv_is_f8(c)) {
+      if (c.dtype == BSRA_F16) s = launch_simt_d<__half, __nv_fp8_e4m3>(p, c.head_dim, grid, st);
+      else s = launch_simt_d<__nv_bfloat16, __nv_fp8_e4m3>(p, c.head_dim, grid, st);
+    } else {
+      switch (c.dtype) {
+        case BSRA_F32: s = launch_simt_d<float>(p, c.head_dim, grid, st); break;
+        case BSRA_F16: s = launch_simt_d<__half>(p, c.head_dim, grid, st); break;
+        default: s = launch_simt_d<__nv_bfloat16>(p, c.head_dim, grid, st); break;
+      }
     }
     if (s) return s;
   }
@@ -488,6 +510,15 @@ bsra_status bsra_run_ragged(bsra_engine* e, const void* q, const void* k, const 
   const int64_t ks[3] = {k_strides[0], k_strides[0], k_strides[1]};
   const int64_t vs[3] = {v_strides[0], v_strides[0], v_strides[1]};
   return run_core(e, q, k, v, ks, vs, nullptr, true, custom_mask, mask_bit_indptr, o, lse, stream);
+}
+
+bsra_status bsra_set_kv_scales(bsra_engine* e, float k_scale, float v_scale) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  if (!(k_scale >= 0.f) || !std::isfinite(k_scale) || !(v_scale >= 0.f) || !std::isfinite(v_scale))
+    return fail(BSRA_EINVAL, "k_scale / v_scale must be finite and >= 0");
+  e->k_scale = k_scale > 0.f ? k_scale : 1.f;
+  e->v_scale = v_scale > 0.f ? v_scale : 1.f;
+  return BSRA_OK;
 }
 
 int32_t bsra_last_run_launches(const bsra_engine* e) { return e ? e->last_launches : 0; }

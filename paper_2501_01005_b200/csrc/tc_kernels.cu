@@ -44,46 +44,56 @@ bool make_q_map(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, in
 // paged pool: element (page, slot, head, d) at page*s0 + slot*s1 + head*s2 + d (elements).
 // 4-D view ordered (d, head, slot, page) — coordinates in that order — box (64, 1, B, 1).
 // Contiguous KV uses the same view with slot = token (extent N, clipped there) and one page.
+// f8: E4M3 pools (1-byte elements), box (128, 1, B, 1) = one 128-byte row per token.
 bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int64_t page_size, int64_t s0, int64_t s1,
-                   int64_t s2, int B, int64_t npages = 0x7fffffff) {
+                   int64_t s2, int B, int64_t npages = 0x7fffffff, bool f8 = false) {
   auto enc = get_encode();
   if (!enc) return false;
+  const cuuint64_t es_b = f8 ? 1 : 2;
   cuuint64_t dims[4] = {128, (cuuint64_t)H_kv, (cuuint64_t)std::max<int64_t>(page_size, 1), (cuuint64_t)npages};
-  cuuint64_t strides[3] = {(cuuint64_t)s2 * 2, (cuuint64_t)s1 * 2, (cuuint64_t)s0 * 2};
-  cuuint32_t box[4] = {64, 1, (cuuint32_t)B, 1};
+  cuuint64_t strides[3] = {(cuuint64_t)s2 * es_b, (cuuint64_t)s1 * es_b, (cuuint64_t)s0 * es_b};
+  cuuint32_t box[4] = {f8 ? 128u : 64u, 1, (cuuint32_t)B, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  return enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pool),
+  const CUtensorMapDataType dt =
+      f8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  return enc(m, dt, 4, const_cast<void*>(pool),
              dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int kC, int kMask>
+template <int kC, int kMask, bool kF8>
 cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
+  using L = dec::Lay<kF8>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         dec::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, kF8>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_tc(tc_decode_kernel<kC, kMask>, grid, dec::kThreads, dec::kSmemBytes, st, tp);
+  return launch_tc(tc_decode_kernel<kC, kMask, kF8>, grid, L::kThreads, L::kSmemBytes, st, tp);
 }
 
-template <int kC>
+template <int kC, bool kF8>
 cudaError_t launch_decode_m(int mask, const TcParams& tp, int grid, cudaStream_t st) {
   switch (mask) {
-    case 0: return launch_decode_t<kC, 0>(tp, grid, st);
-    case 1: return launch_decode_t<kC, 1>(tp, grid, st);
-    default: return launch_decode_t<kC, 2>(tp, grid, st);
+    case 0: return launch_decode_t<kC, 0, kF8>(tp, grid, st);
+    case 1: return launch_decode_t<kC, 1, kF8>(tp, grid, st);
+    default: return launch_decode_t<kC, 2, kF8>(tp, grid, st);
   }
 }
 
-cudaError_t launch_decode(int kc, int mask, const TcParams& tp, int grid, cudaStream_t st) {
+template <bool kF8>
+cudaError_t launch_decode_f(int kc, int mask, const TcParams& tp, int grid, cudaStream_t st) {
   switch (kc) {
-    case 4: return launch_decode_m<4>(mask, tp, grid, st);
-    case 8: return launch_decode_m<8>(mask, tp, grid, st);
-    default: return launch_decode_m<16>(mask, tp, grid, st);
+    case 4: return launch_decode_m<4, kF8>(mask, tp, grid, st);
+    case 8: return launch_decode_m<8, kF8>(mask, tp, grid, st);
+    default: return launch_decode_m<16, kF8>(mask, tp, grid, st);
   }
+}
+
+cudaError_t launch_decode(bool f8, int kc, int mask, const TcParams& tp, int grid, cudaStream_t st) {
+  return f8 ? launch_decode_f<true>(kc, mask, tp, grid, st) : launch_decode_f<false>(kc, mask, tp, grid, st);
 }
 
 }  // namespace
@@ -94,10 +104,10 @@ bool make_q_map_ext(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N
 // K and V maps for a launch: paged pools, or contiguous KV (token extent L.total_kv, one page)
 bool make_kv_maps(TcParams& tp, const AttnParams& p, const TcLaunch& L, int B) {
   if (L.ragged)
-    return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.total_kv, p.ks1, p.ks1, p.ks2, B, 1) &&
-           make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.total_kv, p.vs1, p.vs1, p.vs2, B, 1);
-  return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.page_size, p.ks0, p.ks1, p.ks2, B) &&
-         make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.page_size, p.vs0, p.vs1, p.vs2, B);
+    return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.total_kv, p.ks1, p.ks1, p.ks2, B, 1, L.f8kv) &&
+           make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.total_kv, p.vs1, p.vs1, p.vs2, B, 1, L.f8kv);
+  return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.page_size, p.ks0, p.ks1, p.ks2, B, 0x7fffffff, L.f8kv) &&
+         make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.page_size, p.vs0, p.vs1, p.vs2, B, 0x7fffffff, L.f8kv);
 }
 
 int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const char** name, const char** why) {
@@ -127,10 +137,11 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     }
     const int64_t fused = std::min<int64_t>(16, (int64_t)L.max_qo * g);
     const int kc = fused <= 4 ? 4 : fused <= 8 ? 8 : 16;
-    if (launch_decode(kc, L.mask, tp, L.grid, st) != cudaSuccess) return -1;
+    if (launch_decode(L.f8kv, kc, L.mask, tp, L.grid, st) != cudaSuccess) return -1;
     *name = "tc_decode";
     return 1;
   }
+  if (L.f8kv) { *why = "fp8 KV with T_q > 16 runs on the CUDA-core kernel"; return 0; }
   if (L.T_q == 64 || L.T_q == 128 || L.T_q == 256) {
     return tc_prefill_launch(p, L, st, name, why, B);
   }

@@ -18,6 +18,7 @@ struct TcLaunch {
   bool pdl = false;        // programmatic dependent launch (BSRA_FLAG_PDL)
   bool ragged = false;     // contiguous KV [N, H_kv, D] (p.kv_ragged)
   int64_t total_kv = 0;    // ragged: N, the token extent of k / v
+  bool f8kv = false;       // K/V pools in E4M3 (fp8 KV cache, R28)
 };
 
 // Launches the tcgen05 kernel for this plan if one applies (bf16/f16, D = 128, supported page

@@ -7,7 +7,7 @@ import oracle
 import paper_2501_01005_b200 as bsra
 import synth
 
-TOL = {"f32": (1e-5, 1e-5), "f16": (1e-2, 1e-3), "bf16": (1e-2, 1e-3)}  # (o, lse): BASELINE north_star
+TOL = {"f32": (1e-5, 1e-5), "f16": (1e-2, 1e-3), "bf16": (1e-2, 1e-3)}  # fp8 KV: q/o dtype's tolerance  # (o, lse): BASELINE north_star
 
 
 def engine_for(wl, *, num_ctas=0, tile_q=0, tile_set=(16, 64, 128, 256), kernel="auto", o_dtype=None, max_batch=None,
@@ -15,7 +15,8 @@ def engine_for(wl, *, num_ctas=0, tile_q=0, tile_set=(16, 64, 128, 256), kernel=
     cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
                            o_dtype=o_dtype, mask=wl.mask, max_batch=max_batch or max(1, wl.batch),
                            max_total_qo_rows=max_rows or max(1, int(wl.qo_lens.sum())), num_ctas=num_ctas,
-                           tile_set=tile_set, tile_q=tile_q, kernel=kernel)
+                           tile_set=tile_set, tile_q=tile_q, kernel=kernel, kv_dtype=wl.kv_dtype or None,
+                           window=wl.window, soft_cap=wl.soft_cap)
     return bsra.Engine(cfg, device)
 
 
@@ -31,6 +32,8 @@ def run_gpu(inp, eng=None, *, o_dtype=None, **kw):
     lse = torch.full((nq, wl.H_qo), float("nan"), device=dev, dtype=torch.float32)
     mbi = None if inp.mask_bit_indptr is None else torch.from_numpy(inp.mask_bit_indptr).to(dev)
     eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+    if wl.kv_dtype:
+        eng.set_kv_scales(inp.k_scale, inp.v_scale)
     eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse,
             custom_mask=inp.custom_mask, mask_bit_indptr=mbi)
     torch.cuda.synchronize()
