@@ -210,6 +210,8 @@ def per_launch_ms(L: Layered, eng, reps=3):
     torch.cuda.synchronize()
     with torch.cuda.stream(s):
         L.plan(eng, s)
+        for r in range(len(L.layers)):  # warm pass: first-launch costs stay out of the average
+            L.run_layer(eng, r, s)
         for _ in range(reps):
             for r in range(len(L.layers)):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -19,11 +19,6 @@
 //               row max grows by more than 2^8 (the final o = O/l and lse use the same max, so the
 //               result is exact). S^T and P^T are double-buffered and the next tile's S MMA is
 //               issued before this tile's softmax when its K has landed.
-//   warps 5..8  (kF8 only) fp8 KV cache (App. F; R28): TMA lands E4M3 K/V
-//               tiles in an fp8 ring; thread = token row converts its 128-byte K and V rows to
-//               bf16/f16 (exact) straight into the swizzled MMA ring, so the MMAs and the softmax
-//               are the 16-bit kernel's. The "fast numerical array converter" of P:499, on the
-//               CUDA cores beside the tensor-core pipeline; HBM bytes per token are halved.
 // kC = live fused columns (4, 8 or 16) — only those run through the softmax; kMask = mask mode.
 // Epilogue: unsplit rows write o / lse (writethrough, App. D.2), split rows fp32 partials.
 #pragma once
@@ -85,49 +80,6 @@ constexpr int kSmemBytes = kOffRed + 2 * 4 * kN * 4 + 1024;  // + alignment slac
 constexpr int kThreads = 160;
 constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T at col 32
 constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
-
-// Shared-memory layout per variant. kF8: a 2-deep 16-bit MMA ring fed by the converter warps and
-// a 2-deep fp8 landing ring (K 16 KB + V 16 KB per stage) fed by TMA: 209 KB in all.
-template <bool kF8>
-struct Lay {
-  static constexpr int kSt = kF8 ? 2 : kStages;            // 16-bit K/V ring depth
-  static constexpr int kF8St = kF8 ? 2 : 0;                // fp8 landing ring depth
-  static constexpr int kF8Half = kTile * 128;              // one of K or V in fp8: 16 KB
-  static constexpr int kF8StageBytes = 2 * kF8Half;
-  static constexpr int kOffF8 = kSt * kStageBytes;
-  static constexpr int kOffQ = kOffF8 + kF8St * kF8StageBytes;
-  static constexpr int kOffP = kOffQ + 2 * kQBytes;
-  static constexpr int kOffBar = kOffP + 2 * kPBytes;
-  static constexpr int kOffRed = kOffBar + 256;
-  static constexpr int kSmemBytes = kOffRed + 2 * 4 * kN * 4 + 1024;
-  static constexpr int kThreads = kF8 ? 288 : 160;
-};
-static_assert(Lay<false>::kOffQ == kOffQ && Lay<false>::kSmemBytes == kSmemBytes, "16-bit layout unchanged");
-static_assert(Lay<true>::kSmemBytes <= 227 * 1024, "fp8 layout fits one CTA per SM");
-
-// 16 E4M3 bytes -> 16 bf16 / f16 values (two 16-byte chunks), exact: every E4M3 value is an f16
-// normal or zero, and the f16 -> f32 -> bf16 steps are exact for it.
-template <bool kHalf>
-__device__ __forceinline__ void e4m3x16_to_16bit(const uint4& u, uint4& lo, uint4& hi) {
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-  uint32_t r[8];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const __half2_raw x = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)(w[i] >> (16 * h)), __NV_E4M3);
-      if (kHalf) {
-        r[2 * i + h] = (uint32_t)x.x | ((uint32_t)x.y << 16);
-      } else {
-        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&x));
-        const __nv_bfloat162 b = __float22bfloat162_rn(f);
-        r[2 * i + h] = *reinterpret_cast<const uint32_t*>(&b);
-      }
-    }
-  }
-  lo = make_uint4(r[0], r[1], r[2], r[3]);
-  hi = make_uint4(r[4], r[5], r[6], r[7]);
-}
 }  // namespace dec
 
 struct DecItem {
@@ -154,12 +106,9 @@ __device__ __forceinline__ DecItem dec_item(const PlanView& pv, int it, int g) {
   return d;
 }
 
-template <int kC, int kMask, bool kF8 = false>
-__global__ void __launch_bounds__(dec::Lay<kF8>::kThreads, 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
+template <int kC, int kMask>
+__global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
   using namespace dec;
-  using Ly = Lay<kF8>;
-  constexpr int kStages = Ly::kSt;
-  constexpr int kOffQ = Ly::kOffQ, kOffP = Ly::kOffP, kOffBar = Ly::kOffBar, kOffRed = Ly::kOffRed;
   const AttnParams& p = tp.p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -170,9 +119,7 @@ __global__ void __launch_bounds__(dec::Lay<kF8>::kThreads, 1) tc_decode_kernel(c
   uint64_t* empty_q = full_q + 2;        // [2]
   uint64_t* bar_s = empty_q + 2;         // [2] S^T buffer ready
   uint64_t* bar_pv = bar_s + 2;          // [2] PV MMA reading P^T buffer b done
-  uint64_t* f8full = bar_pv + 2;         // [2] (kF8) fp8 stage landed
-  uint64_t* f8empty = f8full + 2;        // [2] (kF8) fp8 stage converted
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(f8empty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_pv + 2);
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [4 warps][kN]
   float* red2 = red + 4 * kN;
 
@@ -183,12 +130,8 @@ __global__ void __launch_bounds__(dec::Lay<kF8>::kThreads, 1) tc_decode_kernel(c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], kF8 ? 128 : 1);  // kF8: every converter thread arrives
+      ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
-    }
-    for (int s = 0; s < Ly::kF8St; ++s) {
-      ptx::mbar_init(&f8full[s], 1);
-      ptx::mbar_init(&f8empty[s], 128);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&full_q[b], 1);
@@ -198,7 +141,7 @@ __global__ void __launch_bounds__(dec::Lay<kF8>::kThreads, 1) tc_decode_kernel(c
     }
     ptx::fence_barrier_init();
   }
-  if (warp >= 1 && warp <= 4) {  // zero both P^T buffers once: rows >= kC stay zero for the kernel's lifetime
+  if (warp >= 1) {  // zero both P^T buffers once: rows >= kC stay zero for the kernel's lifetime
     uint4* pz = reinterpret_cast<uint4*>(smem + kOffP);
     for (int i = threadIdx.x - 32; i < 2 * kPBytes / 16; i += 128) pz[i] = make_uint4(0, 0, 0, 0);
     ptx::fence_proxy_async();
@@ -253,24 +196,6 @@ __global__ void __launch_bounds__(dec::Lay<kF8>::kThreads, 1) tc_decode_kernel(c
             off = (int)(tok % p.page_size);
           }
         }
-        if (kF8) {  // E4M3 rows are 128 bytes: one box {128 d, B tokens} per page for each of K, V
-          if (lane == 0) {
-            ptx::mbar_wait(&f8empty[stage], ephase);
-            ptx::mbar_arrive_expect_tx(&f8full[stage], (uint32_t)nsub * B * 256);
-          }
-          __syncwarp();
-          if (lane < nsub) {
-            uint8_t* kd = smem + Ly::kOffF8 + stage * Ly::kF8StageBytes + lane * B * 128;
-            ptx::tma_load_4d(kd, &tp.tk, &f8full[stage], 0, d.kvh, off, page);
-            ptx::tma_load_4d(kd + Ly::kF8Half, &tp.tv, &f8full[stage], 0, d.kvh, off, page);
-          }
-          __syncwarp();
-          if (++stage == Ly::kF8St) {
-            stage = 0;
-            ephase ^= 1;
-          }
-          continue;
-        }
         if (lane == 0) {
           ptx::mbar_wait(&empty[stage], ephase);
           ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * 512);
@@ -288,49 +213,6 @@ __global__ void __launch_bounds__(dec::Lay<kF8>::kThreads, 1) tc_decode_kernel(c
         if (++stage == kStages) {
           stage = 0;
           ephase ^= 1;
-        }
-      }
-    }
-  } else if (kF8 && warp >= 5) {
-    // ================= fp8 -> 16-bit converter (kF8): thread = token row =================
-    const int row = threadIdx.x - 160;  // 0..127
-    const int sw = row & 7;             // SW128 chunk swizzle of this row (both rings)
-    int fs = 0, stage = 0;
-    uint32_t f8ph = 0, eph = 1;         // fresh empty barriers: parity 1 passes
-    for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
-      for (int ti = 0; ti < d.ntiles; ++ti) {
-        const int n = (int)imin64(kTile, d.ke - (d.kb + (int64_t)ti * kTile));
-        ptx::mbar_wait(&f8full[fs], f8ph);
-        ptx::mbar_wait(&empty[stage], eph);  // the MMAs reading this 16-bit stage completed
-        const uint8_t* src = smem + Ly::kOffF8 + fs * Ly::kF8StageBytes + row * 128;
-        uint8_t* dst = smem + stage * kStageBytes + row * 128;
-#pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {  // K, then V
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {  // 16 d per fp8 chunk: d = 16j .. 16j+15
-            uint4 lo = make_uint4(0, 0, 0, 0), hi = lo;
-            if (row < n) {  // rows past the chunk stay zero (0 * garbage could be NaN in PV)
-              const uint4 u = *reinterpret_cast<const uint4*>(src + kv * Ly::kF8Half + ((j ^ sw) << 4));
-              if (tp.f16) e4m3x16_to_16bit<true>(u, lo, hi);
-              else e4m3x16_to_16bit<false>(u, lo, hi);
-            }
-            uint8_t* h = dst + kv * kKVBytes + (j >> 2) * kHalfBytes;  // 64-column half of d
-            const int c0 = (2 * j) & 7;
-            *reinterpret_cast<uint4*>(h + ((c0 ^ sw) << 4)) = lo;
-            *reinterpret_cast<uint4*>(h + (((c0 + 1) ^ sw) << 4)) = hi;
-          }
-        }
-        ptx::fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core
-        ptx::mbar_arrive(&f8empty[fs]);
-        ptx::mbar_arrive(&full[stage]);
-        if (++fs == Ly::kF8St) {
-          fs = 0;
-          f8ph ^= 1;
-        }
-        if (++stage == kStages) {
-          stage = 0;
-          eph ^= 1;
         }
       }
     }
@@ -411,7 +293,7 @@ __global__ void __launch_bounds__(dec::Lay<kF8>::kThreads, 1) tc_decode_kernel(c
         ptx::mbar_wait(&bar_s[sbuf], sph[sbuf]);
         sph[sbuf] ^= 1;
         uint8_t* vS = smem + stage * kStageBytes + kKVBytes;
-        if (!kF8 && n < kTile && row >= n) {  // rows past the chunk: zero V so 0 * garbage cannot poison O
+        if (n < kTile && row >= n) {  // rows past the chunk: zero V so 0 * garbage cannot poison O
           ptx::mbar_wait(&full[stage], fphase);  // (already complete) orders the TMA writes before ours
           uint4 z = make_uint4(0, 0, 0, 0);
           uint4* v0 = reinterpret_cast<uint4*>(vS + row * 128);
@@ -547,7 +429,7 @@ __global__ void __launch_bounds__(dec::Lay<kF8>::kThreads, 1) tc_decode_kernel(c
         if (c < d.nrows) {
           const float l = (red2[c] + red2[kN + c]) + (red2[2 * kN + c] + red2[3 * kN + c]);
           const bool empty_row = !(l > 0.f);
-          const float val = empty_row ? 0.f : (kF8 ? ov[c] * (p.v_scale / l) : ov[c] / l);
+          const float val = empty_row ? 0.f : ov[c] / l;
           const float lse = empty_row ? -INFINITY : (m[c] + __log2f(l)) * kLn2;
           const int f = d.row0 + c;
           const int tok = f / g, head = d.kvh * g + f % g;

@@ -5,9 +5,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "tc_decode.cuh"
+#include "tc_decode_f8.cuh"
 #include "tc_kernels.hpp"
 #include "tc_prefill.cuh"
 
@@ -63,15 +65,24 @@ bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int64_t
 
 template <int kC, int kMask, bool kF8>
 cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
-  using L = dec::Lay<kF8>;
   static bool attr = false;
+  if constexpr (kF8) {  // fp8 KV cache: K in TMEM, converter warps (tc_decode_f8.cuh)
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(tc_decode_f8_kernel<kC, kMask>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, f8d::kSmemBytes);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    return launch_tc(tc_decode_f8_kernel<kC, kMask>, grid, f8d::kThreads, f8d::kSmemBytes, st, tp);
+  } else {
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, kF8>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, L::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         dec::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_tc(tc_decode_kernel<kC, kMask, kF8>, grid, L::kThreads, L::kSmemBytes, st, tp);
+  return launch_tc(tc_decode_kernel<kC, kMask>, grid, dec::kThreads, dec::kSmemBytes, st, tp);
+  }
 }
 
 template <int kC, bool kF8>

@@ -1,0 +1,3 @@
+timeout -s KILL 600 python -m pytest tests/test_fp8_kv.py -m gpu -x -q 2>&1 | tail -3
+timeout -s KILL 300 python scripts/fp8_perf.py 2>&1 | tail -1
+timeout 300 python scripts/trace_decode_f8.py | cut -c1-700
