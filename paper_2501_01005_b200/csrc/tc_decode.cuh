@@ -76,7 +76,7 @@ constexpr int kOffQ = kStages * kStageBytes;
 constexpr int kOffP = kOffQ + 2 * kQBytes;   // two P^T buffers
 constexpr int kOffBar = kOffP + 2 * kPBytes;
 constexpr int kOffRed = kOffBar + 256;
-constexpr int kSmemBytes = kOffRed + 2 * 4 * kN * 4 + 1024;  // + alignment slack
+constexpr int kSmemBytes = kOffRed + 2 * 4 * kN * 4 + 64 + 1024;  // red, red2, vote flags + alignment slack
 constexpr int kThreads = 160;
 constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T at col 32
 constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     int pbuf = 0;             // P^T buffer to write next
     uint32_t qphase[2] = {0, 0};
     int qb = 0;
+    int tpar = 0;  // tile count (parity selects the vote-flag buffer)
 
     // elected thread: issue S^T(tile in `st`, buffer `b`) = K Q^T
     // issued by all 32 lanes of warp 1 (elect.sync inside the asm keeps the warp converged)
@@ -321,64 +322,85 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           const float sc = p.soft_cap > 0.f ? soft_cap_raw(p, s[c]) : s[c];                // R27
           s[c] = vis ? sc * p.scale_log2 : -INFINITY;
         }
-        float mx[kC];
+        // ---- stale-max softmax (lazy rescale, exact: o and lse use the same max): P = 2^(s - m)
+        // with the running max m; only when some score exceeds m by more than 2^8 (every item's
+        // first tile) do the warps reduce the tile max, rescale O and recompute P. The common
+        // path has no shuffles and one barrier: a warp vote and a per-warp flag (double-buffered
+        // by tile parity) read after it.
+        bool over = false;
 #pragma unroll
-        for (int c = 0; c < kC; ++c) mx[c] = s[c];
+        for (int c = 0; c < kC; ++c) over |= s[c] > m[c] + kRescaleThresh;
+        over = __any_sync(0xffffffffu, over);
+        int* flags = reinterpret_cast<int*>(red2 + 4 * kN) + (tpar & 1) * 4;
+        if (lane == 0) flags[q4] = over ? 1 : 0;
+        float pr[kC];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-          for (int c = 0; c < kC; ++c) mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int c = 0; c < kC; ++c) red[q4 * kN + c] = mx[c];
-        }
+        for (int c = 0; c < kC; ++c) pr[c] = s[c] == -INFINITY ? 0.f : exp2f(s[c] - m[c]);
         wait_pv(pbuf);  // the PV MMA that read this P^T buffer two tiles ago is done
-        ptx::tc_fence_before();
-        ptx::named_bar_sync(1, 128);
-        // ---- lazy max update (exact: o and lse use the same stale max)
-        float alpha[kC];
-        bool rescale = false;
-#pragma unroll
-        for (int c = 0; c < kC; ++c) {
-          const float mt = fmaxf(fmaxf(red[c], red[kN + c]), fmaxf(red[2 * kN + c], red[3 * kN + c]));
-          alpha[c] = 1.f;
-          if (mt > m[c] + kRescaleThresh) {
-            if (m[c] != -INFINITY) {
-              alpha[c] = exp2f(m[c] - mt);
-              rescale = true;
-            }
-            m[c] = mt;
-          }
-          const float pr = s[c] == -INFINITY ? 0.f : exp2f(s[c] - m[c]);
-          lp[c] = lp[c] * alpha[c] + pr;
-          s[c] = pr;
-        }
-        if (rescale) {  // rare: bring O^T to the new max (no PV MMA may be in flight)
-          wait_pv(pbuf ^ 1);
-          ptx::tc_fence_after();
-          float ov[kC];
-          ptx::tmem_ld<kC>(tO, ov);
-          ptx::tmem_ld_wait();
-#pragma unroll
-          for (int c = 0; c < kC; ++c) ov[c] *= alpha[c];
-          ptx::tmem_st<kC>(tO, ov);
-          ptx::tmem_st_wait();
-        }
         // ---- P^T (K-major, SW128): row c, token `row`
-        {
-          uint8_t* pa = smem + kOffP + pbuf * kPBytes + (row >> 6) * (kN * 128);
-          const int tt = row & 63;
+        uint8_t* pa = smem + kOffP + pbuf * kPBytes + (row >> 6) * (kN * 128);
+        const int tt = row & 63;
+        auto store_p = [&]() {
 #pragma unroll
           for (int c = 0; c < kC; ++c) {
             const uint32_t off = (c >> 3) * 1024 + (c & 7) * 128 + ((((tt >> 3) ^ (c & 7)) << 4) | ((tt & 7) << 1));
-            if (tp.f16) *reinterpret_cast<__half*>(pa + off) = __float2half_rn(s[c]);
-            else *reinterpret_cast<__nv_bfloat16*>(pa + off) = __float2bfloat16_rn(s[c]);
+            if (tp.f16) *reinterpret_cast<__half*>(pa + off) = __float2half_rn(pr[c]);
+            else *reinterpret_cast<__nv_bfloat16*>(pa + off) = __float2bfloat16_rn(pr[c]);
           }
-        }
+        };
+        store_p();
         ptx::fence_proxy_async();
         ptx::tc_fence_before();
         ptx::named_bar_sync(1, 128);
+        if (flags[0] | flags[1] | flags[2] | flags[3]) {  // slow path
+          float mx[kC];
+#pragma unroll
+          for (int c = 0; c < kC; ++c) mx[c] = s[c];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int c = 0; c < kC; ++c) mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+          }
+          if (lane == 0) {
+#pragma unroll
+            for (int c = 0; c < kC; ++c) red[q4 * kN + c] = mx[c];
+          }
+          ptx::named_bar_sync(1, 128);
+          float alpha[kC];
+          bool rescale = false;
+#pragma unroll
+          for (int c = 0; c < kC; ++c) {
+            const float mt = fmaxf(fmaxf(red[c], red[kN + c]), fmaxf(red[2 * kN + c], red[3 * kN + c]));
+            alpha[c] = 1.f;
+            if (mt > m[c] + kRescaleThresh) {
+              if (m[c] != -INFINITY) {
+                alpha[c] = exp2f(m[c] - mt);
+                rescale = true;
+              }
+              m[c] = mt;
+            }
+            pr[c] = s[c] == -INFINITY ? 0.f : exp2f(s[c] - m[c]);
+            lp[c] *= alpha[c];
+          }
+          if (rescale) {  // bring O^T to the new max (no PV MMA may be in flight)
+            wait_pv(pbuf ^ 1);
+            ptx::tc_fence_after();
+            float ov[kC];
+            ptx::tmem_ld<kC>(tO, ov);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < kC; ++c) ov[c] *= alpha[c];
+            ptx::tmem_st<kC>(tO, ov);
+            ptx::tmem_st_wait();
+          }
+          store_p();
+          ptx::fence_proxy_async();
+          ptx::tc_fence_before();
+          ptx::named_bar_sync(1, 128);
+        }
+#pragma unroll
+        for (int c = 0; c < kC; ++c) lp[c] += pr[c];
+        ++tpar;
         // ---- O^T += V^T P^T ; then the next S^T if it was not issued early
         if (warp == 1) {
           ptx::tc_fence_after();
