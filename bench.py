@@ -640,6 +640,16 @@ def main():
                    "kernel": e3.selected_kernel(), "tile_q": int(e3.export_plan()[3]), "flops_per_layer": fl}
         del L3
         torch.cuda.empty_cache()
+        if not args.no_fp8:  # the same prefill with an E4M3 KV cache (NEXT-2): gather pass + tcgen05 prefill
+            import dataclasses
+            L3f = Layered(dataclasses.replace(wl3, kv_dtype="e4m3"), 2, dev, seed_base=1000 * rank)
+            e3f = L3f.engine(num_ctas=148, kernel=args.kernel, tile_q=args.prefill_tile)
+            pf_ms = per_launch_ms(L3f, e3f, reps=3)
+            prefill["fp8_kv"] = {"ms_per_layer": pf_ms, "value": fl / (pf_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                                 "kernel": e3f.selected_kernel(), "launches_per_run": e3f.last_launches(),
+                                 "vs_bf16_kv": p_ms / pf_ms}
+            del L3f
+            torch.cuda.empty_cache()
 
     composable = None
     if not args.no_composable:

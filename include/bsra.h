@@ -86,7 +86,12 @@ typedef struct {
    * BSRA_E4M3 => K/V pools hold one byte per element (dtype must be F16 or BF16; q and o stay in
    * dtype). Element values are k_scale * E4M3(byte) and v_scale * E4M3(byte): per-tensor
    * dequantisation scales (0 => 1), changeable per run with bsra_set_kv_scales. The kernels
-   * dequantise exactly (every E4M3 value is exact in fp16 and bf16) and compute as for dtype. */
+   * dequantise exactly (every E4M3 value is exact in fp16 and bf16) and compute as for dtype.
+   * Decode tiles (T_q = 16) dequantise inside the attention kernel. Prefill tiles (T_q >= 64)
+   * on the tcgen05 path first gather the plan's tokens into an ENGINE-OWNED 16-bit device buffer
+   * (one extra launch per run; 4 * sum(l_kv) * H_kv * head_dim bytes, allocated by bsra_plan and
+   * grown when a plan needs more — a CUDA graph captured before such a growing plan must be
+   * re-captured). */
   int32_t kv_dtype;
   float k_scale;
   float v_scale;

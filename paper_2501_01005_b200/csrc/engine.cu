@@ -16,6 +16,7 @@
 
 #include "../../include/bsra.h"
 #include "attn_simt.cuh"
+#include "f8_gather.cuh"
 #include "merge.cuh"
 #include "scheduler.hpp"
 #include "tc_kernels.hpp"
@@ -47,7 +48,8 @@ bsra_dtype kv_dtype_of(const bsra_config& c) { return kv_is_f8(c) ? BSRA_E4M3 : 
 struct Layout {
   int32_t num_ctas = 0, T_max = 0, T_min = 0;
   size_t plan_words = 0;
-  size_t off_plan = 0, off_part_o = 0, off_part_lse = 0, off_counters = 0, total = 0;
+  size_t off_plan = 0, off_part_o = 0, off_part_lse = 0, off_counters = 0, off_aux = 0, total = 0;
+  size_t aux_words = 0;  // fp8 prefill gather: src_begin[max_batch+1], kv_off[max_batch+1]
 };
 
 int tile_mask_of(const bsra_config& c) { return c.tile_set_mask ? c.tile_set_mask : 15; }
@@ -110,6 +112,9 @@ Layout make_layout(const bsra_config& c, int32_t num_ctas) {
   off = align_up(off + slots * L.T_max * 4, 256);
   L.off_counters = off;
   off = align_up(off + (size_t)(num_ctas + 1) * 4, 256);
+  L.off_aux = off;
+  L.aux_words = 2 * ((size_t)c.max_batch + 1);
+  off = align_up(off + L.aux_words * 4, 256);
   L.total = off;
   return L;
 }
@@ -138,6 +143,11 @@ struct bsra_engine {
   int64_t total_kv = 0;  // ragged KV: token extent of k / v (kv_indptr[batch])
   int32_t max_qo = 0;
   float k_scale = 1.f, v_scale = 1.f;  // fp8 KV dequantisation scales (bsra_set_kv_scales)
+  // fp8 KV with prefill tiles (f8_gather.cuh): the current plan addresses a 16-bit gathered copy
+  bool f8_prefill = false;
+  int64_t f8_rows = 0;       // sum of l_kv of the current plan
+  uint16_t* f8_buf = nullptr;  // engine-owned [2][f8_cap_rows, H_kv, 128] 16-bit
+  int64_t f8_cap_rows = 0;
   long long* trace = nullptr;  // debug: device buffer for kernel pipeline traces
   int32_t last_launches = 0;
   const char* selected = "none";
@@ -199,7 +209,7 @@ bsra_status bsra_engine_create(const bsra_config* cfg, int32_t device, void* d_w
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  cudaError_t ce = cudaMallocHost(&e->staging, lay.plan_words * 4);
+  cudaError_t ce = cudaMallocHost(&e->staging, (lay.plan_words + lay.aux_words) * 4);
   if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&e->staged, cudaEventDisableTiming);
   cudaSetDevice(prev);
   if (ce != cudaSuccess) {
@@ -218,6 +228,7 @@ void bsra_engine_destroy(bsra_engine* e) {
     cudaEventDestroy(e->staged);
   }
   if (e->staging) cudaFreeHost(e->staging);
+  if (e->f8_buf) cudaFree(e->f8_buf);
   delete e;
 }
 
@@ -263,6 +274,9 @@ namespace {
 
 // Shared inspector core: Algorithm 1 over (qo, kv) lengths; `page_begin` gives each request's
 // first BSR page (paged) or first token row (contiguous KV) for the plan's request table.
+// fp8 KV with a prefill tile (T_q > 16) on the tcgen05 path: the plan is re-encoded with each
+// request's first row in the gathered 16-bit copy (f8_gather.cuh) and `page_begin` goes to the
+// aux section for the gather pass.
 bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* page_begin,
                       const std::vector<int32_t>& qo, const std::vector<int32_t>& kv, float sm_scale, void* stream) {
   const bsra_config& c = e->cfg;
@@ -273,13 +287,44 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
   bsra::PlanSummary sum;
   std::string err = bsra::build_plan(sched_params(c, c.num_ctas), qo, kv, qo_indptr, page_begin, im, sum);
   if (!err.empty()) return fail(BSRA_EINVAL, err);
+  const int32_t batch = (int32_t)qo.size();
+  const int32_t g = c.num_qo_heads / c.num_kv_heads;
+  const bool f8_prefill = kv_is_f8(c) && sum.T_q > 16 && c.kernel != BSRA_KERNEL_SIMT && c.head_dim == 128 &&
+                          (g & (g - 1)) == 0;
+  std::vector<int32_t> kv_off;
+  int64_t f8_rows = 0;
+  if (f8_prefill) {
+    kv_off.resize(batch + 1, 0);
+    for (int32_t i = 0; i < batch; ++i) {
+      f8_rows += kv[i];
+      if (f8_rows > INT32_MAX) return fail(BSRA_EBOUNDS, "fp8 prefill: more than 2^31 KV tokens in one plan");
+      kv_off[i + 1] = (int32_t)f8_rows;
+    }
+    err = bsra::build_plan(sched_params(c, c.num_ctas), qo, kv, qo_indptr, kv_off.data(), im, sum);
+    if (!err.empty()) return fail(BSRA_EINVAL, err);
+  }
   if (im.size() > e->lay.plan_words) return fail(BSRA_EBOUNDS, "plan image exceeds the workspace plan section");
   if (sum.T_q > e->lay.T_max) return fail(BSRA_EBOUNDS, "tile larger than the workspace partial slots");
+  if (f8_prefill && f8_rows > e->f8_cap_rows) {  // engine-owned 16-bit copy (grows; see bsra.h)
+    const int64_t cap = std::max<int64_t>(f8_rows, e->f8_cap_rows * 5 / 4);
+    uint16_t* nb = nullptr;
+    CUDA_TRY(cudaMalloc(&nb, (size_t)cap * c.num_kv_heads * 128 * 2 * sizeof(uint16_t)));
+    if (e->f8_buf) CUDA_TRY(cudaFree(e->f8_buf));
+    e->f8_buf = nb;
+    e->f8_cap_rows = cap;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // the previous upload must have left the pinned buffer before it is overwritten
   if (e->have_event_pending) CUDA_TRY(cudaEventSynchronize(e->staged));
   std::memcpy(e->staging, im.data(), im.size() * 4);
   CUDA_TRY(cudaMemcpyAsync(e->ws + e->lay.off_plan, e->staging, im.size() * 4, cudaMemcpyHostToDevice, st));
+  if (f8_prefill) {  // aux: src_begin[batch+1] at 0, kv_off[batch+1] at max_batch+1
+    int32_t* aux = e->staging + e->lay.plan_words;
+    const size_t stride = (size_t)c.max_batch + 1;
+    std::memcpy(aux, page_begin, (size_t)(batch + 1) * 4);
+    std::memcpy(aux + stride, kv_off.data(), (size_t)(batch + 1) * 4);
+    CUDA_TRY(cudaMemcpyAsync(e->ws + e->lay.off_aux, aux, e->lay.aux_words * 4, cudaMemcpyHostToDevice, st));
+  }
   CUDA_TRY(cudaEventRecord(e->staged, st));
   e->have_event_pending = true;
   if (!e->counters_zeroed) {  // merge-list arrival counters start at 0; the merging CTA resets them
@@ -289,6 +334,8 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
   e->image.swap(im);
   e->summary = sum;
   e->planned = true;
+  e->f8_prefill = f8_prefill;
+  e->f8_rows = f8_rows;
   e->sm_scale = sm_scale > 0.f ? sm_scale : 1.f / std::sqrt((float)c.head_dim);
   e->total_qo = rows;
   e->max_qo = 0;
@@ -441,6 +488,42 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   bsra_status s = BSRA_OK;
   const int T_q = e->summary.T_q;
   bool used_tc = false;
+  int gather_launches = 0;
+  bool kv16 = !kv_is_f8(c);  // the attention kernel reads 16-bit (or f32) K/V
+  if (e->f8_prefill) {
+    // fp8 KV, prefill tiles: dequantise-and-gather the plan's tokens into the engine's 16-bit
+    // copy, then run the 16-bit kernels on it as contiguous KV (f8_gather.cuh)
+    bsra::F8GatherParams gp{};
+    gp.k = static_cast<const uint8_t*>(k_pool);
+    gp.v = static_cast<const uint8_t*>(v_pool);
+    gp.ks0 = k_strides[0];
+    gp.ks1 = k_strides[1];
+    gp.ks2 = k_strides[2];
+    gp.vs0 = v_strides[0];
+    gp.vs1 = v_strides[1];
+    gp.vs2 = v_strides[2];
+    gp.page_indices = ragged ? nullptr : kv_page_indices;
+    const int32_t* aux = reinterpret_cast<const int32_t*>(e->ws + e->lay.off_aux);
+    gp.src_begin = aux;
+    gp.kv_off = aux + c.max_batch + 1;
+    gp.plan = p.plan;
+    gp.page_size = c.page_size;
+    gp.H_kv = c.num_kv_heads;
+    gp.f16 = c.dtype == BSRA_F16;
+    const int64_t plane = e->f8_cap_rows * c.num_kv_heads * 128;
+    gp.ko = e->f8_buf;
+    gp.vo = e->f8_buf + plane;
+    bsra::f8_gather_kernel<<<4 * 148, 256, 0, st>>>(gp);
+    CUDA_TRY(cudaGetLastError());
+    gather_launches = 1;
+    p.k = gp.ko;
+    p.v = gp.vo;
+    p.ks0 = p.ks1 = p.vs0 = p.vs1 = (int64_t)c.num_kv_heads * 128;
+    p.ks2 = p.vs2 = 128;
+    p.kv_ragged = 1;
+    ragged = true;
+    kv16 = true;
+  }
   if (c.kernel != BSRA_KERNEL_SIMT && c.dtype != BSRA_F32) {
     bsra::TcLaunch tl;
     tl.f16 = c.dtype == BSRA_F16;
@@ -453,8 +536,8 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     tl.mask = c.mask;
     tl.pdl = (c.flags & BSRA_FLAG_PDL) != 0;
     tl.ragged = ragged;
-    tl.total_kv = e->total_kv;
-    tl.f8kv = kv_is_f8(c);
+    tl.total_kv = e->f8_prefill ? e->f8_rows : e->total_kv;
+    tl.f8kv = !kv16;
     const char* why = "";
     int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
     if (rc < 0)
@@ -465,7 +548,7 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   }
   if (!used_tc) {
     e->selected = "simt";
-    if (kv_is_f8(c)) {
+    if (!kv16) {
       if (c.dtype == BSRA_F16) s = launch_simt_d<__half, __nv_fp8_e4m3>(p, c.head_dim, grid, st);
       else s = launch_simt_d<__nv_bfloat16, __nv_fp8_e4m3>(p, c.head_dim, grid, st);
     } else {
@@ -477,14 +560,14 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     }
     if (s) return s;
   }
-  e->last_launches = 1;
+  e->last_launches = 1 + gather_launches;
   if (!p.fused_merge) {  // contraction stage: fixed grid, exits at once if nothing split
     const int cgrid = std::max(1, std::min(grid, 2 * 148));
     if (c.o_dtype == BSRA_F32 || c.dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
     else if (c.dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
     else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
     if (s) return s;
-    e->last_launches = 2;
+    e->last_launches = 2 + gather_launches;
   }
   return BSRA_OK;
 }

@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(pre::kThreads, 1) tc_prefill_kernel(const __gr
       // ---- epilogue: thread r owns its whole row (TMEM loads warp-uniform, stores per row)
       {
         const bool empty_row = !(l > 0.f);
-        const float inv = empty_row ? 0.f : 1.f / l;
+        const float inv = empty_row ? 0.f : p.v_scale / l;  // v_scale: fp8 KV (R28), else 1
         const float lse = empty_row ? -INFINITY : (m + __log2f(l)) * kLn2;
         if (d.ntiles > 0) ptx::tc_fence_after();
         if (d.slot < 0) {

@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       }
       if (r == 0 && w == 0) BSRA_TRACE(12, it - it0);
       const bool empty_row = !(l > 0.f);
-      const float inv = empty_row ? 0.f : 1.f / l;
+      const float inv = empty_row ? 0.f : p.v_scale / l;  // v_scale: fp8 KV (R28), else 1
       const float lse = empty_row ? -INFINITY : (m + __log2f(l)) * kLn2;
       const int64_t orow = (d.qo_begin + tok) * p.H_qo + head;
       const int64_t prow = (int64_t)d.slot * p.T_slot + ri;

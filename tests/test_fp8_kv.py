@@ -183,14 +183,87 @@ def test_fp8_ragged_kv(cuda_device):
     assert_close(gpu, oracle.attention_from_inputs(inp), "bf16", what="fp8 ragged")
 
 
+def _pre(mask="causal", ps=16, qo=(70, 129, 1, 300), kv=(70, 200, 50, 300), H=(64, 8), dtype="bf16"):
+    return _fp8(synth.Workload("f8pre", H[0], H[1], 128, ps, dtype, mask, np.array(qo, np.int32),
+                               np.array(kv, np.int32)))
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("mask", ["none", "causal", "custom"])
+@pytest.mark.parametrize("tile_q", [64, 128, 256])
+def test_fp8_prefill_tc_masks_tiles(cuda_device, mask, tile_q):
+    """Prefill tiles with an fp8 KV cache: dequantise-and-gather pass + the tcgen05 prefill kernel
+    on the gathered 16-bit copy (f8_gather.cuh); gather + attention (+ contraction) launches."""
+    gpu = _case(cuda_device, _pre(mask=mask), num_ctas=148, tile_q=tile_q, expect="tc_prefill")
+    assert gpu[2].last_launches() == 3  # gather, attention, contraction (64/128/256-row engines)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ps", [1, 4, 16, 48, 256])
+def test_fp8_prefill_tc_page_sizes(cuda_device, ps):
+    """The gather reads any page size (pages smaller than 8 tokens included)."""
+    _case(cuda_device, _pre(ps=ps), num_ctas=64, tile_q=128, expect="tc_prefill")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,layout", [("f16", "NHD"), ("bf16", "HND")])
+def test_fp8_prefill_tc_dtypes_layouts(cuda_device, dtype, layout):
+    _case(cuda_device, _pre(dtype=dtype), layout=layout, num_ctas=37, tile_q=128, expect="tc_prefill")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nc", [1, 7, 148])
+def test_fp8_prefill_tc_split_kv_and_variants(cuda_device, nc):
+    """Split KV (partials scaled by v_scale before the contraction), window and soft-cap."""
+    wl = dataclasses.replace(_pre(qo=(700, 1, 64), kv=(900, 3000, 64)), window=513, soft_cap=20.0)
+    _case(cuda_device, wl, num_ctas=nc, expect="tc_prefill")
+
+
+@pytest.mark.gpu
+def test_fp8_prefill_replan_grows_buffer(cuda_device):
+    """A later plan with more KV tokens grows the engine's 16-bit copy; a smaller one reuses it."""
+    small, big = _pre(qo=(70, 30), kv=(70, 90)), _pre(qo=(300, 500, 64), kv=(900, 2000, 64))
+    eng = engine_for(big, num_ctas=148, tile_q=128, max_batch=4, max_rows=2048)
+    for wl in (small, big, small):
+        inp = synth.make_inputs(wl, device=cuda_device)
+        gpu = run_gpu(inp, eng)
+        assert gpu[2].selected_kernel() == "tc_prefill"
+        assert_close(gpu, oracle.attention_from_inputs(inp), "bf16", what=f"replan {wl.kv_lens}")
+
+
+@pytest.mark.gpu
+def test_fp8_prefill_ragged_kv(cuda_device):
+    """fp8 contiguous (ragged) KV with prefill tiles: the gather reads token rows."""
+    wl = _pre(qo=(70, 129, 1, 300), kv=(70, 200, 50, 300))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=128, dtype=wl.dtype, mask=wl.mask,
+                           max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()), num_ctas=64, tile_q=128,
+                           ragged_kv=True, kv_dtype="e4m3", k_scale=inp.k_scale, v_scale=inp.v_scale)
+    gpu = run_ragged(inp, bsra.Engine(cfg, 0))
+    assert gpu[2].selected_kernel() == "tc_prefill"
+    assert_close(gpu, oracle.attention_from_inputs(inp), "bf16", what="fp8 ragged prefill")
+
+
+@pytest.mark.gpu
+def test_fp8_c3_full_size_sampled(cuda_device):
+    """configs[2] (ragged causal prefill, 64/8 heads) with an E4M3 KV cache at full size in the
+    bench launch configuration; the shortest and one long request checked element by element."""
+    wl = _fp8(synth.c3_prefill_llama70b())
+    inp = synth.make_inputs(wl, device=cuda_device)
+    gpu = run_gpu(inp, num_ctas=148)
+    assert gpu[2].selected_kernel() == "tc_prefill"
+    order = np.argsort(wl.qo_lens)
+    reqs = sorted({int(order[0]), int(order[3])})
+    assert_close(gpu, oracle.attention_from_inputs(inp, req_list=reqs), "bf16", rows=rows_of_requests(inp, reqs),
+                 what="fp8 c3 sampled")
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("tile_q", [64, 128])
-def test_fp8_prefill_tiles_simt(cuda_device, mask, tile_q):
-    """Prefill tiles with an fp8 KV cache run on the CUDA-core kernel."""
-    wl = _fp8(synth.Workload("f8pre", 64, 8, 128, 16, "bf16", mask, np.array([70, 129, 1, 300], np.int32),
-                             np.array([70, 200, 50, 300], np.int32)))
-    _case(cuda_device, wl, num_ctas=148, tile_q=tile_q, expect="simt")
+def test_fp8_prefill_simt_forced(cuda_device, tile_q):
+    """kernel="simt": the CUDA-core kernel reads the E4M3 pool directly (no gather)."""
+    gpu = _case(cuda_device, _pre(mask="custom"), num_ctas=148, tile_q=tile_q, kernel="simt", expect="simt")
+    assert gpu[2].last_launches() == 2
 
 
 @pytest.mark.gpu
