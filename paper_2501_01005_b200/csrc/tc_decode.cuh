@@ -8,13 +8,15 @@
 // so one KV load serves all fused rows and the tensor core does the arithmetic while the kernel
 // streams HBM (decode is HBM-bound, fig:varlen).
 //
-// Warp roles (one CTA per SM, persistent over the CTA's plan queue):
+// Warp roles (one CTA per SM, persistent over the CTA's plan queue; warp 5 issues the MMAs):
 //   warp 0      TMA producer: per page and 64-column half, one box {64 d, B_c tokens} of the
 //               4-D pool view (d, kv head, slot, page) — the BSR `indices` give the page coordinate
 //               (the sparse gather of §3.2.1, done by TMA). Runs ahead across items
 //               through a kStages-deep smem ring.
 //   warps 1..4  128 threads: thread = TMEM lane = token (softmax) = head-dim row d (output).
-//               One elected thread issues the MMAs. Online softmax in the log2 domain with
+//   warp 5      MMA issuer: S^T(t) as soon as K(t) landed and the S^T buffer was read, PV(t-1)
+//               once P(t-1) is written (s_free / p_full / o_free barriers), so the ~35-cycle
+//               per-instruction MMA issue stays off the softmax chain. Online softmax in the log2 domain with
 //               lazy rescaling: O^T accumulates in TMEM across tiles and is rescaled only when a
 //               row max grows by more than 2^8 (the final o = O/l and lse use the same max, so the
 //               result is exact). S^T and P^T are double-buffered and the next tile's S MMA is
@@ -77,7 +79,7 @@ constexpr int kOffP = kOffQ + 2 * kQBytes;   // two P^T buffers
 constexpr int kOffBar = kOffP + 2 * kPBytes;
 constexpr int kOffRed = kOffBar + 256;
 constexpr int kSmemBytes = kOffRed + 2 * 4 * kN * 4 + 64 + 1024;  // red, red2, vote flags + alignment slack
-constexpr int kThreads = 160;
+constexpr int kThreads = 192;  // producer, 4 softmax warps, MMA warp
 constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T at col 32
 constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
 }  // namespace dec
@@ -119,7 +121,10 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   uint64_t* empty_q = full_q + 2;        // [2]
   uint64_t* bar_s = empty_q + 2;         // [2] S^T buffer ready
   uint64_t* bar_pv = bar_s + 2;          // [2] PV MMA reading P^T buffer b done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_pv + 2);
+  uint64_t* s_free = bar_pv + 2;         // [2] softmax read S^T buffer b (4 warp arrivals)
+  uint64_t* p_full = s_free + 2;         // [2] P^T buffer b written (1 arrival)
+  uint64_t* o_free = p_full + 2;         // [1] epilogue read O^T (1 arrival)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [4 warps][kN]
   float* red2 = red + 4 * kN;
 
@@ -138,15 +143,18 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       ptx::mbar_init(&empty_q[b], 1);
       ptx::mbar_init(&bar_s[b], 1);
       ptx::mbar_init(&bar_pv[b], 1);
+      ptx::mbar_init(&s_free[b], 4);
+      ptx::mbar_init(&p_full[b], 1);
     }
+    ptx::mbar_init(o_free, 1);
     ptx::fence_barrier_init();
   }
-  if (warp >= 1) {  // zero both P^T buffers once: rows >= kC stay zero for the kernel's lifetime
+  if (warp >= 1 && warp <= 4) {  // zero both P^T buffers once: rows >= kC stay zero for the kernel's lifetime
     uint4* pz = reinterpret_cast<uint4*>(smem + kOffP);
     for (int i = threadIdx.x - 32; i < 2 * kPBytes / 16; i += 128) pz[i] = make_uint4(0, 0, 0, 0);
     ptx::fence_proxy_async();
   }
-  if (warp == 1) ptx::tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == 5) ptx::tmem_alloc<kTmemCols>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -216,42 +224,88 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         }
       }
     }
+  } else if (warp == 5) {
+    // ================================ MMA issuer ================================
+    // S^T(t) as soon as K(t) landed and the softmax has read the S^T buffer; PV(t-1) once P(t-1)
+    // is written: the MMA issue latency stays off the softmax chain.
+    const uint32_t fmt = tp.f16 ? 0u : 1u;
+    const uint32_t idS = ptx::idesc_f16(fmt, 128, kN, 0, 0);  // A = K (K-major), B = Q (K-major)
+    const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
+    const uint32_t sbase = ptx::smem_u32(smem);
+    int stage = 0, sb = 0, pb = 0, qb = 0;
+    uint32_t fphase = 0, ofph = 1;
+    uint32_t sfph[2] = {1, 1}, pfph[2] = {0, 0}, qphase[2] = {0, 0};
+    auto issue_pv = [&](int ti, int st) {  // PV of the item's tile ti, staged in ring stage st
+      ptx::mbar_wait(&p_full[pb], pfph[pb]);
+      pfph[pb] ^= 1;
+      ptx::tc_fence_after();
+      const uint64_t a0 = ptx::smem_desc_sw128(sbase + st * kStageBytes + kKVBytes, kHalfBytes, 1024);
+      const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffP + pb * kPBytes, 16, 1024);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t sbo = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
+        ptx::mma_f16_ss_warp(tmem + 32, a0 + (uint64_t)(kk * 128), b0 + sbo, idO, (ti > 0 || kk > 0) ? 1u : 0u);
+      }
+      ptx::mma_commit_warp(&empty[st]);  // K/V stage free once these MMAs complete
+      ptx::mma_commit_warp(&bar_pv[pb]);
+      pb ^= 1;
+    };
+    for (int it = it0; it < it1; ++it) {
+      const DecItem d = dec_item(pv, it, g);
+      ptx::mbar_wait(&full_q[qb], qphase[qb]);
+      qphase[qb] ^= 1;
+      if (d.ntiles == 0) {
+        ptx::mbar_arrive_warp(&empty_q[qb]);
+        qb ^= 1;
+        continue;
+      }
+      const uint64_t bq = ptx::smem_desc_sw128(sbase + kOffQ + qb * kQBytes, 16, 1024);
+      int pstage = 0;
+      for (int ti = 0; ti < d.ntiles; ++ti) {
+        ptx::mbar_wait(&full[stage], fphase);
+        ptx::mbar_wait(&s_free[sb], sfph[sb]);
+        sfph[sb] ^= 1;
+        ptx::tc_fence_after();
+        const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes, 16, 1024);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t sa = (uint64_t)((kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2);
+          const uint64_t sbo = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
+          ptx::mma_f16_ss_warp(tmem + sb * 16, a0 + sa, bq + sbo, idS, kk > 0);
+        }
+        ptx::mma_commit_warp(&bar_s[sb]);
+        if (ti + 1 == d.ntiles) ptx::mma_commit_warp(&empty_q[qb]);  // last reader of this Q buffer
+        sb ^= 1;
+        if (ti == 0) {  // the item's first PV overwrites O: the previous epilogue must have read it
+          ptx::mbar_wait(o_free, ofph);
+          ofph ^= 1;
+        } else {
+          issue_pv(ti - 1, pstage);
+        }
+        pstage = stage;
+        if (++stage == kStages) {
+          stage = 0;
+          fphase ^= 1;
+        }
+      }
+      issue_pv(d.ntiles - 1, pstage);
+      qb ^= 1;
+    }
   } else {
-    // ===================== softmax / MMA / epilogue warps =====================
+    // ===================== softmax / epilogue warps (1..4) =====================
     const int ct = threadIdx.x - 32;         // 0..127
     const int q4 = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = q4 * 32 + lane;          // TMEM lane: token (softmax) / head-dim d (output)
     const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
     const uint32_t tO = tmem + lane_addr + 32;
-    const uint32_t fmt = tp.f16 ? 0u : 1u;
-    const uint32_t idS = ptx::idesc_f16(fmt, 128, kN, 0, 0);  // A = K (K-major), B = Q (K-major)
-    const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
-    const uint32_t sbase = ptx::smem_u32(smem);
-    // pipeline state (identical in every compute thread)
+    // pipeline state (identical in every softmax thread)
     int stage = 0;            // ring stage of the tile being processed
     uint32_t fphase = 0;      // its full-barrier parity
     uint32_t sph[2] = {0, 0}, pvph[2] = {0, 0};
     bool pv_pending[2] = {false, false};
     int sbuf = 0;             // S^T buffer of the tile being processed
     int pbuf = 0;             // P^T buffer to write next
-    uint32_t qphase[2] = {0, 0};
-    int qb = 0;
-    int tpar = 0;  // tile count (parity selects the vote-flag buffer)
-
-    // elected thread: issue S^T(tile in `st`, buffer `b`) = K Q^T
-    // issued by all 32 lanes of warp 1 (elect.sync inside the asm keeps the warp converged)
-    auto issue_S = [&](int st, int b, uint32_t qaddr) {
-      ptx::tc_fence_after();
-      const uint64_t a0 = ptx::smem_desc_sw128(sbase + st * kStageBytes, 16, 1024);
-      const uint64_t b0 = ptx::smem_desc_sw128(qaddr, 16, 1024);
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const uint64_t sa = (uint64_t)((kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2);
-        const uint64_t sb = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
-        ptx::mma_f16_ss_warp(tmem + b * 16, a0 + sa, b0 + sb, idS, kk > 0);
-      }
-      ptx::mma_commit_warp(&bar_s[b]);
-    };
+    int tpar = 0;             // tile count (parity selects the vote-flag buffer)
     auto wait_pv = [&](int b) {
       if (pv_pending[b]) {
         ptx::mbar_wait(&bar_pv[b], pvph[b]);
@@ -262,9 +316,6 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
 
     for (int it = it0; it < it1; ++it) {
       const DecItem d = dec_item(pv, it, g);
-      const uint32_t qaddr = sbase + kOffQ + qb * kQBytes;
-      ptx::mbar_wait(&full_q[qb], qphase[qb]);
-      qphase[qb] ^= 1;
       float m[kC], lp[kC];
       int64_t lim[kC];
 #pragma unroll
@@ -274,28 +325,21 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         const int tok = (d.row0 + c) / g;
         lim[c] = kMask == 1 ? d.lk - d.lq + tok : (kMask == 2 ? p.mask_indptr[d.req] + (int64_t)tok * d.lk : 0);
       }
-      // prologue: S^T of tile 0
-      bool next_issued = false;
-      if (d.ntiles > 0 && warp == 1) {
-        ptx::mbar_wait(&full[stage], fphase);
-        issue_S(stage, sbuf, qaddr);
-      }
       for (int ti = 0; ti < d.ntiles; ++ti) {
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
         const int n = (int)imin64(kTile, d.ke - t0);
-        const int nstage = stage + 1 == kStages ? 0 : stage + 1;
-        const uint32_t nfphase = nstage == 0 ? fphase ^ 1 : fphase;
-        // early issue of the next S^T when its K tile has already landed
-        next_issued = false;
-        if (warp == 1 && ti + 1 < d.ntiles && ptx::mbar_test_wait_warp(&full[nstage], nfphase)) {
-          issue_S(nstage, sbuf ^ 1, qaddr);
-          next_issued = true;
-        }
         ptx::mbar_wait(&bar_s[sbuf], sph[sbuf]);
         sph[sbuf] ^= 1;
-        uint8_t* vS = smem + stage * kStageBytes + kKVBytes;
+        ptx::tc_fence_after();
+        float s[kC];
+        ptx::tmem_ld<kC>(tmem + lane_addr + sbuf * 16, s);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&s_free[sbuf]);  // the MMA warp may reuse this S^T buffer
         if (n < kTile && row >= n) {  // rows past the chunk: zero V so 0 * garbage cannot poison O
           ptx::mbar_wait(&full[stage], fphase);  // (already complete) orders the TMA writes before ours
+          uint8_t* vS = smem + stage * kStageBytes + kKVBytes;
           uint4 z = make_uint4(0, 0, 0, 0);
           uint4* v0 = reinterpret_cast<uint4*>(vS + row * 128);
           uint4* v1 = reinterpret_cast<uint4*>(vS + kHalfBytes + row * 128);
@@ -304,13 +348,8 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
             v0[j] = z;
             v1[j] = z;
           }
-          ptx::fence_proxy_async();
         }
-        ptx::tc_fence_after();
-        float s[kC];
-        ptx::tmem_ld<kC>(tmem + lane_addr + sbuf * 16, s);
-        ptx::tmem_ld_wait();
-        // ---- mask + scale, column max over the 128 tokens
+        // ---- mask + scale
         const int64_t t = t0 + row;
         const bool tok_ok = row < n;
 #pragma unroll
@@ -349,8 +388,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           }
         };
         store_p();
-        ptx::fence_proxy_async();
-        ptx::tc_fence_before();
+        ptx::fence_proxy_async();  // P (and zeroed V rows) visible to the tensor core
         ptx::named_bar_sync(1, 128);
         if (flags[0] | flags[1] | flags[2] | flags[3]) {  // slow path
           float mx[kC];
@@ -382,7 +420,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
             pr[c] = s[c] == -INFINITY ? 0.f : exp2f(s[c] - m[c]);
             lp[c] *= alpha[c];
           }
-          if (rescale) {  // bring O^T to the new max (no PV MMA may be in flight)
+          if (rescale) {  // bring O^T to the new max (PV(t-1) done; PV(t) waits for p_full)
             wait_pv(pbuf ^ 1);
             ptx::tc_fence_after();
             float ov[kC];
@@ -400,35 +438,18 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         }
 #pragma unroll
         for (int c = 0; c < kC; ++c) lp[c] += pr[c];
+        if (ct == 0) ptx::mbar_arrive(&p_full[pbuf]);  // the MMA warp issues PV(t)
         ++tpar;
-        // ---- O^T += V^T P^T ; then the next S^T if it was not issued early
-        if (warp == 1) {
-          ptx::tc_fence_after();
-          const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes + kKVBytes, kHalfBytes, 1024);
-          const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffP + pbuf * kPBytes, 16, 1024);
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t sb = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
-            ptx::mma_f16_ss_warp(tmem + 32, a0 + (uint64_t)(kk * 128), b0 + sb, idO, (ti > 0 || kk > 0) ? 1u : 0u);
-          }
-          ptx::mma_commit_warp(&empty[stage]);  // K/V stage free once these MMAs complete
-          ptx::mma_commit_warp(&bar_pv[pbuf]);
-          if (!next_issued && ti + 1 < d.ntiles) {
-            ptx::mbar_wait(&full[nstage], nfphase);
-            issue_S(nstage, sbuf ^ 1, qaddr);
-          }
-        }
         pv_pending[pbuf] = true;
         pbuf ^= 1;
         sbuf ^= 1;
-        stage = nstage;
-        fphase = nfphase;
+        if (++stage == kStages) {
+          stage = 0;
+          fphase ^= 1;
+        }
       }
-      // Q buffer no longer read once every MMA of this item completed (PV waits below cover them)
       wait_pv(0);
       wait_pv(1);
-      if (ct == 0) ptx::mbar_arrive(&empty_q[qb]);
-      qb ^= 1;
       pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
       // ---- epilogue: denominators (sum over the 128 token lanes), normalise, write
       float ov[kC];
@@ -446,6 +467,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       }
       ptx::tc_fence_before();
       ptx::named_bar_sync(1, 128);
+      if (ct == 0 && d.ntiles > 0) ptx::mbar_arrive(o_free);  // O^T read: the next item's PV may overwrite it
 #pragma unroll
       for (int c = 0; c < kC; ++c) {
         if (c < d.nrows) {
@@ -479,7 +501,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   ptx::tc_fence_before();
   __syncthreads();
   if (p.trace && threadIdx.x == 0) p.trace[17 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
-  if (warp == 1) ptx::tmem_dealloc<kTmemCols>(tmem);
+  if (warp == 5) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 
 }  // namespace bsra
