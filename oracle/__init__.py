@@ -59,9 +59,12 @@ def _load():
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_double, ctypes.c_double, P, P, P, P, P,
                                             ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                                            ctypes.c_int,
                                             P, ctypes.c_int, P, P, ctypes.c_int]
         lib.orc_merge.restype = None
         lib.orc_merge.argtypes = [ctypes.c_int64, ctypes.c_int, P, P, P, P, P, P]
+        lib.orc_alibi_slope.restype = ctypes.c_double
+        lib.orc_alibi_slope.argtypes = [ctypes.c_int, ctypes.c_int]
         lib.orc_decode.restype = ctypes.c_double
         lib.orc_decode.argtypes = [ctypes.c_int, ctypes.c_uint32]
         _lib = lib
@@ -72,13 +75,30 @@ def _ptr(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
+def alibi_slope(h: int, H: int) -> float:
+    """ALiBi slope of qo head h of H (C oracle; R30)."""
+    return _load().orc_alibi_slope(int(h), int(H))
+
+
+def alibi_slopes_numpy(H: int) -> np.ndarray:
+    """ALiBi slopes written from Press et al.'s construction (different code from the C oracle):
+    the geometric sequence 2^(-8/n), 2^(-16/n), ... for n = the largest power of two <= H, then
+    every other term of the 2n sequence for the remaining H - n heads."""
+    n = 2 ** int(np.floor(np.log2(H)))
+    base = 2.0 ** (-8.0 / n)
+    pow2 = [base ** (i + 1) for i in range(n)]
+    base2 = 2.0 ** (-8.0 / (2 * n))
+    extra = [base2 ** (i + 1) for i in range(2 * n)][0::2][:H - n]
+    return np.array(pow2 + extra, np.float64)
+
+
 def decode_scalar(dtype: str, bits: int) -> float:
     return _load().orc_decode(DT_CODE[dtype], int(bits))
 
 
 def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
                     k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
-                    mask_bit_indptr=None, sm_scale, window: int = 0, soft_cap: float = 0.0,
+                    mask_bit_indptr=None, sm_scale, window: int = 0, soft_cap: float = 0.0, alibi: bool = False,
                     kv_dtype: Optional[str] = None, k_scale: float = 1.0, v_scale: float = 1.0,
                     req_list: Optional[Sequence[int]] = None, num_threads: int = 0, out=None):
     """float64 oracle (C). Array arguments are host numpy arrays; ``q``/pools hold raw
@@ -111,7 +131,7 @@ def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indi
                                  _ptr(kv_page_indices), H_qo, H_kv, D, page_size, DT_CODE[dtype],
                                  DT_CODE[kv_dtype or dtype], float(k_scale), float(v_scale), _ptr(q),
                                  _ptr(k_pool), _ptr(v_pool), _ptr(ks), _ptr(vs), MASK_CODE[mask], _ptr(cm),
-                                 _ptr(mb), float(sm_scale), int(window), float(soft_cap), _ptr(rl),
+                                 _ptr(mb), float(sm_scale), int(window), float(soft_cap), int(bool(alibi)), _ptr(rl),
                                  0 if rl is None else len(rl), _ptr(o),
                                  _ptr(lse), int(num_threads))
     if rc != 0:
@@ -130,7 +150,7 @@ def attention_from_inputs(inp, req_list=None, num_threads=0):
         H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
         custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
         mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap,
-        kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale,
+        alibi=wl.alibi, kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale,
         req_list=req_list, num_threads=num_threads)
 
 
@@ -162,7 +182,8 @@ def to_float64(bits: np.ndarray, dtype: str) -> np.ndarray:
 
 def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
                 k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
-                mask_bit_indptr=None, sm_scale, window=0, soft_cap=0.0, kv_dtype=None, k_scale=1.0, v_scale=1.0):
+                mask_bit_indptr=None, sm_scale, window=0, soft_cap=0.0, alibi=False, kv_dtype=None, k_scale=1.0,
+                v_scale=1.0):
     """NumPy brute force (tiny inputs): dense un-paged K/V per request, the full masked
     score matrix, float64 softmax. Same definition as the C oracle, different code.
     fp8 KV: pools of ``kv_dtype`` scaled by k_scale / v_scale.
@@ -201,6 +222,9 @@ def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices,
         S = sm_scale * np.einsum("rhd,thd->hrt", qf[q0:q1], Kr)  # [H, lq, lk]
         if soft_cap > 0:
             S = soft_cap * np.tanh(S / soft_cap)
+        if alibi:  # slope_h * (t - p), p = l_kv - l_qo + r (R30)
+            rel = np.arange(lk)[None, :] - (lk - lq + np.arange(lq))[:, None]
+            S = S + alibi_slopes_numpy(H_qo)[:, None, None] * rel[None]
         if mask == "none":
             vis = np.ones((lq, lk), bool)
         elif mask == "causal":
@@ -233,7 +257,7 @@ def brute_force_from_inputs(inp):
         H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
         custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
         mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap,
-        kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale)
+        alibi=wl.alibi, kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale)
 
 
 # --------------------------------------------------------------------- ⊕ ---

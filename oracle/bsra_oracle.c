@@ -22,6 +22,11 @@
  *     additionally hides t < l_kv - l_qo + r - W + 1 (W keys up to the row's own position).
  *   - LogitsTransform variant, logits soft-cap (R27): cap c > 0 replaces
  *     the scaled logit s by c * tanh(s / c) before Eq. 1-2.
+ *   - LogitsTransform variant, ALiBi bias (App. G Table "ALiBi Bias", PAPER.md:554;
+ *     DESIGN.md R30): with alibi != 0 the logit of key t for query row r of qo head h becomes
+ *     s + slope_h * (t - p), p = l_kv - l_qo + r the row's right-aligned position, applied after
+ *     the soft-cap; slope_h from Press et al.: n = 2^floor(log2 H_qo); h < n: 2^(-8(h+1)/n),
+ *     else 2^(-4(2(h-n)+1)/n).
  *   - Eq. 1: lse = log sum_{t in vis} exp(s_t), s_t = sm_scale * q.k_t
  *     (R1: the logits are scaled by sm_scale; R2: natural log).
  *   - Eq. 2: o = sum_{t in vis} exp(s_t) / exp(lse) * v_t
@@ -98,6 +103,14 @@ static double orc_load(const void* base, int dtype, int64_t idx) {
 
 int orc_version(void) { return 1; }
 
+/* ALiBi slope of qo head h of H (Press et al. 2022; R30). */
+double orc_alibi_slope(int h, int H) {
+  int n = 1;
+  while (2 * n <= H) n *= 2;
+  if (h < n) return pow(2.0, -8.0 * (h + 1) / n);
+  return pow(2.0, -4.0 * (2 * (h - n) + 1) / n);
+}
+
 /* Exposed for the closed-form pins of the decoders themselves. */
 double orc_decode(int dtype, uint32_t bits) {
   if (dtype == ORC_F32) {
@@ -124,7 +137,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
                         double k_scale, double v_scale, const void* q,
                         const void* k_pool, const void* v_pool, const int64_t* k_strides,
                         const int64_t* v_strides, int mask_mode, const uint8_t* custom_mask,
-                        const int64_t* mask_bit_indptr, double sm_scale, int window, double soft_cap,
+                        const int64_t* mask_bit_indptr, double sm_scale, int window, double soft_cap, int alibi,
                         const int32_t* req_list, int n_req_list, double* o_out, double* lse_out,
                         int num_threads) {
   if (batch < 0 || H_qo <= 0 || H_kv <= 0 || H_qo % H_kv != 0 || D <= 0 || page_size <= 0) return 1;
@@ -212,6 +225,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
           for (int d = 0; d < D; ++d) dot += orc_load(q, dtype, qbase + d) * (k_scale * orc_load(k_pool, kv_dtype, kb + d));
           s[a] = sm_scale * dot;
           if (soft_cap > 0.0) s[a] = soft_cap * tanh(s[a] / soft_cap);
+          if (alibi) s[a] += orc_alibi_slope(h, H_qo) * (double)(t - (l_kv - l_qo + r));
           if (s[a] > m) m = s[a];
         }
         /* pass 2: normaliser, lse, output (Eq. 1-2) */

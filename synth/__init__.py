@@ -50,6 +50,7 @@ class Workload:
     window: int = 0       # sliding window W (0 = off), R26
     soft_cap: float = 0.0  # logits soft-cap c (0 = off), R27
     kv_dtype: str = ""     # "" = dtype; "e4m3" = fp8 KV cache with fp16/bf16 q and o (R28)
+    alibi: bool = False    # ALiBi bias (R30)
 
     @property
     def batch(self) -> int:

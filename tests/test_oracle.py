@@ -546,3 +546,53 @@ def test_fp8_kv_scales_closed_forms():
     fin = np.isfinite(base[1])
     assert np.max(np.abs(vs[0] - (-2.5) * base[0])) < 1e-12
     assert np.array_equal(vs[1][fin], base[1][fin])
+
+
+# ------------------------------------------- ALiBi bias (NEXT-3; R30)
+@pytest.mark.parametrize("H", [1, 2, 4, 6, 8, 12, 32, 40, 64])
+def test_alibi_slopes_c_vs_numpy_and_closed_forms(H):
+    """C slopes == NumPy construction; power-of-two H gives 2^(-8(h+1)/H) (Press et al.)."""
+    c = np.array([oracle.alibi_slope(h, H) for h in range(H)])
+    assert np.allclose(c, oracle.alibi_slopes_numpy(H), rtol=1e-14, atol=0)
+    if H & (H - 1) == 0:
+        assert np.allclose(c, [2.0 ** (-8.0 * (h + 1) / H) for h in range(H)], rtol=1e-15)
+    assert oracle.alibi_slope(0, 8) == 0.5 and oracle.alibi_slope(7, 8) == 2.0 ** -8
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_alibi_c_oracle_matches_numpy_brute_force(seed):
+    rng = np.random.default_rng(9000 + seed)
+    wl = synth.random_workload(rng, dtype=["f32", "bf16"][seed % 2], mask=synth.MASKS[seed % 3],
+                               heads=((4, 1), (8, 2), (6, 3), (12, 4)))
+    import dataclasses
+    wl = dataclasses.replace(wl, alibi=True, window=int(rng.integers(1, 30)) if seed % 4 == 1 else 0,
+                             soft_cap=5.0 if seed % 4 == 2 else 0.0)
+    inp = _inp(wl, seed_base=seed)
+    _cmp(_run(inp), oracle.brute_force_from_inputs(inp), 1e-12)
+
+
+def test_alibi_closed_form_identical_keys():
+    """All keys equal: the logits differ only by the bias slope*(t - p), so the weights are
+    softmax(slope * (t - p)) and lse = s0 + ln sum_t e^{slope (t - p)} — a geometric series."""
+    lk, H, D = 9, 4, 8
+    q = np.ones((1, H, D)) * 0.25
+    K = np.tile(np.linspace(-1, 1, D), (lk, H, 1))
+    V = np.random.default_rng(2).uniform(-1, 1, (lk, H, D))
+    o, lse = oracle.paged_attention(**_single_request(q, K, V, page_size=4, sm_scale=0.5), alibi=True)
+    qf, Kf, Vf = (x.astype(np.float32).astype(np.float64) for x in (q, K, V))
+    for h in range(H):
+        m = 2.0 ** (-8.0 * (h + 1) / H)
+        s0 = 0.5 * float(qf[0, h] @ Kf[0, h])
+        w = np.exp(m * (np.arange(lk) - (lk - 1)))
+        assert abs(lse[0, h] - (s0 + np.log(w.sum()))) < 1e-13
+        assert np.allclose(o[0, h], (w[:, None] * Vf[:, h]).sum(0) / w.sum(), atol=1e-14)
+
+
+def test_alibi_single_key_bias_cancels():
+    """One visible key: the bias shifts lse by slope*(t - p) and leaves o = v."""
+    q = np.array([[[1.0, 0.5]] * 2])
+    K = np.array([[[0.3, -0.2]] * 2])
+    V = np.array([[[0.7, -0.4]] * 2])
+    a = oracle.paged_attention(**_single_request(q, K, V, sm_scale=1.0), alibi=True)
+    b = oracle.paged_attention(**_single_request(q, K, V, sm_scale=1.0))
+    assert np.allclose(a[0], b[0], atol=1e-15) and np.allclose(a[1], b[1], atol=1e-15)  # t == p: bias 0
