@@ -95,7 +95,11 @@ typedef struct {
   int32_t kv_dtype;
   float k_scale;
   float v_scale;
-  int32_t reserved[1];       /* must be zero                                                    */
+  /* ALiBi bias (a LogitsTransform, P:228 / P:554; R30): 1 => the scaled logit of key t
+   * for query row r of qo head h gets + slope_h * (t - p), p = l_kv - l_qo + r, after the soft-cap;
+   * slope_h = 2^(-8(h+1)/n) for h < n = 2^floor(log2 H_qo), else 2^(-4(2(h-n)+1)/n). 0 = off. */
+  int32_t alibi;
+  int32_t reserved[3];       /* must be zero                                                    */
 } bsra_config;
 
 /* flags: BSRA_FLAG_PDL launches the tcgen05 kernels with programmatic dependent launch: a run()

@@ -39,7 +39,7 @@ class Config(ctypes.Structure):
                 ("kv_chunk_min", ctypes.c_int32), ("kernel", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("sliding_window", ctypes.c_int32), ("logits_soft_cap", ctypes.c_float),
                 ("kv_dtype", ctypes.c_int32), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float),
-                ("reserved", ctypes.c_int32 * 1)]
+                ("alibi", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
 
 
 FLAG_PDL = 1  # BSRA_FLAG_PDL (include/bsra.h)
@@ -114,13 +114,14 @@ def _i32(a) -> np.ndarray:
 def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="none", max_batch=1,
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
                 kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False, window=0,
-                soft_cap=0.0, kv_dtype=None, k_scale=0.0, v_scale=0.0) -> Config:
+                soft_cap=0.0, kv_dtype=None, k_scale=0.0, v_scale=0.0, alibi=False) -> Config:
     """window: sliding window W (0 = off, DESIGN.md R26); soft_cap: logits soft-cap c (0 = off, R27);
     kv_dtype "e4m3": fp8 KV cache with per-tensor scales k_scale / v_scale (0 = 1; R28)."""
     c = Config()
     if kv_dtype:
         c.kv_dtype = DTYPE[kv_dtype] if isinstance(kv_dtype, str) else kv_dtype
     c.k_scale, c.v_scale = float(k_scale), float(v_scale)
+    c.alibi = 1 if alibi else 0
     c.sliding_window, c.logits_soft_cap = int(window), float(soft_cap)
     c.flags = (FLAG_PDL if pdl else 0) | (FLAG_RAGGED_KV if ragged_kv else 0)
     c.num_qo_heads, c.num_kv_heads, c.head_dim, c.page_size = H_qo, H_kv, D, page_size

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
       const int head = kvh * g + f % g;
       const int64_t causal_lim = lk - lq + tok;  // visible iff t <= lim (right aligned)
       const int64_t mbase = p.mask_mode == 2 ? p.mask_indptr[req] + (int64_t)tok * lk : 0;
+      const float slope = p.alibi ? alibi_slope_raw(p, head) : 0.f;  // ALiBi (R30)
 
       // q row in registers (every lane holds all D values for the lane = token dot products)
       float qv[D];
@@ -129,7 +130,9 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
 #pragma unroll
             for (int e = 0; e < kVecK; ++e) dot = fmaf(qv[c * kVecK + e], kf[e], dot);
           }
-          s = (p.soft_cap > 0.f ? soft_cap_raw(p, dot) : dot) * p.scale_log2;  // soft-cap (R27)
+          float sr = p.soft_cap > 0.f ? soft_cap_raw(p, dot) : dot;  // soft-cap (R27)
+          if (p.alibi) sr += slope * (float)(t - causal_lim);         // ALiBi (R30): t - p
+          s = sr * p.scale_log2;
         }
         const float mt = warp_max(s);
         const float mnew = fmaxf(m, mt);

@@ -44,6 +44,9 @@ struct AttnParams {
   // fp8 KV cache (R28): pools hold E4M3 bytes; v_scale multiplies o
   int32_t kv_f8;
   float v_scale;
+  // ALiBi (R30): raw score s += slope_h / logit_scale * (t - p)
+  int32_t alibi;
+  float inv_logit_scale;
 };
 
 // LogitsTransform soft-cap on a raw score (R27): s -> c * tanh(s / c), c in raw units.
@@ -55,6 +58,14 @@ __device__ __forceinline__ float soft_cap_raw(const AttnParams& p, float s) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(s * p.inv_soft_cap * 2.8853900817779268f));  // 2 log2(e)
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.f));
   return p.soft_cap * fmaf(-2.f, r, 1.f);
+}
+
+// ALiBi slope of qo head h of H in raw q.k units (R30); fp64 once per row for a correctly
+// rounded slope (n = 2^floor(log2 H); h < n: 2^(-8(h+1)/n), else 2^(-4(2(h-n)+1)/n))
+__device__ __forceinline__ float alibi_slope_raw(const AttnParams& p, int h) {
+  const int n = 1 << (31 - __clz(p.H_qo));
+  const double e = h < n ? -8.0 * (h + 1) / n : -4.0 * (2 * (h - n) + 1) / n;
+  return (float)(exp2(e) * (double)p.inv_logit_scale);
 }
 
 struct PlanView {

@@ -82,7 +82,9 @@ bsra_status validate_config(const bsra_config& c) {
     return fail(BSRA_EINVAL, "an E4M3 KV cache takes F16 or BF16 q / o (P:499)");
   if (!(c.k_scale >= 0.f) || !std::isfinite(c.k_scale) || !(c.v_scale >= 0.f) || !std::isfinite(c.v_scale))
     return fail(BSRA_EINVAL, "k_scale / v_scale must be finite and >= 0");
-  if (c.reserved[0]) return fail(BSRA_EINVAL, "reserved fields must be zero");
+  if (c.alibi != 0 && c.alibi != 1) return fail(BSRA_EINVAL, "alibi must be 0 or 1");
+  for (int i = 0; i < 3; ++i)
+    if (c.reserved[i]) return fail(BSRA_EINVAL, "reserved fields must be zero");
   return BSRA_OK;
 }
 
@@ -482,6 +484,8 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   p.T_slot = e->lay.T_max;
   p.D = c.head_dim;
   p.scale_log2 = logit_scale * bsra::kLog2e;
+  p.alibi = c.alibi;
+  p.inv_logit_scale = 1.f / logit_scale;  // ALiBi bias in raw q.k units (R30)
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = c.num_ctas;

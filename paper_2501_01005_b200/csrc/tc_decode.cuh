@@ -316,13 +316,14 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
 
     for (int it = it0; it < it1; ++it) {
       const DecItem d = dec_item(pv, it, g);
-      float m[kC], lp[kC];
+      float m[kC], lp[kC], aslope[kC];
       int64_t lim[kC];
 #pragma unroll
       for (int c = 0; c < kC; ++c) {
         m[c] = -INFINITY;
         lp[c] = 0.f;
         const int tok = (d.row0 + c) / g;
+        aslope[c] = p.alibi ? alibi_slope_raw(p, d.kvh * g + (d.row0 + c) % g) : 0.f;  // ALiBi (R30)
         lim[c] = kMask == 1 ? d.lk - d.lq + tok : (kMask == 2 ? p.mask_indptr[d.req] + (int64_t)tok * d.lk : 0);
       }
       for (int ti = 0; ti < d.ntiles; ++ti) {
@@ -358,7 +359,8 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           if (kMask == 1) vis = vis && t <= lim[c];
           if (kMask == 2) vis = vis && mask_bit(p.mask, lim[c] + t);
           if (p.window > 0) vis = vis && t >= d.lk - d.lq + (d.row0 + c) / g - p.window + 1;  // R26
-          const float sc = p.soft_cap > 0.f ? soft_cap_raw(p, s[c]) : s[c];                // R27
+          float sc = p.soft_cap > 0.f ? soft_cap_raw(p, s[c]) : s[c];                      // R27
+          if (p.alibi) sc += aslope[c] * (float)(t - (d.lk - d.lq + (d.row0 + c) / g));  // R30
           s[c] = vis ? sc * p.scale_log2 : -INFINITY;
         }
         // ---- stale-max softmax (lazy rescale, exact: o and lse use the same max): P = 2^(s - m)

@@ -471,7 +471,7 @@ inline int tc_prefill_launch(const AttnParams& p, const TcLaunch& L, cudaStream_
   }
   cudaError_t e;
   static const bool v1 = getenv("BSRA_PREFILL_V1") != nullptr;  // A/B against the one-warpgroup kernel
-  const bool variants = p.window > 0 || p.soft_cap > 0.f;  // the v1 A/B kernel has no variant support
+  const bool variants = p.window > 0 || p.soft_cap > 0.f || p.alibi;  // the v1 A/B kernel has no variant support
   if (L.T_q == 256) {  // paired: both softmax WGs on one item, every K/V tile feeds 256 rows
     switch (L.mask) {
       case 0: e = launch_prefill2_t<0, true>(tp, L.grid, st); break;

@@ -564,6 +564,10 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       // the general (per-element) path; plain tiles keep the fast path
       const int64_t wlo = kVar && p.window > 0 ? d.lk - d.lq + tok - p.window + 1 : INT64_MIN / 2;
       const bool capped = kVar && p.soft_cap > 0.f;
+      // ALiBi (R30): raw-unit bias aslope * (t - apos) on every element, after the soft-cap
+      const bool biased = kVar && p.alibi;
+      const float aslope = biased ? alibi_slope_raw(p, head) : 0.f;
+      const float apos = (float)(d.lk - d.lq + tok);
       float m = -INFINITY, l = 0.f;
       for (int ti = 0; ti < d.ntiles; ++ti) {
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
@@ -571,7 +575,8 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         const int64_t vis_end = row_ok ? (kMask == 1 ? imin64(lim + 1, t0 + n) : t0 + n) : t0;
         const int nvis = (int)(vis_end > t0 ? vis_end - t0 : 0);
         const int vbeg = kVar && wlo > t0 ? (int)imin64(wlo - t0, kTile) : 0;  // first visible column
-        const bool need_mask = kMask == 2 || nvis < kTile || vbeg > 0 || capped;
+        const bool need_mask = kMask == 2 || nvis < kTile || vbeg > 0 || capped || biased;
+        const float abase = aslope * ((float)t0 - apos);  // bias of column 0 of this tile
         ptx::mbar_wait(&bar_s[w], sph);
         sph ^= 1;
         if (r == 0) BSRA_TRACE(5 + 2 * w, tcount);
@@ -678,7 +683,9 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
             for (int j = 0; j < 64; ++j) {
               bool vis = c * 32 + j < nvis && c * 32 + j >= vbeg;
               if (kMask == 2) vis = vis && mask_bit(p.mask, mbase + t0 + c * 32 + j);
-              s[j] = vis ? s[j] : -INFINITY;
+              float x = s[j];
+              if (biased) x = (capped ? soft_cap_raw(p, x) : x) + fmaf(aslope, (float)(c * 32 + j), abase);
+              s[j] = vis ? x : -INFINITY;
             }
           }
           float a0 = fmaxf(s[0], s[1]), a1 = fmaxf(s[2], s[3]), a2 = fmaxf(s[4], s[5]), a3 = fmaxf(s[6], s[7]);
@@ -692,7 +699,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           mx = fmaxf(mx, fmaxf(fmaxf(a0, a1), fmaxf(a2, a3)));
         }
         // soft-cap is monotone, so the capped max is the cap of the raw max (-inf stays -inf)
-        const float mt = (capped && mx != -INFINITY ? soft_cap_raw(p, mx) : mx) * sc;
+        const float mt = (capped && !biased && mx != -INFINITY ? soft_cap_raw(p, mx) : mx) * sc;
         float alpha = 1.f;
         bool rescale = false;
         if (mt > m + kRescaleThresh) {
@@ -734,7 +741,9 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
             for (int j = 0; j < 32; ++j) {
               bool vis = c * 32 + j < nvis && c * 32 + j >= vbeg;
               if (kMask == 2) vis = vis && mask_bit(p.mask, mbase + t0 + c * 32 + j);
-              s[j] = vis ? (capped ? soft_cap_raw(p, s[j]) : s[j]) : -INFINITY;
+              float x = capped ? soft_cap_raw(p, s[j]) : s[j];
+              if (biased) x += fmaf(aslope, (float)(c * 32 + j), abase);
+              s[j] = vis ? x : -INFINITY;
             }
           }
           uint32_t pk[16];
@@ -860,7 +869,7 @@ inline cudaError_t launch_prefill2_f(const TcParams& tp, int grid, cudaStream_t 
 
 template <int kMask, bool kPair, bool kF16>
 inline cudaError_t launch_prefill2_v(const TcParams& tp, int grid, cudaStream_t st) {
-  const bool var = tp.p.window > 0 || tp.p.soft_cap > 0.f;
+  const bool var = tp.p.window > 0 || tp.p.soft_cap > 0.f || tp.p.alibi;
   return var ? launch_prefill2_f<kMask, kPair, kF16, true>(tp, grid, st)
              : launch_prefill2_f<kMask, kPair, kF16, false>(tp, grid, st);
 }

@@ -16,7 +16,7 @@ def engine_for(wl, *, num_ctas=0, tile_q=0, tile_set=(16, 64, 128, 256), kernel=
                            o_dtype=o_dtype, mask=wl.mask, max_batch=max_batch or max(1, wl.batch),
                            max_total_qo_rows=max_rows or max(1, int(wl.qo_lens.sum())), num_ctas=num_ctas,
                            tile_set=tile_set, tile_q=tile_q, kernel=kernel, kv_dtype=wl.kv_dtype or None,
-                           window=wl.window, soft_cap=wl.soft_cap)
+                           window=wl.window, soft_cap=wl.soft_cap, alibi=wl.alibi)
     return bsra.Engine(cfg, device)
 
 

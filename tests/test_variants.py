@@ -13,20 +13,22 @@ import synth
 from tests.helpers import assert_close, engine_for, rows_of_requests, run_gpu
 
 
-def _variant(wl, window=0, soft_cap=0.0):
-    return dataclasses.replace(wl, window=window, soft_cap=soft_cap)
+def _variant(wl, window=0, soft_cap=0.0, alibi=False):
+    return dataclasses.replace(wl, window=window, soft_cap=soft_cap, alibi=alibi)
 
 
 def _engine(wl, **kw):
     cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
                            mask=wl.mask, max_batch=max(1, wl.batch), max_total_qo_rows=max(1, int(wl.qo_lens.sum())),
-                           window=wl.window, soft_cap=wl.soft_cap, **kw)
+                           window=wl.window, soft_cap=wl.soft_cap, alibi=wl.alibi,
+                           kv_dtype=wl.kv_dtype or None, **kw)
     return bsra.Engine(cfg, 0)
 
 
 def _case(cuda_device, wl, *, seed=0, reqs=None, q_scale=1.0, **kw):
     inp = synth.make_inputs(wl, device=cuda_device, seed_base=seed, q_scale=q_scale)
-    gpu = run_gpu(inp, _engine(wl, **kw))
+    eng = _engine(wl, **kw)
+    gpu = run_gpu(inp, eng)
     ref = oracle.attention_from_inputs(inp, req_list=reqs)
     rows = rows_of_requests(inp, reqs) if reqs is not None else None
     assert_close(gpu, ref, wl.dtype, rows=rows, what=f"{wl.name} W={wl.window} cap={wl.soft_cap} {kw}")
@@ -117,3 +119,58 @@ def test_variants_on_contiguous_kv(cuda_device):
                            ragged_kv=True, window=wl.window, soft_cap=wl.soft_cap)
     assert_close(run_ragged(inp, bsra.Engine(cfg, 0)), oracle.attention_from_inputs(inp), "bf16",
                  what="contiguous KV + variants")
+
+
+# ------------------------------------------------------------------ ALiBi (R30)
+def test_alibi_config_validation_host():
+    L = bsra.lib()
+    n = ctypes.c_size_t()
+    cfg = bsra.make_config(H_qo=8, H_kv=2, D=128, page_size=16, max_batch=2, max_total_qo_rows=4, num_ctas=4, alibi=True)
+    assert L.bsra_workspace_bytes(ctypes.byref(cfg), 0, ctypes.byref(n)) == 0
+    cfg.alibi = 2
+    assert L.bsra_workspace_bytes(ctypes.byref(cfg), 0, ctypes.byref(n)) != 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mask", ["none", "causal", "custom"])
+@pytest.mark.parametrize("tile_q", [16, 64, 128, 256])
+@pytest.mark.parametrize("window,cap", [(0, 0.0), (200, 0.0), (0, 10.0)])
+def test_alibi_tc(cuda_device, mask, tile_q, window, cap):
+    wl = _variant(dataclasses.replace(_BASE, mask=mask), window, cap, alibi=True)
+    eng = _case(cuda_device, wl, seed=5, num_ctas=148, tile_q=tile_q, tile_set=(16, 64, 128, 256))
+    assert eng.selected_kernel() == ("tc_decode" if tile_q == 16 else "tc_prefill")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("H", [(32, 8), (40, 8), (12, 4)])
+def test_alibi_head_counts(cuda_device, H):
+    """Non-power-of-two head counts use the interleaved extra slopes (Press et al.)."""
+    wl = _variant(synth.Workload("alibiH", H[0], H[1], 128, 16, "bf16", "causal", np.array([1, 9, 130], np.int32),
+                                 np.array([700, 9, 400], np.int32)), alibi=True)
+    _case(cuda_device, wl, num_ctas=64)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("wl", [synth.c1_tiny_decode(), synth.Workload("d64", 8, 2, 64, 16, "bf16", "causal",
+                                                                          np.array([3, 40], np.int32),
+                                                                          np.array([200, 40], np.int32))],
+                         ids=["c1-f32", "d64-bf16"])
+def test_alibi_simt(cuda_device, wl):
+    eng = _case(cuda_device, _variant(wl, alibi=True), num_ctas=16)
+    assert eng.selected_kernel() == "simt"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile_q", [16, 128])
+def test_alibi_fp8_kv(cuda_device, tile_q):
+    """ALiBi with an E4M3 KV cache: fp8 decode kernel and the gather + prefill path."""
+    wl = dataclasses.replace(_variant(dataclasses.replace(_BASE, mask="causal"), alibi=True), kv_dtype="e4m3")
+    _case(cuda_device, wl, num_ctas=148, tile_q=tile_q, tile_set=(16, 64, 128, 256))
+
+
+@pytest.mark.gpu
+def test_alibi_split_kv(cuda_device):
+    wl = _variant(synth.Workload("split", 64, 8, 128, 16, "bf16", "causal", np.array([700, 1, 64], np.int32),
+                                 np.array([900, 3000, 64], np.int32)), 0, 0.0, alibi=True)
+    for nc in (1, 7, 148):
+        _case(cuda_device, wl, num_ctas=nc)
