@@ -98,7 +98,9 @@ __device__ __forceinline__ void e4m3x16_perm(const uint4& u, uint32_t* r) {
   e4m3x4_perm<kHalf>(u.w, r[6], r[7]);
 }
 
-template <int kC, int kMask>
+// kF16: fp16 q / o (else bf16) as a template parameter, so each instantiation carries one
+// converter (ncu: 37 % of warp samples stalled on instruction fetch with both inlined)
+template <int kC, int kMask, bool kF16>
 __global__ void __launch_bounds__(f8d::kThreads, 1) tc_decode_f8_kernel(const __grid_constant__ TcParams tp) {
   using namespace f8d;
   const AttnParams& p = tp.p;
@@ -165,9 +167,13 @@ __global__ void __launch_bounds__(f8d::kThreads, 1) tc_decode_f8_kernel(const __
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
   // debug timeline of CTA 0 (p.trace set; scripts/trace_decode_f8.py): clock64 per event and tile
+#ifdef BSRA_F8_TRACE
   long long* trace = blockIdx.x == 0 ? p.trace : nullptr;
 #define F8T(ev, i) \
   if (trace && (i) < 1024) trace[(ev) * 1024 + (i)] = clock64();
+#else
+#define F8T(ev, i)
+#endif
   if (threadIdx.x == 0) F8T(9, 0);
   int tpos = 0;  // tiles seen by this role (trace index)
 
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(f8d::kThreads, 1) tc_decode_f8_kernel(const __
 #pragma unroll
         for (int h = 0; h < 4; ++h) {  // 32 d per step: two fp8 chunks -> 16 columns
           uint32_t r[16];
-          if (tp.f16) {
+          if constexpr (kF16) {
             e4m3x16_perm<true>(u[2 * h], r);
             e4m3x16_perm<true>(u[2 * h + 1], r + 8);
           } else {
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(f8d::kThreads, 1) tc_decode_f8_kernel(const __
 #pragma unroll
           for (int j = 0; j < 8; ++j) {  // fp8 chunk j (d 16j..16j+15) -> 16-bit chunks 2j, 2j+1
             uint32_t r[8];
-            if (tp.f16) e4m3x16_perm<true>(u[j], r);
+            if constexpr (kF16) e4m3x16_perm<true>(u[j], r);
             else e4m3x16_perm<false>(u[j], r);
             uint8_t* hb = dst + (j >> 2) * kHalfBytes;
             const int c0 = (2 * j) & 7;
@@ -331,7 +337,7 @@ __global__ void __launch_bounds__(f8d::kThreads, 1) tc_decode_f8_kernel(const __
     }
   } else if (warp == 13) {
     // ================================ MMA issuer ================================
-    const uint32_t fmt = tp.f16 ? 0u : 1u;
+    const uint32_t fmt = kF16 ? 0u : 1u;
     const uint32_t idS = ptx::idesc_f16(fmt, 128, kN, 0, 0);  // A = K (TMEM), B = Q (K-major)
     const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(f8d::kThreads, 1) tc_decode_f8_kernel(const __
 #pragma unroll
           for (int c = 0; c < kC; ++c) {
             const uint32_t off = (c >> 3) * 1024 + (c & 7) * 128 + ((((tt >> 3) ^ (c & 7)) << 4) | ((tt & 7) << 1));
-            if (tp.f16) *reinterpret_cast<__half*>(pa + off) = __float2half_rn(pr[c]);
+            if constexpr (kF16) *reinterpret_cast<__half*>(pa + off) = __float2half_rn(pr[c]);
             else *reinterpret_cast<__nv_bfloat16*>(pa + off) = __float2bfloat16_rn(pr[c]);
           }
         };
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(f8d::kThreads, 1) tc_decode_f8_kernel(const __
           if (d.slot < 0) {
             const int64_t orow = (d.qo_begin + tok) * p.H_qo + head;
             if (p.o_f32) reinterpret_cast<float*>(p.o)[orow * 128 + drow] = val;
-            else if (tp.f16) reinterpret_cast<__half*>(p.o)[orow * 128 + drow] = __float2half_rn(val);
+            else if constexpr (kF16) reinterpret_cast<__half*>(p.o)[orow * 128 + drow] = __float2half_rn(val);
             else reinterpret_cast<__nv_bfloat16*>(p.o)[orow * 128 + drow] = __float2bfloat16_rn(val);
             if (p.lse && row == 0) p.lse[orow] = lse;
           } else {
@@ -606,7 +612,7 @@ __global__ void __launch_bounds__(f8d::kThreads, 1) tc_decode_f8_kernel(const __
       }
       if (d.slot >= 0 && p.fused_merge) {
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
-        if (tp.f16) fused_contraction<__half, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
+        if constexpr (kF16) fused_contraction<__half, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
         else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
       }
       ptx::named_bar_sync(1, 128);
