@@ -108,7 +108,9 @@ __device__ __forceinline__ DecItem dec_item(const PlanView& pv, int it, int g) {
   return d;
 }
 
-template <int kC, int kMask>
+// kF16: fp16 q / o (else bf16) at compile time: one code path per instantiation (instruction
+// fetch stalls measured on the fp8 kernel when both were inlined)
+template <int kC, int kMask, bool kF16>
 __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
   using namespace dec;
   const AttnParams& p = tp.p;
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     // ================================ MMA issuer ================================
     // S^T(t) as soon as K(t) landed and the softmax has read the S^T buffer; PV(t-1) once P(t-1)
     // is written: the MMA issue latency stays off the softmax chain.
-    const uint32_t fmt = tp.f16 ? 0u : 1u;
+    const uint32_t fmt = kF16 ? 0u : 1u;
     const uint32_t idS = ptx::idesc_f16(fmt, 128, kN, 0, 0);  // A = K (K-major), B = Q (K-major)
     const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
 #pragma unroll
           for (int c = 0; c < kC; ++c) {
             const uint32_t off = (c >> 3) * 1024 + (c & 7) * 128 + ((((tt >> 3) ^ (c & 7)) << 4) | ((tt & 7) << 1));
-            if (tp.f16) *reinterpret_cast<__half*>(pa + off) = __float2half_rn(pr[c]);
+            if constexpr (kF16) *reinterpret_cast<__half*>(pa + off) = __float2half_rn(pr[c]);
             else *reinterpret_cast<__nv_bfloat16*>(pa + off) = __float2bfloat16_rn(pr[c]);
           }
         };
@@ -482,7 +484,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           if (d.slot < 0) {
             const int64_t orow = (d.qo_begin + tok) * p.H_qo + head;
             if (p.o_f32) reinterpret_cast<float*>(p.o)[orow * 128 + row] = val;
-            else if (tp.f16) reinterpret_cast<__half*>(p.o)[orow * 128 + row] = __float2half_rn(val);
+            else if constexpr (kF16) reinterpret_cast<__half*>(p.o)[orow * 128 + row] = __float2half_rn(val);
             else reinterpret_cast<__nv_bfloat16*>(p.o)[orow * 128 + row] = __float2bfloat16_rn(val);
             if (p.lse && row == 0) p.lse[orow] = lse;
           } else {
@@ -494,7 +496,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       }
       if (d.slot >= 0 && p.fused_merge) {  // split item: the CTA completing its merge list folds it
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
-        if (tp.f16) fused_contraction<__half, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
+        if constexpr (kF16) fused_contraction<__half, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
         else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
       }
       ptx::named_bar_sync(1, 128);  // red2 reuse; TMEM reads done before the next item's MMAs

@@ -67,7 +67,6 @@ template <int kC, int kMask, bool kF8>
 cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
   static bool attr = false;
   if constexpr (kF8) {  // fp8 KV cache: K in TMEM, converter warps (tc_decode_f8.cuh)
-    static bool attr16 = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(tc_decode_f8_kernel<kC, kMask, false>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, f8d::kSmemBytes);
@@ -75,18 +74,22 @@ cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
       e = cudaFuncSetAttribute(tc_decode_f8_kernel<kC, kMask, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                f8d::kSmemBytes);
       if (e != cudaSuccess) return e;
-      attr = attr16 = true;
+      attr = true;
     }
     if (tp.f16) return launch_tc(tc_decode_f8_kernel<kC, kMask, true>, grid, f8d::kThreads, f8d::kSmemBytes, st, tp);
     return launch_tc(tc_decode_f8_kernel<kC, kMask, false>, grid, f8d::kThreads, f8d::kSmemBytes, st, tp);
   } else {
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         dec::kSmemBytes);
+    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dec::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_tc(tc_decode_kernel<kC, kMask>, grid, dec::kThreads, dec::kSmemBytes, st, tp);
+  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true>, grid, dec::kThreads, dec::kSmemBytes, st, tp);
+  return launch_tc(tc_decode_kernel<kC, kMask, false>, grid, dec::kThreads, dec::kSmemBytes, st, tp);
   }
 }
 
