@@ -14,6 +14,10 @@
 //               (the sparse gather of §3.2.1, done by TMA). Runs ahead across items
 //               through a kStages-deep smem ring.
 //   warps 1..4  128 threads: thread = TMEM lane = token (softmax) = head-dim row d (output).
+//   warps 6..9  epilogue: O^T is double-buffered in TMEM (cols 32 / 48 by item parity); the
+//               softmax warps hand each finished item over (row-sum partials + running max in
+//               smem) and go on with the next one while these warps normalise and store o / lse
+//               (and run the fused contraction for split items).
 //   warp 5      MMA issuer: S^T(t) as soon as K(t) landed and the S^T buffer was read, PV(t-1)
 //               once P(t-1) is written (s_free / p_full / o_free barriers), so the ~35-cycle
 //               per-instruction MMA issue stays off the softmax chain. Online softmax in the log2 domain with
@@ -78,9 +82,10 @@ constexpr int kOffQ = kStages * kStageBytes;
 constexpr int kOffP = kOffQ + 2 * kQBytes;   // two P^T buffers
 constexpr int kOffBar = kOffP + 2 * kPBytes;
 constexpr int kOffRed = kOffBar + 256;
-constexpr int kSmemBytes = kOffRed + 2 * 4 * kN * 4 + 64 + 1024;  // red, red2, vote flags + alignment slack
-constexpr int kThreads = 192;  // producer, 4 softmax warps, MMA warp
-constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T at col 32
+// red [4][kN], vote flags [2][4], epilogue hand-off sums [2][4][kN] and max [2][kN]; + alignment slack
+constexpr int kSmemBytes = kOffRed + 1024 + 1024;
+constexpr int kThreads = 320;  // producer, 4 softmax warps, MMA warp, 4 epilogue warps
+constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T double buffer at 32 / 48
 constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
 }  // namespace dec
 
@@ -125,10 +130,14 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   uint64_t* bar_pv = bar_s + 2;          // [2] PV MMA reading P^T buffer b done
   uint64_t* s_free = bar_pv + 2;         // [2] softmax read S^T buffer b (4 warp arrivals)
   uint64_t* p_full = s_free + 2;         // [2] P^T buffer b written (1 arrival)
-  uint64_t* o_free = p_full + 2;         // [1] epilogue read O^T (1 arrival)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 1);
+  uint64_t* o_free = p_full + 2;         // [2] epilogue read O^T buffer b (1 arrival)
+  uint64_t* epi_full = o_free + 2;       // [2] item's row sums / max handed to the epilogue (4 warps)
+  uint64_t* epi_empty = epi_full + 2;    // [2] epilogue consumed hand-off buffer b (1 arrival)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_empty + 2);
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [4 warps][kN]
-  float* red2 = red + 4 * kN;
+  int* vflags = reinterpret_cast<int*>(red + 4 * kN);     // [2][4] vote flags
+  float* hsum = reinterpret_cast<float*>(vflags + 8);      // [2][4 warps][kN] row-sum partials
+  float* hmax = hsum + 2 * 4 * kN;                          // [2][kN] running max
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const PlanView pv = load_plan(p.plan);
@@ -148,7 +157,11 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       ptx::mbar_init(&s_free[b], 4);
       ptx::mbar_init(&p_full[b], 1);
     }
-    ptx::mbar_init(o_free, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&o_free[b], 1);
+      ptx::mbar_init(&epi_full[b], 4);
+      ptx::mbar_init(&epi_empty[b], 1);
+    }
     ptx::fence_barrier_init();
   }
   if (warp >= 1 && warp <= 4) {  // zero both P^T buffers once: rows >= kC stay zero for the kernel's lifetime
@@ -234,8 +247,9 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     const uint32_t idS = ptx::idesc_f16(fmt, 128, kN, 0, 0);  // A = K (K-major), B = Q (K-major)
     const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
     const uint32_t sbase = ptx::smem_u32(smem);
-    int stage = 0, sb = 0, pb = 0, qb = 0;
-    uint32_t fphase = 0, ofph = 1;
+    int stage = 0, sb = 0, pb = 0, qb = 0, ob = 0;
+    uint32_t fphase = 0;
+    uint32_t ofph[2] = {1, 1};
     uint32_t sfph[2] = {1, 1}, pfph[2] = {0, 0}, qphase[2] = {0, 0};
     auto issue_pv = [&](int ti, int st) {  // PV of the item's tile ti, staged in ring stage st
       ptx::mbar_wait(&p_full[pb], pfph[pb]);
@@ -246,7 +260,8 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t sbo = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
-        ptx::mma_f16_ss_warp(tmem + 32, a0 + (uint64_t)(kk * 128), b0 + sbo, idO, (ti > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_f16_ss_warp(tmem + 32 + ob * 16, a0 + (uint64_t)(kk * 128), b0 + sbo, idO,
+                             (ti > 0 || kk > 0) ? 1u : 0u);
       }
       ptx::mma_commit_warp(&empty[st]);  // K/V stage free once these MMAs complete
       ptx::mma_commit_warp(&bar_pv[pb]);
@@ -278,9 +293,9 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         ptx::mma_commit_warp(&bar_s[sb]);
         if (ti + 1 == d.ntiles) ptx::mma_commit_warp(&empty_q[qb]);  // last reader of this Q buffer
         sb ^= 1;
-        if (ti == 0) {  // the item's first PV overwrites O: the previous epilogue must have read it
-          ptx::mbar_wait(o_free, ofph);
-          ofph ^= 1;
+        if (ti == 0) {  // the item's first PV overwrites O[ob]: the epilogue two items back read it
+          ptx::mbar_wait(&o_free[ob], ofph[ob]);
+          ofph[ob] ^= 1;
         } else {
           issue_pv(ti - 1, pstage);
         }
@@ -292,14 +307,16 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       }
       issue_pv(d.ntiles - 1, pstage);
       qb ^= 1;
+      ob ^= 1;
     }
-  } else {
-    // ===================== softmax / epilogue warps (1..4) =====================
+  } else if (warp <= 4) {
+    // ============================ softmax warps (1..4) ============================
     const int ct = threadIdx.x - 32;         // 0..127
     const int q4 = warp & 3;                 // TMEM lane quarter this warp may access
     const int row = q4 * 32 + lane;          // TMEM lane: token (softmax) / head-dim d (output)
     const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
-    const uint32_t tO = tmem + lane_addr + 32;
+    int ob = 0;                              // O^T buffer of the current item (32 / 48)
+    uint32_t eeph[2] = {1, 1};               // epi_empty parities (fresh: first waits pass)
     // pipeline state (identical in every softmax thread)
     int stage = 0;            // ring stage of the tile being processed
     uint32_t fphase = 0;      // its full-barrier parity
@@ -318,6 +335,8 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
 
     for (int it = it0; it < it1; ++it) {
       const DecItem d = dec_item(pv, it, g);
+      if (d.ntiles == 0) continue;  // empty item: the epilogue warps write the empty state
+      const uint32_t tO = tmem + lane_addr + 32 + ob * 16;
       float m[kC], lp[kC], aslope[kC];
       int64_t lim[kC];
 #pragma unroll
@@ -374,7 +393,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
 #pragma unroll
         for (int c = 0; c < kC; ++c) over |= s[c] > m[c] + kRescaleThresh;
         over = __any_sync(0xffffffffu, over);
-        int* flags = reinterpret_cast<int*>(red2 + 4 * kN) + (tpar & 1) * 4;
+        int* flags = vflags + (tpar & 1) * 4;
         if (lane == 0) flags[q4] = over ? 1 : 0;
         float pr[kC];
 #pragma unroll
@@ -453,32 +472,75 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         }
       }
       wait_pv(0);
-      wait_pv(1);
-      pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
-      // ---- epilogue: denominators (sum over the 128 token lanes), normalise, write
-      float ov[kC];
-      if (d.ntiles > 0) {
-        ptx::tc_fence_after();
-        ptx::tmem_ld<kC>(tO, ov);
-        ptx::tmem_ld_wait();
-      }
+      wait_pv(1);  // every PV of the item completed: O[ob] is final
+      // ---- hand the item to the epilogue warps: per-warp row-sum partials and the running max
+      float x[kC];
 #pragma unroll
       for (int c = 0; c < kC; ++c) {
-        float x = lp[c];
+        x[c] = lp[c];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane == 0) red2[q4 * kN + c] = x;
+        for (int o = 16; o > 0; o >>= 1) x[c] += __shfl_xor_sync(0xffffffffu, x[c], o);
+      }
+      ptx::mbar_wait(&epi_empty[ob], eeph[ob]);
+      eeph[ob] ^= 1;
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < kC; ++c) hsum[(ob * 4 + q4) * kN + c] = x[c];
+        if (q4 == 0) {
+#pragma unroll
+          for (int c = 0; c < kC; ++c) hmax[ob * kN + c] = m[c];
+        }
       }
       ptx::tc_fence_before();
-      ptx::named_bar_sync(1, 128);
-      if (ct == 0 && d.ntiles > 0) ptx::mbar_arrive(o_free);  // O^T read: the next item's PV may overwrite it
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&epi_full[ob]);
+      ob ^= 1;
+    }
+  } else {
+    // ====== epilogue warps (6..9): thread = TMEM lane = head-dim row d of O^T; normalise, write ======
+    const int et = threadIdx.x - 192;        // 0..127
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
+    int ob = 0;
+    uint32_t efph[2] = {0, 0};
+    pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
+    for (int it = it0; it < it1; ++it) {
+      const DecItem d = dec_item(pv, it, g);
+      float ov[kC], l[kC], mm[kC];
+      if (d.ntiles > 0) {
+        ptx::mbar_wait(&epi_full[ob], efph[ob]);
+        efph[ob] ^= 1;
+        ptx::tc_fence_after();
+        ptx::tmem_ld<kC>(tmem + lane_addr + 32 + ob * 16, ov);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < kC; ++c) {
+          const float* hs = hsum + ob * 4 * kN + c;
+          l[c] = (hs[0] + hs[kN]) + (hs[2 * kN] + hs[3 * kN]);
+          mm[c] = hmax[ob * kN + c];
+        }
+        ptx::tc_fence_before();
+        ptx::named_bar_sync(2, 128);  // all lanes of O[ob] and the hand-off buffer read
+        if (et == 0) {
+          ptx::mbar_arrive(&o_free[ob]);     // the item two ahead may overwrite O[ob]
+          ptx::mbar_arrive(&epi_empty[ob]);  // and the softmax may refill the hand-off buffer
+        }
+        ob ^= 1;
+      } else {
+#pragma unroll
+        for (int c = 0; c < kC; ++c) {
+          ov[c] = 0.f;
+          l[c] = 0.f;
+          mm[c] = -INFINITY;
+        }
+      }
 #pragma unroll
       for (int c = 0; c < kC; ++c) {
         if (c < d.nrows) {
-          const float l = (red2[c] + red2[kN + c]) + (red2[2 * kN + c] + red2[3 * kN + c]);
-          const bool empty_row = !(l > 0.f);
-          const float val = empty_row ? 0.f : ov[c] / l;
-          const float lse = empty_row ? -INFINITY : (m[c] + __log2f(l)) * kLn2;
+          const bool empty_row = !(l[c] > 0.f);
+          const float val = empty_row ? 0.f : ov[c] / l[c];
+          const float lse = empty_row ? -INFINITY : (mm[c] + __log2f(l[c])) * kLn2;
           const int f = d.row0 + c;
           const int tok = f / g, head = d.kvh * g + f % g;
           if (d.slot < 0) {
@@ -496,10 +558,9 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       }
       if (d.slot >= 0 && p.fused_merge) {  // split item: the CTA completing its merge list folds it
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
-        if constexpr (kF16) fused_contraction<__half, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
-        else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, ct, 128, 1, s_flag);
+        if constexpr (kF16) fused_contraction<__half, 128>(p, pv, d.slot, et, 128, 2, s_flag);
+        else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, et, 128, 2, s_flag);
       }
-      ptx::named_bar_sync(1, 128);  // red2 reuse; TMEM reads done before the next item's MMAs
     }
   }
   ptx::tc_fence_before();
