@@ -1,0 +1,11 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.max.mem --format=csv
+timeout -s KILL 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -4
+timeout -s KILL 900 python bench.py > gpurun_out/bench_r01s4.json 2> gpurun_out/bench_r01s4.err; head -c 300 gpurun_out/bench_r01s4.json
+timeout -s KILL 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_r01s4.json 2>/dev/null; head -c 200 gpurun_out/bench_ref_r01s4.json
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 200 --csv --log-file gpurun_out/ncu_launches_r01s4.csv python bench.py --steps 2 --warmup 3 --layers 4 --no-cpu-baseline --no-e2e --no-graph --no-composable --no-long --no-contiguous > /dev/null 2>&1
+mkdir -p /tmp/reps
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:tc_decode_kernel -s 4 -c 1 -o /tmp/reps/dec python bench.py --steps 1 --warmup 3 --layers 2 --no-cpu-baseline --no-e2e --no-graph --no-prefill --no-composable --no-long --no-contiguous --no-fp8 > /dev/null 2>&1
+python scripts/ncu_summary.py /tmp/reps/dec.ncu-rep 623602436 > gpurun_out/ncu_tc_decode_r01s4.txt 2>&1
+cat gpurun_out/ncu_tc_decode_r01s4.txt | head -12
