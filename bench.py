@@ -435,8 +435,11 @@ def bench_long_context(dev, pk, world, rank, local, layers=2, reps=10):
                         full.qo_lens.copy(), np.full(full.batch, shard_len, np.int32))
     Ls = [synth.make_inputs(wl, device=dev, seed_base=1000 * rank + 100 * r) for r in range(layers)]
     nq = wl.batch
+    # few long rows: plan with the queue count of smallest Algorithm-1 makespan (148 CTAs would cut
+    # each 512K row into 4.6 chunks; scripts/long_ctx_ctas.py)
     cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
-                           o_dtype="f32", max_batch=wl.batch, max_total_qo_rows=nq, num_ctas=148, tile_q=16)
+                           o_dtype="f32", max_batch=wl.batch, max_total_qo_rows=nq, num_ctas=148, tile_q=16,
+                           balance_ctas=True)
     eng = bsra.Engine(cfg, local)
     i0 = Ls[0]
     eng.plan(i0.qo_indptr, i0.kv_page_indptr, i0.kv_last_page_len, i0.sm_scale)

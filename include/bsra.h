@@ -114,6 +114,14 @@ typedef struct {
  * bsra_plan_ragged and run with bsra_run_ragged, and requires page_size = 128 (the KV tile and
  * the default chunk alignment). */
 #define BSRA_FLAG_RAGGED_KV 2
+/* flags: BSRA_FLAG_BALANCE_CTAS makes bsra_plan run Algorithm 1 for every queue count c in
+ * [num_ctas - num_ctas/8, num_ctas] and keep the plan with the smallest makespan under the
+ * Algorithm-1 cost model (ties: larger c). The grid stays num_ctas (graphs stay valid): queues
+ * c..num_ctas-1 are empty and those CTAs exit at once. With few long rows, L = ceil(sum/#CTA)
+ * can leave a ragged last chunk per row (configs[4]: 4.6 chunks per row at 148 CTAs, makespan
+ * 1.25x the mean; 144 queues give exactly 4.0). Costs ~c Algorithm-1 runs of host time per
+ * plan, so it is off by default. */
+#define BSRA_FLAG_BALANCE_CTAS 4
 
 typedef struct bsra_engine bsra_engine;
 

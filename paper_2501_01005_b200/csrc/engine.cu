@@ -71,7 +71,8 @@ bsra_status validate_config(const bsra_config& c) {
   if (c.cost_alpha < 0 || c.cost_beta < 0) return fail(BSRA_EINVAL, "negative cost parameters");
   if (c.kv_chunk_align < 0 || c.kv_chunk_min < 0) return fail(BSRA_EINVAL, "negative chunk parameters");
   if (c.kernel < BSRA_KERNEL_AUTO || c.kernel > BSRA_KERNEL_TC) return fail(BSRA_EINVAL, "bad kernel selector");
-  if (c.flags & ~(BSRA_FLAG_PDL | BSRA_FLAG_RAGGED_KV)) return fail(BSRA_EINVAL, "unknown flag bits");
+  if (c.flags & ~(BSRA_FLAG_PDL | BSRA_FLAG_RAGGED_KV | BSRA_FLAG_BALANCE_CTAS))
+    return fail(BSRA_EINVAL, "unknown flag bits");
   if ((c.flags & BSRA_FLAG_RAGGED_KV) && c.page_size != 128)
     return fail(BSRA_EINVAL, "BSRA_FLAG_RAGGED_KV engines take page_size = 128 (the KV tile)");
   if (c.sliding_window < 0) return fail(BSRA_EINVAL, "sliding_window < 0");
@@ -279,6 +280,30 @@ namespace {
 // fp8 KV with a prefill tile (T_q > 16) on the tcgen05 path: the plan is re-encoded with each
 // request's first row in the gathered 16-bit copy (f8_gather.cuh) and `page_begin` goes to the
 // aux section for the gather pass.
+// Makespan of a plan image under the Algorithm-1 cost model (alpha*T_q + beta*chunk per item).
+int64_t image_makespan(const std::vector<int32_t>& im, int64_t alpha, int64_t beta) {
+  const int nc = im[2], T_q = im[3], n_items = im[5];
+  const int32_t* ind = im.data() + bsra::kHeaderWords;
+  const int32_t* kb = ind + nc + 1 + 3 * n_items;
+  const int32_t* ke = kb + n_items;
+  int64_t mx = 0;
+  for (int c = 0; c < nc; ++c) {
+    int64_t s = 0;
+    for (int it = ind[c]; it < ind[c + 1]; ++it) s += alpha * T_q + beta * (int64_t)(ke[it] - kb[it]);
+    mx = std::max(mx, s);
+  }
+  return mx;
+}
+
+// Re-encodes an image planned with c queues for a grid of nc >= c CTAs: queues c..nc-1 empty.
+void pad_queues(std::vector<int32_t>& im, int32_t nc) {
+  const int32_t c = im[2];
+  if (c == nc) return;
+  const int32_t n_items = im[bsra::kHeaderWords + c];  // cta_indptr[c]
+  im[2] = nc;
+  im.insert(im.begin() + bsra::kHeaderWords + c + 1, (size_t)(nc - c), n_items);
+}
+
 bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* page_begin,
                       const std::vector<int32_t>& qo, const std::vector<int32_t>& kv, float sm_scale, void* stream) {
   const bsra_config& c = e->cfg;
@@ -287,8 +312,26 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
   if (rows > c.max_total_qo_rows) return fail(BSRA_EBOUNDS, "sum of qo lengths exceeds max_total_qo_rows");
   std::vector<int32_t> im;
   bsra::PlanSummary sum;
-  std::string err = bsra::build_plan(sched_params(c, c.num_ctas), qo, kv, qo_indptr, page_begin, im, sum);
+  int32_t queues = c.num_ctas;  // Algorithm 1's #CTA (BSRA_FLAG_BALANCE_CTAS may pick fewer)
+  std::string err = bsra::build_plan(sched_params(c, queues), qo, kv, qo_indptr, page_begin, im, sum);
   if (!err.empty()) return fail(BSRA_EINVAL, err);
+  if (c.flags & BSRA_FLAG_BALANCE_CTAS) {
+    const int64_t alpha = c.cost_alpha ? c.cost_alpha : 1, beta = c.cost_beta ? c.cost_beta : 1;
+    int64_t best = image_makespan(im, alpha, beta);
+    for (int32_t q = c.num_ctas - 1; q >= std::max(1, c.num_ctas - c.num_ctas / 8); --q) {
+      std::vector<int32_t> im2;
+      bsra::PlanSummary s2;
+      err = bsra::build_plan(sched_params(c, q), qo, kv, qo_indptr, page_begin, im2, s2);
+      if (!err.empty()) return fail(BSRA_EINVAL, err);
+      const int64_t mk = image_makespan(im2, alpha, beta);
+      if (mk < best) {
+        best = mk;
+        queues = q;
+        im.swap(im2);
+        sum = s2;
+      }
+    }
+  }
   const int32_t batch = (int32_t)qo.size();
   const int32_t g = c.num_qo_heads / c.num_kv_heads;
   const bool f8_prefill = kv_is_f8(c) && sum.T_q > 16 && c.kernel != BSRA_KERNEL_SIMT && c.head_dim == 128 &&
@@ -302,9 +345,10 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
       if (f8_rows > INT32_MAX) return fail(BSRA_EBOUNDS, "fp8 prefill: more than 2^31 KV tokens in one plan");
       kv_off[i + 1] = (int32_t)f8_rows;
     }
-    err = bsra::build_plan(sched_params(c, c.num_ctas), qo, kv, qo_indptr, kv_off.data(), im, sum);
+    err = bsra::build_plan(sched_params(c, queues), qo, kv, qo_indptr, kv_off.data(), im, sum);
     if (!err.empty()) return fail(BSRA_EINVAL, err);
   }
+  pad_queues(im, c.num_ctas);
   if (im.size() > e->lay.plan_words) return fail(BSRA_EBOUNDS, "plan image exceeds the workspace plan section");
   if (sum.T_q > e->lay.T_max) return fail(BSRA_EBOUNDS, "tile larger than the workspace partial slots");
   if (f8_prefill && f8_rows > e->f8_cap_rows) {  // engine-owned 16-bit copy (grows; see bsra.h)

@@ -146,3 +146,30 @@ def test_gpu_nccl_single_rank_equals_simulated(cuda_device):
     torch.cuda.synchronize()
     d.close()
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nc", [148, 37])
+def test_balance_ctas_flag(cuda_device, nc):
+    """BSRA_FLAG_BALANCE_CTAS: Algorithm 1 with the queue count c <= num_ctas of smallest makespan,
+    the grid unchanged (empty queues exit). Few long rows (configs[4]'s shape, shorter): the
+    makespan does not grow, and o / lse match the oracle and the unbalanced plan."""
+    import paper_2501_01005_b200 as bsra
+    from tests.helpers import assert_close, run_gpu
+    wl = synth.Workload("long_small", 32, 8, 128, 16, "bf16", "none", np.ones(4, np.int32),
+                        np.full(4, 18_500, np.int32))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    res = {}
+    for bal in (False, True):
+        cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
+                               max_batch=wl.batch, max_total_qo_rows=wl.batch, num_ctas=nc, tile_q=16,
+                               balance_ctas=bal)
+        eng = bsra.Engine(cfg, 0)
+        gpu = run_gpu(inp, eng)
+        costs, mk = eng.plan_stats()
+        assert len(costs) == nc  # the grid (and a captured graph) keep num_ctas CTAs
+        res[bal] = (gpu, mk, int((costs > 0).sum()))
+    assert res[True][1] <= res[False][1]
+    ref = oracle.attention_from_inputs(inp)
+    assert_close(res[True][0], ref, "bf16", what=f"balanced nc={nc}")
+    assert np.max(np.abs(res[True][0][0] - res[False][0][0])) < 1e-2
