@@ -274,3 +274,43 @@ def test_fp8_random_small_simt_d64(cuda_device, seed):
     wl = _fp8(synth.random_workload(rng, dtype=["bf16", "f16"][seed % 2], heads=((4, 1), (8, 2), (6, 3)),
                                     page_sizes=(1, 4, 16)))
     _case(cuda_device, wl, seed=seed, num_ctas=int(rng.integers(1, 40)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile_q", [16, 128])
+def test_fp8_graph_capture_and_replan(cuda_device, tile_q):
+    """run() with an E4M3 cache is graph-capturable (decode kernel; gather pass + prefill): a graph
+    captured once replays bitwise-equal to eager runs, also after a re-plan that does not grow the
+    gathered 16-bit buffer."""
+    import torch
+    wl = _dec(qo=[1, 3, 2, 1], kv=[300, 37, 900, 250]) if tile_q == 16 else _pre(qo=(70, 129, 1, 300),
+                                                                                  kv=(70, 200, 50, 300))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    eng = engine_for(wl, num_ctas=64, tile_q=tile_q)
+    nq = int(inp.qo_indptr[-1])
+    o = torch.zeros((nq, wl.H_qo, wl.D), device=cuda_device, dtype=torch.bfloat16)
+    lse = torch.zeros((nq, wl.H_qo), device=cuda_device)
+    eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+    eng.set_kv_scales(inp.k_scale, inp.v_scale)
+    mbi = None if inp.mask_bit_indptr is None else torch.from_numpy(inp.mask_bit_indptr).to(cuda_device)
+    run = lambda: eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse,
+                          custom_mask=inp.custom_mask, mask_bit_indptr=mbi)
+    run()
+    torch.cuda.synchronize()
+    eager = (o.clone(), lse.clone())
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        run()
+    torch.cuda.synchronize()
+    with torch.cuda.graph(g, stream=s):
+        run()
+    o.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o, eager[0]) and torch.equal(lse, eager[1])
+    eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)  # same lengths
+    o.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(o, eager[0]) and torch.equal(lse, eager[1])
