@@ -314,3 +314,17 @@ def test_fp8_graph_capture_and_replan(cuda_device, tile_q):
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(o, eager[0]) and torch.equal(lse, eager[1])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile_q", [16, 128])
+def test_fp8_with_balanced_queues(cuda_device, tile_q):
+    """BSRA_FLAG_BALANCE_CTAS with an E4M3 cache: padded plan images drive the fp8 decode kernel
+    and the gather + prefill path (re-encoded request table) unchanged."""
+    wl = _dec(qo=[1, 1, 1], kv=[5000, 4100, 3000]) if tile_q == 16 else _pre(qo=(300, 129), kv=(3000, 2200))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
+                           max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()), num_ctas=148, tile_q=tile_q,
+                           kv_dtype="e4m3", balance_ctas=True)
+    gpu = run_gpu(inp, bsra.Engine(cfg, 0))
+    assert_close(gpu, oracle.attention_from_inputs(inp), wl.dtype, what=f"fp8 balanced T_q={tile_q}")
