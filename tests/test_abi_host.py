@@ -137,3 +137,21 @@ def test_config_validation(kw, msg):
 def test_empty_request_without_pages_ignores_last_page_len():
     img = bsra.plan_host(_cfg(), 4, [0, 1, 2], [0, 0, 1], [999, 3])
     assert img[S.HEADER_WORDS - 16 + 5] == 2 * 2  # 2 requests x 2 kv heads, one item each
+
+
+def test_config_struct_layout_matches_header(tmp_path):
+    """The ctypes mirror of bsra_config (the binding) has the C header's size and field offsets:
+    compiled with gcc against include/bsra.h, compared field by field."""
+    import ctypes
+    import subprocess
+    fields = [f[0] for f in bsra.Config._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "bsra.h"\nint main(void) {\n'
+                   '  printf("%zu\\n", sizeof(bsra_config));\n'
+                   + "".join(f'  printf("%zu\\n", offsetof(bsra_config, {f}));\n' for f in fields) + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = [int(x) for x in subprocess.check_output([str(exe)]).split()]
+    assert out[0] == ctypes.sizeof(bsra.Config)
+    for f, off in zip(fields, out[1:]):
+        assert getattr(bsra.Config, f).offset == off, f
