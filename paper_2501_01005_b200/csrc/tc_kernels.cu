@@ -76,8 +76,8 @@ cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    if (tp.f16) return launch_tc(tc_decode_f8_kernel<kC, kMask, true>, grid, f8d::kThreads, f8d::kSmemBytes, st, tp);
-    return launch_tc(tc_decode_f8_kernel<kC, kMask, false>, grid, f8d::kThreads, f8d::kSmemBytes, st, tp);
+    if (tp.f16) return launch_tc(tc_decode_f8_kernel<kC, kMask, true>, grid, f8d::threads_for(kC), f8d::kSmemBytes, st, tp);
+    return launch_tc(tc_decode_f8_kernel<kC, kMask, false>, grid, f8d::threads_for(kC), f8d::kSmemBytes, st, tp);
   } else {
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false>,
