@@ -1,7 +1,7 @@
 # Build libbsra.so (sm_100a) and the C oracle. `python -c "import __graft_entry__ as g; g.build()"` runs this.
 NVCC    ?= /usr/local/cuda/bin/nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v $(if $(WATCHDOG),-DBSRA_WATCHDOG,)
+NVFLAGS := -O3 -lineinfo -std=c++17 $(ARCH) -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr -Xptxas -v $(if $(WATCHDOG),-DBSRA_WATCHDOG,) $(if $(EXPERIMENTS),-DBSRA_EXPERIMENTS,)
 PKG     := paper_2501_01005_b200
 SRC     := $(PKG)/csrc
 BUILD   := build

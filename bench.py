@@ -158,7 +158,8 @@ class Layered:
         if wl.kv_dtype:
             kw = dict(kw, kv_dtype=wl.kv_dtype, k_scale=self.inp0.k_scale, v_scale=self.inp0.v_scale)
         cfg = self.bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
-                                    mask=wl.mask, max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()), **kw)
+                                    mask=wl.mask, max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()),
+                                    max_total_kv_tokens=int(wl.kv_lens.astype(np.int64).sum()), **kw)
         return self.bsra.Engine(cfg, torch.cuda.current_device())
 
     def plan(self, eng, stream=None):

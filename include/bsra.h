@@ -88,10 +88,9 @@ typedef struct {
    * dequantisation scales (0 => 1), changeable per run with bsra_set_kv_scales. The kernels
    * dequantise exactly (every E4M3 value is exact in fp16 and bf16) and compute as for dtype.
    * Decode tiles (T_q = 16) dequantise inside the attention kernel. Prefill tiles (T_q >= 64)
-   * on the tcgen05 path first gather the plan's tokens into an ENGINE-OWNED 16-bit device buffer
-   * (one extra launch per run; 4 * sum(l_kv) * H_kv * head_dim bytes, allocated by bsra_plan and
-   * grown when a plan needs more — a CUDA graph captured before such a growing plan must be
-   * re-captured). */
+   * on the tcgen05 path first gather the plan's tokens into a 16-bit copy in the caller's
+   * WORKSPACE (one extra launch per run; 4 * max_total_kv_tokens * H_kv * head_dim bytes, sized
+   * by bsra_workspace_bytes — the library never allocates device memory). */
   int32_t kv_dtype;
   float k_scale;
   float v_scale;
@@ -99,7 +98,19 @@ typedef struct {
    * for query row r of qo head h gets + slope_h * (t - p), p = l_kv - l_qo + r, after the soft-cap;
    * slope_h = 2^(-8(h+1)/n) for h < n = 2^floor(log2 H_qo), else 2^(-4(2(h-n)+1)/n). 0 = off. */
   int32_t alibi;
-  int32_t reserved[3];       /* must be zero                                                    */
+  /* Bounds that fix launch choices independently of the plan, so one captured CUDA graph serves
+   * every re-plan within them (App. D.1, "fixed offsets ... compatible with CUDAGraphs"):
+   *   max_total_kv_tokens  bound on sum_i l_kv(i) (0 = none). Sizes the workspace region an E4M3
+   *                        engine with prefill tiles gathers its 16-bit K/V copy into (such a
+   *                        plan fails with EBOUNDS when it is 0 or exceeded), and is the token
+   *                        extent of a contiguous-KV engine's K/V tensor maps under capture.
+   *   max_qo_len           bound on any one request's l_qo (0 = none). When set, the decode
+   *                        kernel's live fused columns are min(16, max_qo_len * g) for every plan
+   *                        (plan() rejects a longer request with EBOUNDS); when 0 they follow each
+   *                        plan and capture tracking (bsra_run) guards graphs against growth. */
+  int32_t max_total_kv_tokens;
+  int32_t max_qo_len;
+  int32_t reserved[4];       /* must be zero                                                    */
 } bsra_config;
 
 /* flags: BSRA_FLAG_PDL launches the tcgen05 kernels with programmatic dependent launch: a run()
@@ -159,6 +170,13 @@ bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, c
 
 /* Executor: device pointers only; no allocation and no host synchronisation, so it is
  * CUDA-graph capturable. Uses the most recent plan of `e` in stream order.
+ * Graph capture: a run() enqueued on a capturing stream bakes the plan's launch choices (query
+ * tile T_q and kernel, the decode kernel's live columns, the fp8 gather pass, tensor-map extents)
+ * into the graph. The engine records them, and every later bsra_plan / bsra_plan_ragged whose
+ * plan a replay could not run correctly fails with BSRA_EBOUNDS and keeps the previous plan —
+ * until bsra_graph_release(e) says those graphs are gone. Under capture the q tensor map spans
+ * max_total_qo_rows rows, so the q buffer of a captured run must hold max_total_qo_rows rows
+ * (contiguous KV: k / v must hold max_total_kv_tokens rows when that bound is set).
  *   q                [sum l_qo, H_qo, D] device, contiguous, cfg->dtype
  *   k_pool, v_pool   device pools; element (page p, slot s, kv head h, dim d) lives at
  *                    p*strides[0] + s*strides[1] + h*strides[2] + d  (strides in ELEMENTS, host
@@ -176,6 +194,11 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
                      const int64_t* k_strides, const int64_t* v_strides, const int32_t* kv_page_indices,
                      const uint8_t* custom_mask, const int64_t* mask_bit_indptr, void* o, float* lse,
                      void* stream);
+
+/* Declares that every CUDA graph captured over run() calls of `e` has been destroyed (or will
+ * be re-captured): clears the launch choices recorded at capture, so the next plan may change
+ * them. Host only. Errors: EINVAL (NULL engine). */
+bsra_status bsra_graph_release(bsra_engine* e);
 
 /* Dequantisation scales of an fp8 KV cache for subsequent run() calls on `e` (e.g. per layer);
  * 0 => 1. A captured graph keeps the scales of the run() it captured. Host only.

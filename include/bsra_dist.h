@@ -43,6 +43,40 @@ bsra_status bsra_dist_allgather_merge(bsra_dist* d, const float* o_local, const 
                                       int32_t heads, int32_t head_dim, void* scratch, void* o_out,
                                       bsra_dtype out_dtype, float* lse_out, void* stream);
 
+/* Polls the communicator for an asynchronous NCCL failure (ncclCommGetAsyncError): BSRA_OK while
+ * healthy or in progress, BSRA_ENCCL (message in bsra_dist_last_error) once NCCL reports an
+ * error — e.g. a peer died or a network/NVLink fault. bsra_dist_allgather_merge polls it too. */
+bsra_status bsra_dist_check(bsra_dist* d);
+
+/* Sequence split of a BSR page table for long-context decode (BASELINE configs[4]; north_star
+ * "very long contexts split along the sequence"): rank r of P owns the contiguous logical page
+ * range [floor(r*n/P), floor((r+1)*n/P)) of every request, n = its page count. The shard is
+ * itself a BSR table over the SAME physical pool (page ids are copied, not renumbered); its
+ * last_page_len is the request's own on the rank that holds the request's final page and
+ * page_size elsewhere (a rank with no page of request i gets l_kv = 0 there). ⊕ of the ranks'
+ * states in rank order is the whole request's attention. Host only; no CUDA, no NCCL.
+ *   kv_page_indptr [batch+1], kv_page_indices [kv_page_indptr[batch]], kv_last_page_len [batch]:
+ *                  host int32, validated as in bsra_plan
+ *   out_indptr [batch+1], out_last [batch]: host int32; out_indices: host int32, cap entries
+ *                  (kv_page_indptr[batch] always suffices); may be NULL with cap = 0 to size it
+ *   out_nnz        pages in this rank's shard
+ * Errors: EINVAL (malformed table, rank not in [0, nranks)), ENOMEM (cap too small). */
+bsra_status bsra_dist_shard_bsr(int32_t nranks, int32_t rank, int32_t batch, int32_t page_size,
+                                const int32_t* kv_page_indptr, const int32_t* kv_page_indices,
+                                const int32_t* kv_last_page_len, int32_t* out_indptr, int32_t* out_indices,
+                                size_t cap, int32_t* out_last, int64_t* out_nnz);
+
+/* KV-head partition for batched decode / prefill (north_star "requests and KV
+ * heads sharded with no communication"): rank r of P owns kv heads [begin, end) with
+ * begin = floor(r*H_kv/P), end = floor((r+1)*H_kv/P), and with them qo heads [begin*g, end*g)
+ * (GQA groups never straddle ranks). Each rank runs its own engine with
+ * num_kv_heads = end - begin over pools holding only those heads (or the full pools offset by
+ * begin*head_dim elements with the full strides); its o is the head slice of the 1-GPU output,
+ * so no collective is needed (output stays head-sharded, like tensor-parallel attention).
+ * Host only. Errors: EINVAL (H_kv < 1, rank not in [0, nranks), NULL outputs). */
+bsra_status bsra_dist_head_shard(int32_t num_kv_heads, int32_t nranks, int32_t rank, int32_t* kv_head_begin,
+                                 int32_t* kv_head_end);
+
 /* Message of the last failing bsra_dist_* call on this thread (NCCL / dlopen errors). */
 const char* bsra_dist_last_error(void);
 

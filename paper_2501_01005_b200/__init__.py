@@ -39,7 +39,8 @@ class Config(ctypes.Structure):
                 ("kv_chunk_min", ctypes.c_int32), ("kernel", ctypes.c_int32), ("flags", ctypes.c_int32),
                 ("sliding_window", ctypes.c_int32), ("logits_soft_cap", ctypes.c_float),
                 ("kv_dtype", ctypes.c_int32), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float),
-                ("alibi", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3)]
+                ("alibi", ctypes.c_int32), ("max_total_kv_tokens", ctypes.c_int32), ("max_qo_len", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 4)]
 
 
 FLAG_PDL = 1  # BSRA_FLAG_PDL (include/bsra.h)
@@ -49,11 +50,12 @@ FLAG_BALANCE_CTAS = 4  # BSRA_FLAG_BALANCE_CTAS: plan with the queue count that 
 
 _lib = None
 EXPORTS = ["bsra_version", "bsra_num_sms", "bsra_workspace_bytes", "bsra_engine_create", "bsra_engine_destroy",
-           "bsra_plan", "bsra_run", "bsra_set_kv_scales", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
+           "bsra_plan", "bsra_run", "bsra_graph_release", "bsra_set_kv_scales", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
            "bsra_plan_host", "bsra_plan_export",
            "bsra_plan_stats", "bsra_last_run_launches", "bsra_selected_kernel", "bsra_last_error",
            "bsra_dist_unique_id", "bsra_dist_create", "bsra_dist_destroy", "bsra_dist_scratch_bytes",
-           "bsra_dist_allgather_merge", "bsra_dist_last_error"]
+           "bsra_dist_allgather_merge", "bsra_dist_check", "bsra_dist_shard_bsr", "bsra_dist_head_shard",
+           "bsra_dist_last_error"]
 
 
 def lib():
@@ -74,6 +76,7 @@ def lib():
             "bsra_plan": (I32, [P, I32, P, P, P, ctypes.c_float, P]),
             "bsra_run": (I32, [P, P, P, P, P, P, P, P, P, P, P, P]),
             "bsra_set_kv_scales": (I32, [P, ctypes.c_float, ctypes.c_float]),
+            "bsra_graph_release": (I32, [P]),
             "bsra_plan_ragged": (I32, [P, I32, P, P, ctypes.c_float, P]),
             "bsra_run_ragged": (I32, [P, P, P, P, P, P, P, P, P, P, P]),
             "bsra_merge_states": (I32, [P, P, P, P, I32, I64, I32, I32, P, I32, P, P]),
@@ -115,10 +118,13 @@ def _i32(a) -> np.ndarray:
 def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="none", max_batch=1,
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
                 kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False, window=0,
-                soft_cap=0.0, kv_dtype=None, k_scale=0.0, v_scale=0.0, alibi=False, balance_ctas=False) -> Config:
+                soft_cap=0.0, kv_dtype=None, k_scale=0.0, v_scale=0.0, alibi=False, balance_ctas=False,
+                max_total_kv_tokens=0, max_qo_len=0) -> Config:
     """window: sliding window W (0 = off, DESIGN.md R26); soft_cap: logits soft-cap c (0 = off, R27);
-    kv_dtype "e4m3": fp8 KV cache with per-tensor scales k_scale / v_scale (0 = 1; R28)."""
+    kv_dtype "e4m3": fp8 KV cache with per-tensor scales k_scale / v_scale (0 = 1; R28);
+    max_total_kv_tokens / max_qo_len: engine bounds (include/bsra.h)."""
     c = Config()
+    c.max_total_kv_tokens, c.max_qo_len = int(max_total_kv_tokens), int(max_qo_len)
     if kv_dtype:
         c.kv_dtype = DTYPE[kv_dtype] if isinstance(kv_dtype, str) else kv_dtype
     c.k_scale, c.v_scale = float(k_scale), float(v_scale)
@@ -203,6 +209,10 @@ class Engine:
                               ctypes.cast(vs, ctypes.c_void_p), _p(kv_page_indices), _p(custom_mask),
                               _p(mask_bit_indptr), _p(o), _p(lse), self._stream(stream)))
 
+    def graph_release(self):
+        """Every CUDA graph captured over this engine's run() calls is gone (bsra_graph_release)."""
+        _check(lib().bsra_graph_release(self._h))
+
     def set_kv_scales(self, k_scale: float, v_scale: float):
         """fp8 KV dequantisation scales for the following run() calls (0 = 1)."""
         _check(lib().bsra_set_kv_scales(self._h, float(k_scale), float(v_scale)))
@@ -269,24 +279,36 @@ def merge_many(o_parts, lse_parts, o_out, lse_out=None, stream=None):
 
 
 def sequence_shard(kv_page_indptr, kv_page_indices, kv_last_page_len, page_size, nranks, rank):
-    """Sequence split of a BSR page table for long-context decode (BASELINE configs[4]): rank r
-    owns the contiguous page range [r*n/P, (r+1)*n/P) of every request (n = its page count). The
-    last page length is the request's own only on the rank holding its final page. Host-only
-    index arithmetic; returns (kv_page_indptr, kv_page_indices, kv_last_page_len) of the shard."""
-    kp = np.asarray(kv_page_indptr, np.int64)
-    idx = np.asarray(kv_page_indices)
-    last = np.asarray(kv_last_page_len, np.int32)
-    indptr = [0]
-    sel = []
-    lasts = []
-    for i in range(len(kp) - 1):
-        n = int(kp[i + 1] - kp[i])
-        a, b = (rank * n) // nranks, ((rank + 1) * n) // nranks
-        sel.append(idx[kp[i] + a:kp[i] + b])
-        indptr.append(indptr[-1] + (b - a))
-        lasts.append(int(last[i]) if (b == n and b > a) else page_size)
-    ind = np.concatenate(sel).astype(np.int32) if sel else np.zeros(0, np.int32)
-    return np.array(indptr, np.int32), ind, np.array(lasts, np.int32)
+    """Sequence split of a BSR page table for long-context decode (BASELINE configs[4]): the
+    shard rank `rank` of `nranks` owns (bsra_dist_shard_bsr, include/bsra_dist.h). Marshalling
+    only; returns (kv_page_indptr, kv_page_indices, kv_last_page_len) of the shard."""
+    kp, idx, last = _i32(kv_page_indptr), _i32(kv_page_indices), _i32(kv_last_page_len)
+    B = len(kp) - 1
+    L = lib()
+    P = ctypes.c_void_p
+    L.bsra_dist_shard_bsr.restype = ctypes.c_int32
+    L.bsra_dist_shard_bsr.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, P, P, P, P,
+                                      ctypes.c_size_t, P, ctypes.POINTER(ctypes.c_int64)]
+    out_ip = np.zeros(B + 1, np.int32)
+    out_last = np.zeros(max(B, 0), np.int32)
+    out_idx = np.zeros(max(1, idx.size), np.int32)
+    nnz = ctypes.c_int64()
+    rc = L.bsra_dist_shard_bsr(nranks, rank, B, page_size, _p(kp), _p(idx), _p(last), _p(out_ip), _p(out_idx),
+                               out_idx.size, _p(out_last), ctypes.byref(nnz))
+    if rc:
+        raise BsraError(f"bsra_dist_shard_bsr: {rc}: {Dist.last_error()}")
+    return out_ip, out_idx[:nnz.value].copy(), out_last
+
+
+def head_shard(num_kv_heads: int, nranks: int, rank: int):
+    """KV heads [begin, end) rank `rank` of `nranks` owns (bsra_dist_head_shard)."""
+    L = lib()
+    L.bsra_dist_head_shard.restype = ctypes.c_int32
+    b, e = ctypes.c_int32(), ctypes.c_int32()
+    rc = L.bsra_dist_head_shard(num_kv_heads, nranks, rank, ctypes.byref(b), ctypes.byref(e))
+    if rc:
+        raise BsraError(f"bsra_dist_head_shard: {rc}: {Dist.last_error()}")
+    return b.value, e.value
 
 
 class Dist:
@@ -338,6 +360,14 @@ class Dist:
         if rc:
             raise BsraError(f"bsra_dist_allgather_merge: {rc}: {Dist.last_error()} {L.bsra_last_error().decode()}")
         return o_out, lse_out
+
+    def check(self):
+        """Raise if NCCL reported an asynchronous error on this communicator (bsra_dist_check)."""
+        L = lib()
+        L.bsra_dist_check.argtypes = [ctypes.c_void_p]
+        rc = L.bsra_dist_check(self._h)
+        if rc:
+            raise BsraError(f"bsra_dist_check: {rc}: {Dist.last_error()}")
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:

@@ -135,6 +135,8 @@ bsra_status bsra_dist_allgather_merge(bsra_dist* d, const float* o_local, const 
   const size_t cnt = (size_t)rows * heads;
   float* go = static_cast<float*>(scratch);
   float* gl = reinterpret_cast<float*>(static_cast<uint8_t*>(scratch) + align256((size_t)d->nranks * cnt * head_dim * 4));
+  bsra_status hs = bsra_dist_check(d);  // a communicator with a pending async error cannot be used
+  if (hs) return hs;
   ncclResult_t r = n->GroupStart();
   if (!r) r = n->AllGather(o_local, go, cnt * head_dim, kNcclFloat32, d->comm, st);
   if (!r) r = n->AllGather(lse_local, gl, cnt, kNcclFloat32, d->comm, st);
@@ -143,4 +145,78 @@ bsra_status bsra_dist_allgather_merge(bsra_dist* d, const float* o_local, const 
   if (r2) return nccl_fail(r2, "ncclGroupEnd");
   // ⊕ in rank order (identical on every rank): bsra_merge_many over [P, rows, heads, D]
   return bsra_merge_many(go, gl, d->nranks, rows, heads, head_dim, o_out, out_dtype, lse_out, stream);
+}
+
+bsra_status bsra_dist_check(bsra_dist* d) {
+  if (!d) return BSRA_EINVAL;
+  Nccl* n = nccl();
+  if (!n) return BSRA_ENCCL;
+  if (!n->CommGetAsyncError) return BSRA_OK;  // very old NCCL: nothing to poll
+  ncclResult_t async = 0;
+  ncclResult_t r = n->CommGetAsyncError(d->comm, &async);
+  if (r) return nccl_fail(r, "ncclCommGetAsyncError");
+  constexpr ncclResult_t kInProgress = 7;  // ncclInProgress (non-blocking communicators)
+  if (async != 0 && async != kInProgress) return nccl_fail(async, "NCCL asynchronous error");
+  return BSRA_OK;
+}
+
+bsra_status bsra_dist_shard_bsr(int32_t nranks, int32_t rank, int32_t batch, int32_t page_size,
+                                const int32_t* kv_page_indptr, const int32_t* kv_page_indices,
+                                const int32_t* kv_last_page_len, int32_t* out_indptr, int32_t* out_indices,
+                                size_t cap, int32_t* out_last, int64_t* out_nnz) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || batch < 0 || page_size < 1 || !out_nnz) {
+    g_dist_err = "bad nranks / rank / batch / page_size";
+    return BSRA_EINVAL;
+  }
+  if (batch > 0 && (!kv_page_indptr || !kv_last_page_len || !out_indptr || !out_last)) {
+    g_dist_err = "NULL array";
+    return BSRA_EINVAL;
+  }
+  if (batch > 0 && kv_page_indptr[0] != 0) {
+    g_dist_err = "kv_page_indptr[0] != 0";
+    return BSRA_EINVAL;
+  }
+  int64_t nnz = 0;
+  for (int32_t i = 0; i < batch; ++i) {  // validate and size
+    const int64_t n = (int64_t)kv_page_indptr[i + 1] - kv_page_indptr[i];
+    if (n < 0 || (n > 0 && (kv_last_page_len[i] < 1 || kv_last_page_len[i] > page_size))) {
+      g_dist_err = "malformed BSR table at request " + std::to_string(i);
+      return BSRA_EINVAL;
+    }
+    nnz += (rank + 1) * n / nranks - rank * n / nranks;
+  }
+  *out_nnz = nnz;
+  if (!out_indices && cap == 0) {  // sizing call
+    if (batch > 0) out_indptr[0] = 0;
+    return BSRA_OK;
+  }
+  if ((int64_t)cap < nnz || (nnz > 0 && !out_indices)) {
+    g_dist_err = "out_indices capacity too small";
+    return BSRA_ENOMEM;
+  }
+  if (nnz > 0 && !kv_page_indices) {
+    g_dist_err = "NULL kv_page_indices";
+    return BSRA_EINVAL;
+  }
+  int64_t w = 0;
+  if (batch > 0) out_indptr[0] = 0;
+  for (int32_t i = 0; i < batch; ++i) {
+    const int64_t n = (int64_t)kv_page_indptr[i + 1] - kv_page_indptr[i];
+    const int64_t a = rank * n / nranks, b = (rank + 1) * n / nranks;
+    for (int64_t j = a; j < b; ++j) out_indices[w++] = kv_page_indices[kv_page_indptr[i] + j];
+    out_indptr[i + 1] = (int32_t)w;
+    out_last[i] = (b == n && b > a) ? kv_last_page_len[i] : page_size;
+  }
+  return BSRA_OK;
+}
+
+bsra_status bsra_dist_head_shard(int32_t num_kv_heads, int32_t nranks, int32_t rank, int32_t* kv_head_begin,
+                                 int32_t* kv_head_end) {
+  if (num_kv_heads < 1 || nranks < 1 || rank < 0 || rank >= nranks || !kv_head_begin || !kv_head_end) {
+    g_dist_err = "bad num_kv_heads / nranks / rank, or NULL output";
+    return BSRA_EINVAL;
+  }
+  *kv_head_begin = (int32_t)((int64_t)rank * num_kv_heads / nranks);
+  *kv_head_end = (int32_t)((int64_t)(rank + 1) * num_kv_heads / nranks);
+  return BSRA_OK;
 }

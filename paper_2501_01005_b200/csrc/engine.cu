@@ -48,8 +48,9 @@ bsra_dtype kv_dtype_of(const bsra_config& c) { return kv_is_f8(c) ? BSRA_E4M3 : 
 struct Layout {
   int32_t num_ctas = 0, T_max = 0, T_min = 0;
   size_t plan_words = 0;
-  size_t off_plan = 0, off_part_o = 0, off_part_lse = 0, off_counters = 0, off_aux = 0, total = 0;
+  size_t off_plan = 0, off_part_o = 0, off_part_lse = 0, off_counters = 0, off_aux = 0, off_f8 = 0, total = 0;
   size_t aux_words = 0;  // fp8 prefill gather: src_begin[max_batch+1], kv_off[max_batch+1]
+  int64_t f8_rows = 0;   // fp8 prefill gather region: max_total_kv_tokens rows of [H_kv, 128] K and V
 };
 
 int tile_mask_of(const bsra_config& c) { return c.tile_set_mask ? c.tile_set_mask : 15; }
@@ -84,7 +85,8 @@ bsra_status validate_config(const bsra_config& c) {
   if (!(c.k_scale >= 0.f) || !std::isfinite(c.k_scale) || !(c.v_scale >= 0.f) || !std::isfinite(c.v_scale))
     return fail(BSRA_EINVAL, "k_scale / v_scale must be finite and >= 0");
   if (c.alibi != 0 && c.alibi != 1) return fail(BSRA_EINVAL, "alibi must be 0 or 1");
-  for (int i = 0; i < 3; ++i)
+  if (c.max_total_kv_tokens < 0 || c.max_qo_len < 0) return fail(BSRA_EINVAL, "negative bounds");
+  for (int i = 0; i < 4; ++i)
     if (c.reserved[i]) return fail(BSRA_EINVAL, "reserved fields must be zero");
   return BSRA_OK;
 }
@@ -118,6 +120,12 @@ Layout make_layout(const bsra_config& c, int32_t num_ctas) {
   L.off_aux = off;
   L.aux_words = 2 * ((size_t)c.max_batch + 1);
   off = align_up(off + L.aux_words * 4, 256);
+  // fp8 KV with prefill tiles on the tcgen05 path: the 16-bit gather region (f8_gather.cuh),
+  // caller-owned like the rest of the workspace (§8(b) ownership; never cudaMalloc'd by plan)
+  L.off_f8 = off;
+  if (kv_is_f8(c) && L.T_max > 16 && c.head_dim == 128 && c.kernel != BSRA_KERNEL_SIMT)
+    L.f8_rows = c.max_total_kv_tokens;
+  off = align_up(off + (size_t)L.f8_rows * c.num_kv_heads * 128 * 2 * sizeof(uint16_t), 256);
   L.total = off;
   return L;
 }
@@ -129,9 +137,19 @@ bsra_status query_sms(int32_t device, int32_t* sms) {
 
 }  // namespace
 
+// Launch choices a captured CUDA graph bakes in (bsra.h, bsra_run: graph capture)
+struct LaunchSig {
+  int32_t T_q = 0;
+  int32_t kc = 0;           // decode kernel's live fused columns (4 / 8 / 16)
+  bool f8_prefill = false;  // fp8 gather pass + 16-bit prefill kernel
+  int64_t q_extent = 0;     // rows of the q tensor map
+  int64_t kv_extent = 0;    // contiguous-KV token extent of the K/V maps
+};
+
 struct bsra_engine {
   bsra_config cfg;
   int32_t device = 0;
+  int32_t sms = 148;  // SM count of `device` (grid sizes of the helper kernels)
   Layout lay;
   uint8_t* ws = nullptr;
   int32_t* staging = nullptr;  // pinned host buffer (App. D)
@@ -145,13 +163,15 @@ struct bsra_engine {
   int64_t total_qo = 0;
   int64_t total_kv = 0;  // ragged KV: token extent of k / v (kv_indptr[batch])
   int32_t max_qo = 0;
+  int32_t kc = 16;  // decode kernel's live fused columns for the current plan
   float k_scale = 1.f, v_scale = 1.f;  // fp8 KV dequantisation scales (bsra_set_kv_scales)
   // fp8 KV with prefill tiles (f8_gather.cuh): the current plan addresses a 16-bit gathered copy
+  // in the workspace's f8 region ([2][lay.f8_rows, H_kv, 128])
   bool f8_prefill = false;
   int64_t f8_rows = 0;       // sum of l_kv of the current plan
-  uint16_t* f8_buf = nullptr;  // engine-owned [2][f8_cap_rows, H_kv, 128] 16-bit
-  int64_t f8_cap_rows = 0;
-  long long* trace = nullptr;  // debug: device buffer for kernel pipeline traces
+  bool captured = false;     // a run() was captured into a CUDA graph since the last release
+  LaunchSig cap_sig;         // launch choices of that captured run()
+  long long* trace = nullptr;  // BSRA_EXPERIMENTS builds: device buffer for kernel pipeline traces
   int32_t last_launches = 0;
   const char* selected = "none";
 };
@@ -207,6 +227,7 @@ bsra_status bsra_engine_create(const bsra_config* cfg, int32_t device, void* d_w
   e->k_scale = cfg->k_scale > 0.f ? cfg->k_scale : 1.f;
   e->v_scale = cfg->v_scale > 0.f ? cfg->v_scale : 1.f;
   e->device = device;
+  if (query_sms(device, &e->sms) != BSRA_OK) e->sms = 148;
   e->lay = lay;
   e->ws = static_cast<uint8_t*>(d_workspace);
   int prev = 0;
@@ -231,7 +252,6 @@ void bsra_engine_destroy(bsra_engine* e) {
     cudaEventDestroy(e->staged);
   }
   if (e->staging) cudaFreeHost(e->staging);
-  if (e->f8_buf) cudaFree(e->f8_buf);
   delete e;
 }
 
@@ -304,6 +324,13 @@ void pad_queues(std::vector<int32_t>& im, int32_t nc) {
   im.insert(im.begin() + bsra::kHeaderWords + c + 1, (size_t)(nc - c), n_items);
 }
 
+bool is_ragged_engine(const bsra_engine* e) { return (e->cfg.flags & BSRA_FLAG_RAGGED_KV) != 0; }
+int64_t ragged_total(const std::vector<int32_t>& kv) {
+  int64_t t = 0;
+  for (int32_t x : kv) t += x;
+  return t;
+}
+
 bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* page_begin,
                       const std::vector<int32_t>& qo, const std::vector<int32_t>& kv, float sm_scale, void* stream) {
   const bsra_config& c = e->cfg;
@@ -336,6 +363,11 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
   const int32_t g = c.num_qo_heads / c.num_kv_heads;
   const bool f8_prefill = kv_is_f8(c) && sum.T_q > 16 && c.kernel != BSRA_KERNEL_SIMT && c.head_dim == 128 &&
                           (g & (g - 1)) == 0;
+  int32_t max_qo = 0;
+  for (int32_t x : qo) max_qo = std::max(max_qo, x);
+  if (c.max_qo_len > 0 && max_qo > c.max_qo_len) return fail(BSRA_EBOUNDS, "a request's l_qo exceeds max_qo_len");
+  const int64_t fused = std::min<int64_t>(16, (int64_t)(c.max_qo_len > 0 ? c.max_qo_len : max_qo) * g);
+  const int32_t kc = fused <= 4 ? 4 : fused <= 8 ? 8 : 16;
   std::vector<int32_t> kv_off;
   int64_t f8_rows = 0;
   if (f8_prefill) {
@@ -351,13 +383,21 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
   pad_queues(im, c.num_ctas);
   if (im.size() > e->lay.plan_words) return fail(BSRA_EBOUNDS, "plan image exceeds the workspace plan section");
   if (sum.T_q > e->lay.T_max) return fail(BSRA_EBOUNDS, "tile larger than the workspace partial slots");
-  if (f8_prefill && f8_rows > e->f8_cap_rows) {  // engine-owned 16-bit copy (grows; see bsra.h)
-    const int64_t cap = std::max<int64_t>(f8_rows, e->f8_cap_rows * 5 / 4);
-    uint16_t* nb = nullptr;
-    CUDA_TRY(cudaMalloc(&nb, (size_t)cap * c.num_kv_heads * 128 * 2 * sizeof(uint16_t)));
-    if (e->f8_buf) CUDA_TRY(cudaFree(e->f8_buf));
-    e->f8_buf = nb;
-    e->f8_cap_rows = cap;
+  if (f8_prefill && f8_rows > e->lay.f8_rows)
+    return fail(BSRA_EBOUNDS, "fp8 KV with prefill tiles: sum of l_kv (" + std::to_string(f8_rows) +
+                                  ") exceeds max_total_kv_tokens (" + std::to_string(e->lay.f8_rows) +
+                                  "), the workspace's 16-bit gather region");
+  if (e->captured) {  // a CUDA graph holds the launch choices of an earlier plan (bsra.h, bsra_run)
+    const LaunchSig& k = e->cap_sig;
+    std::string why;
+    if (sum.T_q != k.T_q) why = "query tile T_q " + std::to_string(k.T_q) + " -> " + std::to_string(sum.T_q);
+    else if (sum.T_q == 16 && kc > k.kc) why = "decode live columns " + std::to_string(k.kc) + " -> " + std::to_string(kc);
+    else if (f8_prefill != k.f8_prefill) why = "fp8 gather pass";
+    else if (rows > k.q_extent) why = "q rows beyond the captured tensor-map extent";
+    else if (is_ragged_engine(e) && ragged_total(kv) > k.kv_extent) why = "KV tokens beyond the captured extent";
+    if (!why.empty())
+      return fail(BSRA_EBOUNDS, "re-plan changes a launch choice baked into a captured CUDA graph (" + why +
+                                    "); destroy the graph, call bsra_graph_release and re-capture");
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // the previous upload must have left the pinned buffer before it is overwritten
@@ -384,8 +424,8 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
   e->f8_rows = f8_rows;
   e->sm_scale = sm_scale > 0.f ? sm_scale : 1.f / std::sqrt((float)c.head_dim);
   e->total_qo = rows;
-  e->max_qo = 0;
-  for (int32_t x : qo) e->max_qo = std::max(e->max_qo, x);
+  e->max_qo = max_qo;
+  e->kc = kc;
   return BSRA_OK;
 }
 
@@ -535,6 +575,15 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   const int grid = c.num_ctas;
   bsra_status s = BSRA_OK;
   const int T_q = e->summary.T_q;
+  cudaStreamCaptureStatus cap_status = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(st, &cap_status));
+  const bool capturing = cap_status != cudaStreamCaptureStatusNone;
+  // tensor-map extents: the plan's exact sizes, or under capture the engine bounds, so a replay
+  // after a re-plan within the bounds still covers every row (bsra.h, bsra_run)
+  const int64_t q_extent = capturing ? std::max<int64_t>(c.max_total_qo_rows, e->total_qo) : e->total_qo;
+  int64_t kv_extent = e->total_kv;
+  if (ragged && capturing && c.max_total_kv_tokens > 0) kv_extent = std::max<int64_t>(c.max_total_kv_tokens, kv_extent);
+  if (e->f8_prefill) kv_extent = e->lay.f8_rows;  // the workspace gather region's rows
   bool used_tc = false;
   int gather_launches = 0;
   bool kv16 = !kv_is_f8(c);  // the attention kernel reads 16-bit (or f32) K/V
@@ -558,10 +607,11 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     gp.page_size = c.page_size;
     gp.H_kv = c.num_kv_heads;
     gp.f16 = c.dtype == BSRA_F16;
-    const int64_t plane = e->f8_cap_rows * c.num_kv_heads * 128;
-    gp.ko = e->f8_buf;
-    gp.vo = e->f8_buf + plane;
-    bsra::f8_gather_kernel<<<4 * 148, 256, 0, st>>>(gp);
+    const int64_t plane = e->lay.f8_rows * c.num_kv_heads * 128;
+    uint16_t* f8_buf = reinterpret_cast<uint16_t*>(e->ws + e->lay.off_f8);
+    gp.ko = f8_buf;
+    gp.vo = f8_buf + plane;
+    bsra::f8_gather_kernel<<<4 * e->sms, 256, 0, st>>>(gp);
     CUDA_TRY(cudaGetLastError());
     gather_launches = 1;
     p.k = gp.ko;
@@ -577,14 +627,16 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     tl.f16 = c.dtype == BSRA_F16;
     tl.T_q = T_q;
     tl.grid = grid;
-    tl.total_qo = e->total_qo;
+    tl.total_qo = q_extent;
     tl.align = c.kv_chunk_align ? c.kv_chunk_align : c.page_size;
     tl.page_size = c.page_size;
-    tl.max_qo = e->max_qo;
+    tl.kc = e->kc;
     tl.mask = c.mask;
-    tl.pdl = (c.flags & BSRA_FLAG_PDL) != 0;
+    // PDL lets the kernel start before its predecessor drains; the fp8 prefill kernel reads the
+    // 16-bit copy the gather kernel right before it writes, so it is launched fully serialised
+    tl.pdl = (c.flags & BSRA_FLAG_PDL) != 0 && !e->f8_prefill;
     tl.ragged = ragged;
-    tl.total_kv = e->f8_prefill ? e->f8_rows : e->total_kv;
+    tl.total_kv = kv_extent;
     tl.f8kv = !kv16;
     const char* why = "";
     int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
@@ -610,12 +662,27 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   }
   e->last_launches = 1 + gather_launches;
   if (!p.fused_merge) {  // contraction stage: fixed grid, exits at once if nothing split
-    const int cgrid = std::max(1, std::min(grid, 2 * 148));
+    const int cgrid = std::max(1, std::min(grid, 2 * e->sms));
     if (c.o_dtype == BSRA_F32 || c.dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
     else if (c.dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
     else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
     if (s) return s;
     e->last_launches = 2 + gather_launches;
+  }
+  if (capturing) {  // record what the graph baked in; later plans are checked against it
+    LaunchSig k;
+    k.T_q = T_q;
+    k.kc = e->kc;
+    k.f8_prefill = e->f8_prefill;
+    k.q_extent = q_extent;
+    k.kv_extent = ragged && !e->f8_prefill ? kv_extent : INT64_MAX;
+    if (e->captured) {  // several captures: keep the most restrictive choices
+      k.kc = std::min(k.kc, e->cap_sig.kc);
+      k.q_extent = std::min(k.q_extent, e->cap_sig.q_extent);
+      k.kv_extent = std::min(k.kv_extent, e->cap_sig.kv_extent);
+    }
+    e->cap_sig = k;
+    e->captured = true;
   }
   return BSRA_OK;
 }
@@ -643,6 +710,13 @@ bsra_status bsra_run_ragged(bsra_engine* e, const void* q, const void* k, const 
   return run_core(e, q, k, v, ks, vs, nullptr, true, custom_mask, mask_bit_indptr, o, lse, stream);
 }
 
+bsra_status bsra_graph_release(bsra_engine* e) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  e->captured = false;
+  e->cap_sig = LaunchSig();
+  return BSRA_OK;
+}
+
 bsra_status bsra_set_kv_scales(bsra_engine* e, float k_scale, float v_scale) {
   if (!e) return fail(BSRA_EINVAL, "NULL engine");
   if (!(k_scale >= 0.f) || !std::isfinite(k_scale) || !(v_scale >= 0.f) || !std::isfinite(v_scale))
@@ -666,8 +740,8 @@ namespace {
 template <typename TI, typename TO, int D>
 bsra_status merge_states_t(const void* oa, const float* la, const void* ob, const float* lb, int64_t n, void* out,
                            float* lo, cudaStream_t st) {
-  const int grid = (int)std::min<int64_t>((n + 7) / 8, 148 * 16);
   if (n == 0) return BSRA_OK;
+  const int grid = (int)std::min<int64_t>((n + 7) / 8, 148 * 16);  // grid-stride loop: any size works
   bsra::merge_states_kernel<TI, TO, D><<<grid, 256, 0, st>>>(static_cast<const TI*>(oa), la, static_cast<const TI*>(ob),
                                                               lb, n, static_cast<TO*>(out), lo);
   CUDA_TRY(cudaGetLastError());
@@ -691,7 +765,7 @@ bsra_status merge_states_o(bsra_dtype to, int D, const void* oa, const float* la
 template <typename TO, int D>
 bsra_status merge_many_t(const float* op, const float* lp, int P, int64_t n, void* out, float* lo, cudaStream_t st) {
   if (n == 0) return BSRA_OK;
-  const int grid = (int)std::min<int64_t>((n + 7) / 8, 148 * 16);
+  const int grid = (int)std::min<int64_t>((n + 7) / 8, 148 * 16);  // grid-stride loop: any size works
   bsra::merge_many_kernel<TO, D><<<grid, 256, 0, st>>>(op, lp, P, n, static_cast<TO*>(out), lo);
   CUDA_TRY(cudaGetLastError());
   return BSRA_OK;

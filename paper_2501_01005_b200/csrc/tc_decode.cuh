@@ -45,7 +45,7 @@ struct TcParams {
   int32_t q_hb, q_tb;
   int32_t f16;      // 1 = fp16 inputs, 0 = bf16
   int32_t pdl;      // launched with programmatic dependent launch (host-side launch choice)
-  int32_t dbg;      // timing experiments only ($BSRA_DEBUG_PREFILL): 1 skip softmax, 2 skip MMAs, 4 one WG
+  int32_t dbg;      // BSRA_EXPERIMENTS builds only ($BSRA_DEBUG_PREFILL timing modes); 0 otherwise
 };
 
 // Kernel launch honouring TcParams::pdl (cudaLaunchAttributeProgrammaticStreamSerialization).
@@ -176,7 +176,9 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();  // PDL: the next kernel's CTAs may take SMs this grid releases
   // debug (p.trace set): per-CTA start / end time, globaltimer ns (scripts/cta_balance.py)
+#ifdef BSRA_EXPERIMENTS
   if (p.trace && threadIdx.x == 0) p.trace[16 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
+#endif
 
   if (warp == 0) {
     // ============================ TMA producer ============================
@@ -565,7 +567,9 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   }
   ptx::tc_fence_before();
   __syncthreads();
+#ifdef BSRA_EXPERIMENTS
   if (p.trace && threadIdx.x == 0) p.trace[17 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
+#endif
   if (warp == 5) ptx::tmem_dealloc<kTmemCols>(tmem);
 }
 

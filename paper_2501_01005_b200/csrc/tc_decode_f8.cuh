@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
   // debug timeline of CTA 0 (p.trace set; scripts/trace_decode_f8.py): clock64 per event and tile
-#ifdef BSRA_F8_TRACE
+#ifdef BSRA_EXPERIMENTS
   long long* trace = blockIdx.x == 0 ? p.trace : nullptr;
 #define F8T(ev, i) \
   if (trace && (i) < 1024) trace[(ev) * 1024 + (i)] = clock64();

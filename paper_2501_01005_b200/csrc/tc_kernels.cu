@@ -154,9 +154,7 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
       *why = "cuTensorMapEncodeTiled failed";
       return -1;
     }
-    const int64_t fused = std::min<int64_t>(16, (int64_t)L.max_qo * g);
-    const int kc = fused <= 4 ? 4 : fused <= 8 ? 8 : 16;
-    if (launch_decode(L.f8kv, kc, L.mask, tp, L.grid, st) != cudaSuccess) return -1;
+    if (launch_decode(L.f8kv, L.kc, L.mask, tp, L.grid, st) != cudaSuccess) return -1;
     *name = "tc_decode";
     return 1;
   }

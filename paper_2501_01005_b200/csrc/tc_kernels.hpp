@@ -10,14 +10,14 @@ struct TcLaunch {
   bool f16 = false;        // fp16 inputs (else bf16)
   int T_q = 0;             // plan tile
   int grid = 0;            // persistent grid (= plan num_ctas)
-  int64_t total_qo = 0;    // sum of l_qo of the current plan (q tensor extent)
+  int64_t total_qo = 0;    // rows of the q tensor map (the plan's sum of l_qo; max_total_qo_rows under capture)
   int align = 0;           // chunk alignment in tokens
   int page_size = 0;
-  int max_qo = 0;          // max l_qo of the current plan (live fused columns)
+  int kc = 16;             // decode: live fused columns (4 / 8 / 16), from the plan or max_qo_len
   int mask = 0;
   bool pdl = false;        // programmatic dependent launch (BSRA_FLAG_PDL)
   bool ragged = false;     // contiguous KV [N, H_kv, D] (p.kv_ragged)
-  int64_t total_kv = 0;    // ragged: N, the token extent of k / v
+  int64_t total_kv = 0;    // ragged: the token extent of the k / v maps
   bool f8kv = false;       // K/V pools in E4M3 (fp8 KV cache, R28)
 };
 

@@ -204,14 +204,21 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   const int B = tp.box_tok;
   // item streams: 2 (one per softmax WG); 1 when paired (both WGs on every item) or in the
   // one-WG timing experiment
-  const int nstream = (kPair || (tp.dbg & 4)) ? 1 : 2;
-  const int ps = p.page_size;
-  // debug trace (CTA 0): trace[ev * 1024 + i] = clock64() of the i-th event of kind ev
+#ifdef BSRA_EXPERIMENTS
+  // timing experiments and the CTA-0 pipeline trace (scripts/trace_prefill.py); the shipped
+  // build compiles them out (dbg = 0, no trace stores)
+  const int dbg = tp.dbg;
   long long* const trace = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
 #define BSRA_TRACE(ev, i) \
   if (trace && (i) < 1024) trace[(ev) * 1024 + (i)] = clock64();
-  if (threadIdx.x == 0) BSRA_TRACE(9, 0);
   if (p.trace && threadIdx.x == 0) p.trace[16 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
+#else
+  constexpr int dbg = 0;
+#define BSRA_TRACE(ev, i)
+#endif
+  const int nstream = (kPair || (dbg & 4)) ? 1 : 2;
+  const int ps = p.page_size;
+  if (threadIdx.x == 0) BSRA_TRACE(9, 0);
 
   if (warp == 3) {
     ptx::setmaxnreg_dec<kRegsLow>();
@@ -350,7 +357,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         ptx::tma_load_4d(dst + kHalf, tm, &fullx[stage], 64, kvh, off, page);
       }
       __syncwarp();
-      if ((tp.dbg & 8) && lane == 0) {  // timing experiment: TMA issue -> landed latency
+      if ((dbg & 8) && lane == 0) {  // timing experiment: TMA issue -> landed latency
         ptx::mbar_wait(&fullx[stage], ephase ^ 1);
         BSRA_TRACE(isK ? 15 : 14, pos);
       }
@@ -376,7 +383,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t step = (uint64_t)((kk >> 2) * (kHalf >> 4) + (kk & 3) * 2);
-        if (!(tp.dbg & 2)) ptx::mma_f16_ss_warp(dS, a0 + step, b0 + step, idS, kk > 0);
+        if (!(dbg & 2)) ptx::mma_f16_ss_warp(dS, a0 + step, b0 + step, idS, kk > 0);
       }
     };
     // O_w += P_w V from V stage vs; +128 (2 KB = 16 tokens) per K step of the MN-major V
@@ -385,7 +392,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
       const uint32_t dO = tmem + 256 + w * 128, aP = tmem + w * 128;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
-        if (!(tp.dbg & 2)) ptx::mma_f16_ts_warp(dO, aP + kk * 8, b0 + (uint64_t)(kk * 128), idO, (first && kk == 0) ? 0u : 1u);
+        if (!(dbg & 2)) ptx::mma_f16_ts_warp(dO, aP + kk * 8, b0 + (uint64_t)(kk * 128), idO, (first && kk == 0) ? 0u : 1u);
     };
     // rows past the chunk end -> 0 in the V stage (0 * garbage could be NaN)
     auto zero_v_tail = [&](int vs, int n) {
@@ -581,7 +588,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         sph ^= 1;
         if (r == 0) BSRA_TRACE(5 + 2 * w, tcount);
         ptx::tc_fence_after();
-        if (tp.dbg & 1) {  // timing experiment: no softmax work (results are garbage)
+        if (dbg & 1) {  // timing experiment: no softmax work (results are garbage)
           ptx::tc_fence_before();
           ptx::mbar_arrive(&p_ready[w]);
           ++tcount;
@@ -671,9 +678,9 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         l = l * alpha + ((r01.x + r01.y) + (r23.x + r23.y));
         } else {
         // ---- pass 1: raw row max (two 32-column TMEM loads in flight per round trip)
-        float mx = (tp.dbg & 16) ? 0.f : -INFINITY;  // dbg 16: timing experiment, no max pass
+        float mx = (dbg & 16) ? 0.f : -INFINITY;  // dbg 16: timing experiment, no max pass
 #pragma unroll
-        for (int c = 0; c < ((tp.dbg & 16) ? 0 : 4); c += 2) {
+        for (int c = 0; c < ((dbg & 16) ? 0 : 4); c += 2) {
           float s[64];
           ptx::tmem_ld32(tS + c * 32, s);
           ptx::tmem_ld32(tS + c * 32 + 32, s + 32);
@@ -795,14 +802,14 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 32) {
         float ov[32];
-        if (d.ntiles > 0 && !(tp.dbg & 128)) {  // dbg 128: timing experiment, no O read
+        if (d.ntiles > 0 && !(dbg & 128)) {  // dbg 128: timing experiment, no O read
           ptx::tmem_ld32(tO + c0, ov);
           ptx::tmem_ld_wait();
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) ov[j] = 0.f;
         }
-        if (!row_ok || (tp.dbg & 64)) continue;  // dbg 64: timing experiment, no o stores
+        if (!row_ok || (dbg & 64)) continue;  // dbg 64: timing experiment, no o stores
         // 256-bit stores: a lane writes whole 32-byte sectors of its row (half the instructions of
         // 16-byte stores; rows of a warp are scattered, so the instruction count is the cost)
         if (d.slot >= 0 || p.o_f32) {
@@ -850,7 +857,9 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
   ptx::tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) BSRA_TRACE(9, 1);
+#ifdef BSRA_EXPERIMENTS
   if (p.trace && threadIdx.x == 0) p.trace[17 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
+#endif
 #undef BSRA_TRACE
   if (warp == 2) ptx::tmem_dealloc<kTmemCols>(tmem);
 }

@@ -229,6 +229,25 @@ def make_inputs(wl: Workload, *, device="cpu", seed_base=0, permute=True, layout
                   float(sm_scale) if sm_scale is not None else 1.0 / float(np.sqrt(wl.D)), ks, vs)
 
 
+def head_slice(inp: Inputs, h0: int, h1: int) -> Inputs:
+    """The kv heads [h0, h1) of `inp` and their qo heads [h0*g, h1*g) as a self-contained Inputs
+    (data movement only: a contiguous q slice and NHD pools holding only those heads; the page
+    table is shared). What one rank of a KV-head-sharded run holds."""
+    wl = inp.wl
+    g = wl.g
+    wl2 = dataclasses.replace(wl, H_qo=(h1 - h0) * g, H_kv=h1 - h0)
+    q = inp.q[:, h0 * g:h1 * g].contiguous()
+
+    def cut(pool, st):
+        n = pool.numel() // max(1, st[0])
+        view = torch.as_strided(pool, (n, wl.page_size, wl.H_kv, wl.D), (st[0], st[1], st[2], 1))
+        return view[:, :, h0:h1].contiguous()
+
+    k, v = cut(inp.k_pool, inp.k_strides), cut(inp.v_pool, inp.v_strides)
+    st = (wl.page_size * (h1 - h0) * wl.D, (h1 - h0) * wl.D, wl.D)
+    return dataclasses.replace(inp, wl=wl2, q=q, k_pool=k, v_pool=v, k_strides=st, v_strides=st)
+
+
 @dataclasses.dataclass
 class RaggedKV:
     """The same keys / values as a paged Inputs, laid out contiguously:

@@ -220,15 +220,57 @@ def test_fp8_prefill_tc_split_kv_and_variants(cuda_device, nc):
 
 
 @pytest.mark.gpu
-def test_fp8_prefill_replan_grows_buffer(cuda_device):
-    """A later plan with more KV tokens grows the engine's 16-bit copy; a smaller one reuses it."""
+def test_fp8_prefill_replan_within_workspace_region(cuda_device):
+    """The 16-bit gather copy lives in the caller's workspace, sized by max_total_kv_tokens: plans
+    up to the bound reuse it (small -> big -> small), a plan beyond it fails with EBOUNDS and
+    keeps the previous plan; the library allocates no device memory (§8(b) ownership)."""
     small, big = _pre(qo=(70, 30), kv=(70, 90)), _pre(qo=(300, 500, 64), kv=(900, 2000, 64))
     eng = engine_for(big, num_ctas=148, tile_q=128, max_batch=4, max_rows=2048)
+    assert eng.cfg.max_total_kv_tokens == int(big.kv_lens.sum())
     for wl in (small, big, small):
         inp = synth.make_inputs(wl, device=cuda_device)
         gpu = run_gpu(inp, eng)
         assert gpu[2].selected_kernel() == "tc_prefill"
         assert_close(gpu, oracle.attention_from_inputs(inp), "bf16", what=f"replan {wl.kv_lens}")
+    too_big = _pre(qo=(300, 500, 64), kv=(900, 2001, 64))
+    inp = synth.make_inputs(too_big, device=cuda_device)
+    with pytest.raises(bsra.BsraError, match="max_total_kv_tokens"):
+        eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+    # a plan without the bound fails loudly instead of allocating
+    eng0 = engine_for(small, num_ctas=148, tile_q=128, max_kv=-1)
+    inp = synth.make_inputs(small, device=cuda_device)
+    with pytest.raises(bsra.BsraError, match="max_total_kv_tokens"):
+        eng0.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tile_q", [128, 256])
+def test_fp8_prefill_with_pdl(cuda_device, tile_q):
+    """BSRA_FLAG_PDL on an fp8 engine with prefill tiles: the prefill kernel reads the copy the
+    gather kernel just wrote, so it must not overlap it (launched without PDL); several runs
+    back to back on one stream, each checked."""
+    wls = [_pre(qo=(700, 1, 64), kv=(900, 3000, 64)), _pre()]
+    mx = max(int(w.kv_lens.sum()) for w in wls)
+    outs = []
+    for wl in wls:
+        inp = synth.make_inputs(wl, device=cuda_device)
+        cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
+                               mask=wl.mask, max_batch=4, max_total_qo_rows=2048, num_ctas=148, tile_q=tile_q,
+                               kv_dtype="e4m3", k_scale=inp.k_scale, v_scale=inp.v_scale, pdl=True,
+                               max_total_kv_tokens=mx)
+        eng = bsra.Engine(cfg, 0)
+        nq = int(inp.qo_indptr[-1])
+        o = torch.full((nq, wl.H_qo, wl.D), float("nan"), device=cuda_device, dtype=torch.bfloat16)
+        lse = torch.full((nq, wl.H_qo), float("nan"), device=cuda_device)
+        eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+        outs.append((inp, eng, o, lse))
+    for _ in range(3):  # interleaved: each run follows the other engine's kernels on the stream
+        for inp, eng, o, lse in outs:
+            eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse)
+    torch.cuda.synchronize()
+    for inp, eng, o, lse in outs:
+        assert_close((o.float().cpu().numpy(), lse.cpu().numpy()), oracle.attention_from_inputs(inp), "bf16",
+                     what="fp8 prefill + PDL")
 
 
 @pytest.mark.gpu
@@ -238,7 +280,8 @@ def test_fp8_prefill_ragged_kv(cuda_device):
     inp = synth.make_inputs(wl, device=cuda_device)
     cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=128, dtype=wl.dtype, mask=wl.mask,
                            max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()), num_ctas=64, tile_q=128,
-                           ragged_kv=True, kv_dtype="e4m3", k_scale=inp.k_scale, v_scale=inp.v_scale)
+                           ragged_kv=True, kv_dtype="e4m3", k_scale=inp.k_scale, v_scale=inp.v_scale,
+                           max_total_kv_tokens=int(wl.kv_lens.sum()))
     gpu = run_ragged(inp, bsra.Engine(cfg, 0))
     assert gpu[2].selected_kernel() == "tc_prefill"
     assert_close(gpu, oracle.attention_from_inputs(inp), "bf16", what="fp8 ragged prefill")
@@ -325,6 +368,6 @@ def test_fp8_with_balanced_queues(cuda_device, tile_q):
     inp = synth.make_inputs(wl, device=cuda_device)
     cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
                            max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()), num_ctas=148, tile_q=tile_q,
-                           kv_dtype="e4m3", balance_ctas=True)
+                           kv_dtype="e4m3", balance_ctas=True, max_total_kv_tokens=int(wl.kv_lens.sum()))
     gpu = run_gpu(inp, bsra.Engine(cfg, 0))
     assert_close(gpu, oracle.attention_from_inputs(inp), wl.dtype, what=f"fp8 balanced T_q={tile_q}")

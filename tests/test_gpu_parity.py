@@ -139,6 +139,114 @@ def test_graph_capture_and_replan(cuda_device):
                  what="graph step 2")
 
 
+class _GraphRig:
+    """Fixed-address buffers sized by engine bounds (q / o / lse rows = max_total_qo_rows, pools,
+    page table), so one captured graph can be replayed over a sequence of plans: each workload's
+    inputs are copied into the captured addresses before its replay."""
+
+    def __init__(self, dev, H_qo, H_kv, D, ps, max_rows, max_pages):
+        self.dev = dev
+        self.q = torch.zeros((max_rows, H_qo, D), device=dev, dtype=torch.bfloat16)
+        self.o = torch.zeros((max_rows, H_qo, D), device=dev, dtype=torch.bfloat16)
+        self.lse = torch.zeros((max_rows, H_qo), device=dev)
+        self.k = torch.zeros((max_pages, ps, H_kv, D), device=dev, dtype=torch.bfloat16)
+        self.v = torch.zeros_like(self.k)
+        self.idx = torch.zeros(max_pages, dtype=torch.int32, device=dev)
+        self.s = torch.cuda.Stream()
+        self.graph = None
+
+    def load(self, inp):
+        nq, npg, nnz = inp.q.shape[0], inp.k_pool.shape[0], inp.kv_page_indices.numel()
+        self.q[:nq].copy_(inp.q)
+        self.k[:npg].copy_(inp.k_pool)
+        self.v[:npg].copy_(inp.v_pool)
+        self.idx[:nnz].copy_(inp.kv_page_indices)
+        torch.cuda.synchronize()
+        return nq
+
+    def run(self, eng):
+        eng.run(self.q, self.k, self.v, self.k.stride()[:3], self.v.stride()[:3], self.idx, self.o, self.lse,
+                stream=self.s)
+
+    def capture(self, eng):
+        with torch.cuda.stream(self.s):
+            self.run(eng)  # warm (first-launch attribute setup stays outside the graph)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.s):
+            self.run(eng)
+
+    def check(self, inp, nq, what):
+        self.o[:nq].fill_(float("nan"))
+        torch.cuda.synchronize()
+        self.graph.replay()
+        torch.cuda.synchronize()
+        assert_close((self.o[:nq].float().cpu().numpy(), self.lse[:nq].cpu().numpy()),
+                     oracle.attention_from_inputs(inp), "bf16", what=what)
+
+
+def _dec_wl(qo, kv):
+    return synth.Workload("gr", 32, 8, 128, 16, "bf16", "causal", np.array(qo, np.int32), np.array(kv, np.int32))
+
+
+def test_graph_replay_across_growing_plans(cuda_device):
+    """a graph captured once must stay correct when later plans within the
+    engine bounds grow the batch, the rows, and l_qo per request. With max_qo_len set, the decode
+    kernel's live columns come from the bound, and under capture the q map spans max_total_qo_rows
+    rows, so every replay below is of the SAME graph."""
+    seq = [_dec_wl([1] * 4, [40, 300, 17, 900]),
+           _dec_wl([1, 2, 1, 2, 2, 1, 1, 2], [5, 64, 700, 33, 1200, 16, 2, 257]),
+           _dec_wl([2, 2, 2], [3000, 2, 129])]
+    rig = _GraphRig(cuda_device, 32, 8, 128, 16, max_rows=16, max_pages=512)
+    cfg = bsra.make_config(H_qo=32, H_kv=8, D=128, page_size=16, dtype="bf16", mask="causal", max_batch=8,
+                           max_total_qo_rows=16, max_qo_len=2, num_ctas=148, tile_q=16, pdl=True)
+    eng = bsra.Engine(cfg, 0)
+    for k, wl in enumerate(seq):
+        inp = synth.make_inputs(wl, device=cuda_device, seed_base=10 * k)
+        nq = rig.load(inp)
+        eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale, stream=rig.s)
+        if rig.graph is None:
+            rig.capture(eng)
+        rig.check(inp, nq, f"replay {k}")
+    with pytest.raises(bsra.BsraError, match="max_qo_len"):
+        inp = synth.make_inputs(_dec_wl([3], [50]), device=cuda_device)
+        eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+
+
+def test_graph_guard_rejects_replans_a_replay_cannot_run(cuda_device):
+    """Without max_qo_len the live columns follow the plan. After a capture at l_qo = 1 (4 live
+    columns), a plan needing 8 columns, or another query tile, fails with EBOUNDS and keeps the
+    old plan (the graph still replays it correctly); bsra_graph_release lifts the guard and a
+    re-captured graph runs the new plan."""
+    rig = _GraphRig(cuda_device, 32, 8, 128, 16, max_rows=64, max_pages=512)
+    cfg = bsra.make_config(H_qo=32, H_kv=8, D=128, page_size=16, dtype="bf16", mask="causal", max_batch=8,
+                           max_total_qo_rows=64, num_ctas=148, tile_set=(16, 64, 128))
+    eng = bsra.Engine(cfg, 0)
+    wl1 = _dec_wl([1] * 5, [40, 300, 17, 900, 64])
+    inp1 = synth.make_inputs(wl1, device=cuda_device)
+    nq1 = rig.load(inp1)
+    eng.plan(inp1.qo_indptr, inp1.kv_page_indptr, inp1.kv_last_page_len, inp1.sm_scale, stream=rig.s)
+    rig.capture(eng)
+    rig.check(inp1, nq1, "captured plan")
+    grow_cols = synth.make_inputs(_dec_wl([1, 2, 1], [40, 300, 17]), device=cuda_device, seed_base=1)
+    grow_tile = synth.make_inputs(_dec_wl([40, 1], [40, 300]), device=cuda_device, seed_base=2)
+    for inp, why in ((grow_cols, "live columns"), (grow_tile, "query tile")):
+        with pytest.raises(bsra.BsraError, match=why):
+            eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale, stream=rig.s)
+        rig.check(inp1, nq1, f"old plan kept after a refused re-plan ({why})")
+    # shrinking within the captured choices is fine without a release
+    inp3 = synth.make_inputs(_dec_wl([1] * 3, [5, 6, 700]), device=cuda_device, seed_base=3)
+    nq3 = rig.load(inp3)
+    eng.plan(inp3.qo_indptr, inp3.kv_page_indptr, inp3.kv_last_page_len, inp3.sm_scale, stream=rig.s)
+    rig.check(inp3, nq3, "smaller plan, same graph")
+    eng.graph_release()
+    nq = rig.load(grow_cols)
+    eng.plan(grow_cols.qo_indptr, grow_cols.kv_page_indptr, grow_cols.kv_last_page_len, grow_cols.sm_scale,
+             stream=rig.s)
+    rig.capture(eng)
+    rig.check(grow_cols, nq, "re-captured after release")
+
+
 def test_bounds_are_enforced(cuda_device):
     wl = synth.Workload("b", 8, 2, 64, 4, "bf16", "none", np.ones(3, np.int32), np.array([5, 6, 7], np.int32))
     eng = engine_for(wl, max_batch=2, max_rows=2)

@@ -21,7 +21,7 @@ def _engine(wl, **kw):
     cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
                            mask=wl.mask, max_batch=max(1, wl.batch), max_total_qo_rows=max(1, int(wl.qo_lens.sum())),
                            window=wl.window, soft_cap=wl.soft_cap, alibi=wl.alibi,
-                           kv_dtype=wl.kv_dtype or None, **kw)
+                           kv_dtype=wl.kv_dtype or None, max_total_kv_tokens=int(wl.kv_lens.sum()), **kw)
     return bsra.Engine(cfg, 0)
 
 
