@@ -11,8 +11,11 @@ it is read (no flush needed; stated in config).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N > 1 (torchrun): every rank runs its own configs[1] batch (requests sharded, no collective
-on the data path) -> "scaling": "weak"; the time is the max over ranks.
+N > 1: launched under torchrun (or `--gpus N` alone re-launches itself under torchrun), one
+rank per GPU. Headline: every rank runs its own configs[1] batch (requests sharded, no
+collective on the data path) -> "scaling": "weak"; the time is the max over ranks. Secondary
+keys shard the FIXED workload: configs[1] and configs[2] / configs[3] by KV head (no
+collective, strong scaling), configs[4] along the sequence (NCCL all-gather + merge).
 """
 from __future__ import annotations
 
@@ -45,6 +48,8 @@ def emit(obj) -> None:
 import synth  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# BASELINE.json's metric, printed identically by both arms (the driver pairs them by it)
+METRIC = "paged decode HBM TB/s & prefill TFLOP/s (% roofline) at 1/2/4/8 B200"
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -225,26 +230,56 @@ def per_launch_ms(L: Layered, eng, reps=3):
 
 
 def e2e_steps(L: Layered, eng, steps, warmup):
-    """End to end through the public API with HOST buffers: per step, H2D of every layer's q and
-    the page table from pinned memory, plan(), run() per layer, D2H of o and lse. KV pools are
-    the resident cache (model state), not per-step input."""
+    """End to end through the public API with HOST buffers. Per step: plan() on the host (Algorithm
+    1 + upload), then, for every layer r, H2D of q[r] from pinned memory, run(r), and D2H of o[r]
+    and lse[r] into pinned memory, plus the page table's H2D once per step. The copies run on a
+    copy stream and overlap the other layers' kernels (event-ordered per layer); the per-step
+    sequence of copies and run() calls is captured once in a CUDA graph (the same public calls,
+    replayed). KV pools are the resident cache (model state), not per-step input."""
     s = torch.cuda.Stream()
+    cp_in, cp_out = torch.cuda.Stream(), torch.cuda.Stream()
     host_q = [inp.q.cpu().pin_memory() for inp, _, _ in L.layers]
     host_idx = L.inp0.kv_page_indices.cpu().pin_memory()
     host_o = [o.cpu().pin_memory() for _, o, _ in L.layers]
     host_l = [l.cpu().pin_memory() for _, _, l in L.layers]
     h2d = sum(q.numel() * q.element_size() for q in host_q) + host_idx.numel() * 4
     d2h = sum(o.numel() * o.element_size() for o in host_o) + sum(l.numel() * 4 for l in host_l)
+    n = len(L.layers)
+
+    def body():
+        ev_in = [torch.cuda.Event() for _ in range(n)]
+        ev_run = [torch.cuda.Event() for _ in range(n)]
+        cp_in.wait_stream(s)
+        with torch.cuda.stream(cp_in):
+            L.inp0.kv_page_indices.copy_(host_idx, non_blocking=True)
+            for r, (inp, _, _) in enumerate(L.layers):
+                inp.q.copy_(host_q[r], non_blocking=True)
+                ev_in[r].record(cp_in)
+        for r in range(n):
+            s.wait_event(ev_in[r])
+            L.run_layer(eng, r, s)
+            ev_run[r].record(s)
+        with torch.cuda.stream(cp_out):
+            for r, (_, o, lse) in enumerate(L.layers):
+                cp_out.wait_event(ev_run[r])
+                host_o[r].copy_(o, non_blocking=True)
+                host_l[r].copy_(lse, non_blocking=True)
+        s.wait_stream(cp_out)
+        s.wait_stream(cp_in)
+
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        L.plan(eng, s)
+        body()  # eager warm pass
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        body()
 
     def step():
         with torch.cuda.stream(s):
-            L.inp0.kv_page_indices.copy_(host_idx, non_blocking=True)
             L.plan(eng, s)
-            for r, (inp, o, lse) in enumerate(L.layers):
-                inp.q.copy_(host_q[r], non_blocking=True)
-                L.run_layer(eng, r, s)
-                host_o[r].copy_(o, non_blocking=True)
-                host_l[r].copy_(lse, non_blocking=True)
+            graph.replay()
 
     for _ in range(warmup):
         step()
@@ -356,7 +391,7 @@ def bench_fp8_decode(dev, pk, args, world, rank, bf16_ms):
     import dataclasses
     wl = dataclasses.replace(synth.c2_decode_llama8b(), kv_dtype="e4m3")
     L = Layered(wl, args.layers, dev, seed_base=1000 * rank)
-    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel, pdl=not args.no_pdl)
+    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel, pdl=not args.no_pdl, max_qo_len=1)
     s, one_step, _ = time_device_steps(L, eng, args.steps, args.warmup, not args.no_graph)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(world)
@@ -378,13 +413,15 @@ def bench_fp8_decode(dev, pk, args, world, rank, bf16_ms):
             "kernel": eng.selected_kernel(), "algorithmic_bytes_per_launch": by["total"]}
 
 
-def bench_composable(dev, pk, layers=16, reps=20):
+def bench_composable(dev, pk, world=1, rank=0, layers=16, reps=20):
     """configs[3]: 8K shared prefix + 64 branches x 256-token suffixes, one decode step per layer
     through ComposableDecode (prefix engine on tensor-core tiles + suffix engine + ⊕), every layer
     its own pool (16 x 101.7 MB >> L2). Also the single-format baseline the paper compares with
     (64 requests x 528 pages through the decode kernel)."""
     import paper_2501_01005_b200 as bsra
-    cis = [synth.c4_composable(device=dev, seed_base=100 * r) for r in range(layers)]
+    h0, h1 = local_heads(8, world, rank)  # N > 1: the ranks split the 8 kv heads (no collective)
+    cis = [synth.c4_composable(device=dev, seed_base=100 * r + 1000 * rank, H_qo=4 * (h1 - h0), H_kv=h1 - h0)
+           for r in range(layers)]
     c0 = cis[0]
     n = c0.q.shape[0]
     comp = bsra.ComposableDecode(H_qo=c0.H_qo, H_kv=c0.H_kv, D=c0.D, page_size=c0.page_size, n_branch=n,
@@ -400,9 +437,10 @@ def bench_composable(dev, pk, layers=16, reps=20):
         for ci, (o, l) in zip(cis, outs):
             comp.run(ci.q, ci.k_pool, ci.v_pool, ci.strides, pi, si, o, l, stream=s)
 
-    ms = time_graph(step, s, reps) / layers
+    barrier(world)
+    ms = max_over_ranks(time_graph(step, s, reps) / layers, world)
     es = 2
-    unique = (8192 + n * 256) * c0.H_kv * c0.D * 2 * es + n * c0.H_qo * c0.D * es * 2 + n * c0.H_qo * 4
+    unique = (8192 + n * 256) * 8 * c0.D * 2 * es + n * 32 * c0.D * es * 2 + n * 32 * 4  # all 8 / 32 heads
     # single format: 64 requests over prefix + own suffix pages (re-reads the prefix per branch)
     cfg = bsra.make_config(H_qo=c0.H_qo, H_kv=c0.H_kv, D=c0.D, page_size=c0.page_size, dtype="bf16", max_batch=n,
                            max_total_qo_rows=n, num_ctas=148, tile_q=16)
@@ -415,11 +453,12 @@ def bench_composable(dev, pk, layers=16, reps=20):
         for ci, (o, l) in zip(cis, outs):
             eng.run(ci.q, ci.k_pool, ci.v_pool, ci.strides, ci.strides, sgi, o, l, stream=s)
 
-    ms_single = time_graph(step_single, s, max(3, reps // 4)) / layers
+    ms_single = max_over_ranks(time_graph(step_single, s, max(3, reps // 4)) / layers, world)
     tbs = unique / (ms * 1e-3) / 1e12
     return {"workload": "c4_composable (BASELINE configs[3]): 8K prefix + 64 x 256 suffix, 32/8 heads",
             "us_per_layer": ms * 1e3, "unique_bytes_per_layer": unique, "value": tbs, "unit": "TB/s (unique bytes)",
-            "frac": tbs * 1e3 / pk["hbm_gbs"], "single_format_us_per_layer": ms_single * 1e3,
+            "frac": tbs * 1e3 / world / pk["hbm_gbs"], "single_format_us_per_layer": ms_single * 1e3,
+            "n_gpus": world, "scaling": "strong (kv heads split)" if world > 1 else None,
             "speedup_vs_single_format": ms_single / ms, "launches_per_layer": comp.launches(),
             "kernels": [comp.prefix.selected_kernel(), comp.suffix.selected_kernel(), "merge_states"]}
 
@@ -431,9 +470,17 @@ def bench_long_context(dev, pk, world, rank, local, layers=2, reps=10):
     all-gather + ⊕ (bsra_dist). Total work fixed -> strong scaling of one long-context step."""
     import paper_2501_01005_b200 as bsra
     full = synth.c5_long_decode()
-    shard_len = int(full.kv_lens[0]) // world  # pages split evenly (32768 pages / P)
+    # this rank's share of every request (bsra_dist_shard_bsr over the full page table): its
+    # lengths decide the shard workload; the shard's own pool holds exactly those pages
+    ps = full.page_size
+    n_pages = full.num_pages()
+    kp = np.concatenate([[0], np.cumsum(n_pages)]).astype(np.int32)
+    last = (full.kv_lens - (n_pages - 1) * ps).astype(np.int32)
+    ki, _, kl = bsra.sequence_shard(kp, np.arange(int(kp[-1]), dtype=np.int32), last, ps, world, rank)
+    nr = ki[1:] - ki[:-1]
+    shard_lens = np.where(nr > 0, (nr - 1) * ps + kl, 0).astype(np.int32)
     wl = synth.Workload("c5_shard", full.H_qo, full.H_kv, full.D, full.page_size, full.dtype, "none",
-                        full.qo_lens.copy(), np.full(full.batch, shard_len, np.int32))
+                        full.qo_lens.copy(), shard_lens)
     Ls = [synth.make_inputs(wl, device=dev, seed_base=1000 * rank + 100 * r) for r in range(layers)]
     nq = wl.batch
     # few long rows: plan with the queue count of smallest Algorithm-1 makespan (148 CTAs would cut
@@ -476,7 +523,192 @@ def bench_long_context(dev, pk, world, rank, local, layers=2, reps=10):
             "gather_bytes_per_rank": nq * wl.H_qo * (wl.D + 1) * 4, "kernel": eng.selected_kernel()}
 
 
+# ------------------------------------------------------- sharded secondaries ---
+def local_heads(H_kv, world, rank):
+    import paper_2501_01005_b200 as bsra
+    return bsra.head_shard(H_kv, world, rank)
+
+
+def head_sharded_wl(wl, world, rank):
+    """The workload one rank of a P-way KV-head split holds: kv heads [h0, h1) and their qo heads
+    (bsra_dist_head_shard), same lengths. Bytes and flops are linear in heads, so the aggregate
+    over ranks is the whole workload's."""
+    import dataclasses
+    h0, h1 = local_heads(wl.H_kv, world, rank)
+    return dataclasses.replace(wl, H_qo=(h1 - h0) * wl.g, H_kv=h1 - h0), (h0, h1)
+
+
+def bench_decode_head_sharded(dev, pk, args, world, rank):
+    """configs[1] with the FIXED batch of 128 split by KV head over the ranks (strong scaling, no
+    collective: the output stays head-sharded, as in tensor-parallel attention). Same graph,
+    layers and timing as the headline; aggregate TB/s = whole-step bytes / max-over-ranks time."""
+    full = synth.c2_decode_llama8b()
+    wl, (h0, h1) = head_sharded_wl(full, world, rank)
+    L = Layered(wl, args.layers, dev, seed_base=1000 * rank)
+    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel, pdl=not args.no_pdl, max_qo_len=1)
+    s, one_step, _ = time_device_steps(L, eng, args.steps, args.warmup, not args.no_graph)
+    barrier(world)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        a.record(s)
+        for _ in range(args.steps):
+            one_step()
+        b.record(s)
+    torch.cuda.synchronize()
+    mine = a.elapsed_time(b) / args.steps
+    per_rank = gather_over_ranks(mine, world)
+    ms = max(per_rank)
+    step_bytes = decode_bytes(full)["total"] * args.layers
+    return {"workload": "c2_decode_llama8b (configs[1]), batch 128 fixed, KV heads split over ranks",
+            "scaling": "strong", "n_gpus": world, "kv_heads_rank0": [0, local_heads(full.H_kv, world, 0)[1]],
+            "value": step_bytes / (ms * 1e-3) / 1e12, "unit": "TB/s (aggregate)", "ms_per_step": ms,
+            "per_rank_ms": per_rank, "frac_per_gpu": step_bytes / (ms * 1e-3) / 1e9 / world / pk["hbm_gbs"]}
+
+
+def bench_prefill(dev, pk, args, world, rank):
+    """configs[2] ragged causal prefill, TFLOP/s over visible pairs. N > 1: KV heads split over the
+    ranks (8 kv heads; strong scaling), aggregate = whole-layer flops / max-over-ranks time."""
+    full = synth.c3_prefill_llama70b()
+    wl, _ = head_sharded_wl(full, world, rank) if world > 1 else (full, (0, full.H_kv))
+    L3 = Layered(wl, 2, dev, seed_base=1000 * rank)
+    e3 = L3.engine(num_ctas=args.num_ctas, kernel=args.kernel, tile_q=args.prefill_tile)
+    mine = per_launch_ms(L3, e3, reps=3)
+    per_rank = gather_over_ranks(mine, world)
+    p_ms = max(per_rank)
+    fl = causal_flops(full)
+    tf = fl / (p_ms * 1e-3) / 1e12
+    out = {"value": tf, "unit": "TFLOP/s", "workload": "c3_prefill_llama70b (configs[2])", "n_gpus": world,
+           "scaling": "strong" if world > 1 else None, "ms_per_layer": p_ms, "per_rank_ms": per_rank,
+           "frac": tf / world / pk["bf16_tflops"], "peak": pk["bf16_tflops"], "peak_kind": "burst (measured)",
+           "frac_of_sustained": tf / world / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
+           "kernel": e3.selected_kernel(), "tile_q": int(e3.export_plan()[3]), "flops_per_layer": fl}
+    del L3, e3
+    torch.cuda.empty_cache()
+    if not args.no_fp8:  # the same prefill with an E4M3 KV cache (NEXT-2): gather pass + tcgen05 prefill
+        import dataclasses
+        L3f = Layered(dataclasses.replace(wl, kv_dtype="e4m3"), 2, dev, seed_base=1000 * rank)
+        e3f = L3f.engine(num_ctas=args.num_ctas, kernel=args.kernel, tile_q=args.prefill_tile)
+        pf_ms = max(gather_over_ranks(per_launch_ms(L3f, e3f, reps=3), world))
+        out["fp8_kv"] = {"ms_per_layer": pf_ms, "value": fl / (pf_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                         "kernel": e3f.selected_kernel(), "launches_per_run": e3f.last_launches(),
+                         "vs_bf16_kv": p_ms / pf_ms}
+        del L3f, e3f
+        torch.cuda.empty_cache()
+    return out
+
+
+def bench_scheduler(dev, pk, args):
+    """§8(d.6) scheduler fields on configs[1] (one layer): bsra_plan host time (median of 100 calls)
+    and plan + upload (plan, then a stream sync), the Algorithm-1 cost-model efficiency
+    (mean / makespan of per-CTA cost), and the balance ablation — the kernel-level analogue of the
+    paper's load-balancing study: Algorithm 1 (split KV, 148 persistent CTAs) vs the
+    same kernel without KV splitting (LPT over 148 CTAs) vs one (request, kv head) row per CTA
+    (non-persistent grid, the FA2-style baseline). Also for a configs[4] shard (4 x 64K tokens),
+    where splitting decides whether more than 32 CTAs have work."""
+    import dataclasses
+    out = {}
+    for key, wl in (("c2", synth.c2_decode_llama8b()),
+                    ("c5_shard_64k", dataclasses.replace(synth.c5_long_decode(kv_len=65536), name="c5_shard"))):
+        L = Layered(wl, 1, dev)
+        by = decode_bytes(wl)["total"]
+        rows = wl.batch * wl.H_kv
+        res = {}
+        for name, kw in (("algorithm1", dict(num_ctas=args.num_ctas)),
+                         ("no_split_lpt", dict(num_ctas=args.num_ctas, kv_chunk_min=1 << 30)),
+                         ("row_per_cta", dict(num_ctas=rows, kv_chunk_min=1 << 30))):
+            eng = L.engine(tile_q=16, kernel=args.kernel, **kw)
+            ms = per_launch_ms(L, eng, reps=5)
+            costs, mk = eng.plan_stats()
+            res[name] = {"us_per_launch": ms * 1e3, "TB/s": by / (ms * 1e-3) / 1e12,
+                         "frac": by / (ms * 1e-3) / 1e9 / pk["hbm_gbs"], "num_ctas": int(costs.size),
+                         "cost_model_efficiency": float(costs.mean() / mk) if mk else None}
+            if name == "algorithm1":
+                i = L.inp0
+                ts = []
+                for _ in range(100):
+                    t0 = time.perf_counter()
+                    eng.plan(i.qo_indptr, i.kv_page_indptr, i.kv_last_page_len, i.sm_scale)
+                    ts.append(time.perf_counter() - t0)
+                tu = []
+                st = torch.cuda.current_stream()
+                for _ in range(20):
+                    t0 = time.perf_counter()
+                    eng.plan(i.qo_indptr, i.kv_page_indptr, i.kv_last_page_len, i.sm_scale)
+                    st.synchronize()
+                    tu.append(time.perf_counter() - t0)
+                res[name]["plan_host_us_median"] = float(np.median(ts)) * 1e6
+                res[name]["plan_plus_upload_us_median"] = float(np.median(tu)) * 1e6
+                res[name]["plan_words"] = int(eng.export_plan().size)
+            del eng
+        res["speedup_vs_no_split"] = res["no_split_lpt"]["us_per_launch"] / res["algorithm1"]["us_per_launch"]
+        res["speedup_vs_row_per_cta"] = res["row_per_cta"]["us_per_launch"] / res["algorithm1"]["us_per_launch"]
+        out[key] = res
+        del L
+        torch.cuda.empty_cache()
+    return out
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_single_thread():
+    """§8(d.5): the oracle on ONE host thread for configs[0] (best of 3) and one full configs[1]
+    layer (one run)."""
+    import oracle
+    out = {}
+    c1 = synth.make_inputs(synth.c1_tiny_decode(), device="cpu")
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        oracle.paged_attention(**host_inputs(c1), num_threads=1)
+        ts.append(time.perf_counter() - t0)
+    out["c1_us"] = min(ts) * 1e6
+    c2 = synth.make_inputs(synth.c2_decode_llama8b(), device="cpu")
+    t0 = time.perf_counter()
+    oracle.paged_attention(**host_inputs(c2), num_threads=1)
+    el = time.perf_counter() - t0
+    out["c2_layer_s"] = el
+    out["c2_TB/s"] = decode_bytes(c2.wl)["total"] / el / 1e12
+    return out
+
+
 # -------------------------------------------------------------------- main ---
+def free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def maybe_relaunch(args):
+    """`bench.py --gpus N` without torchrun: re-launch this script under torchrun with N ranks
+    (one per GPU) and pass rank 0's JSON line through. Fails loudly if fewer GPUs are visible."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    if args.impl != "reference":
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+            sys.exit(2)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd, stdout=subprocess.PIPE)
+    _JSON_OUT.write(r.stdout.decode())
+    _JSON_OUT.flush()
+    sys.exit(r.returncode)
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -492,19 +724,32 @@ def dist_setup(args):
     return world, rank, local
 
 
-def max_over_ranks(x: float, world: int) -> float:
+def gather_over_ranks(x: float, world: int) -> list:
+    """Every rank's value (device-timed ms), rank order."""
     if world == 1:
-        return x
+        return [x]
     import torch.distributed as dist
-    t = torch.tensor([x], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    out = [None] * world
+    dist.all_gather_object(out, float(x))
+    return out
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    return max(gather_over_ranks(x, world))
 
 
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def headline_config(world, layers, num_ctas, graph):
+    return {"workload": "c2_decode_llama8b (BASELINE configs[1])", "model": "Llama-3-8B attention shape (32/8 heads, d 128)",
+            "global_batch": 128 * world, "seq_len": "kv 128-4096 ShareGPT-like (sum 151,721 per 128 requests), l_qo 1",
+            "page_size": 16, "layers_per_step": layers, "num_ctas": num_ctas,
+            "parallelism": f"requests sharded x{world} (data parallel, no collective)",
+            "l2": "inputs larger than L2 (621 MB KV per layer > 126 MB L2); no flush", "graph": graph}
 
 
 def run_reference(args, world, rank):
@@ -516,8 +761,8 @@ def run_reference(args, world, rank):
     hin = host_inputs(inp)
     import oracle
     threads = len(os.sched_getaffinity(0))
-    # each step = a bounded sample: the 16 longest... use a fixed request subset so K steps stay short
-    reqs = list(range(0, wl.batch, 4))  # 32 of 128 requests
+    # each step = a bounded sample of the workload: 32 of the 128 requests, one layer
+    reqs = list(range(0, wl.batch, 4))
     sub = synth.Workload(wl.name, wl.H_qo, wl.H_kv, wl.D, wl.page_size, wl.dtype, wl.mask, wl.qo_lens[reqs],
                          wl.kv_lens[reqs])
     by = decode_bytes(sub)["total"]
@@ -528,13 +773,14 @@ def run_reference(args, world, rank):
         oracle.paged_attention(**hin, req_list=reqs, num_threads=threads)
     el = (time.perf_counter() - t0) / args.steps
     val = by / el / 1e12
-    sample = f"requests 0,4,...,124 (32 of 128) of configs[1], one layer per step"
+    sample = "requests 0,4,...,124 (32 of 128) of configs[1], one layer per step"
     emit({
-        "impl": "reference", "metric": "paged decode HBM TB/s (configs[1], Llama-3-8B shape, batch 128)",
+        "impl": "reference", "metric": METRIC,
         "value": val, "unit": "TB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": "c2_decode_llama8b (sampled)", "global_batch": 32},
-        "cpu_baseline": {"value": val, "unit": "TB/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "data": "synthetic", "config": headline_config(world, 1, 0, False),
+        "cpu_baseline": {"value": val, "unit": "TB/s", "cores": threads, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": val, "unit": "TB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     })
 
@@ -557,12 +803,17 @@ def main():
     ap.add_argument("--no-contiguous", action="store_true", help="skip the paged-vs-contiguous KV line")
     ap.add_argument("--no-long", action="store_true")
     ap.add_argument("--no-fp8", action="store_true", help="skip the fp8 (E4M3) KV-cache decode line")
+    ap.add_argument("--no-sched", action="store_true", help="skip the scheduler / balance-ablation fields")
     ap.add_argument("--no-pdl", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    maybe_relaunch(args)
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
         return
     import paper_2501_01005_b200 as bsra
     bsra.lib()  # fail loudly if the extension is missing
@@ -573,7 +824,7 @@ def main():
     wl = synth.c2_decode_llama8b()
     L = Layered(wl, args.layers, dev, seed_base=1000 * rank)
     # consecutive layers are independent -> programmatic dependent launch between them
-    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel, pdl=not args.no_pdl)
+    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel, pdl=not args.no_pdl, max_qo_len=1)
     by = decode_bytes(wl)
     s, one_step, launches_per_step = time_device_steps(L, eng, args.steps, args.warmup, not args.no_graph)
     clk = ClockSampler(local)
@@ -589,7 +840,8 @@ def main():
     torch.cuda.synchronize()
     barrier(world)
     clocks = clk.stop()
-    ms = max_over_ranks(a.elapsed_time(b) / args.steps, world)
+    per_rank = gather_over_ranks(a.elapsed_time(b) / args.steps, world)
+    ms = max(per_rank)
     step_bytes = by["total"] * args.layers
     value = world * step_bytes / (ms * 1e-3) / 1e12
 
@@ -598,16 +850,20 @@ def main():
     launch_ms = per_launch_ms(L, eng)
     achieved = by["total"] / (launch_ms * 1e-3) / 1e9
     traffic = None
-    try:  # DRAM read+write per launch from the committed ncu --set full capture of this kernel
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
-            traffic = json.load(f)["tc_decode_kernel<4,0>"]["traffic_bytes"]
-    except Exception:
-        pass
+    traffic_src = None
+    for fn, key in (("r02_ncu_traffic.json", "tc_decode"), ("r01_ncu_traffic.json", "tc_decode_kernel<4,0>")):
+        try:  # DRAM read+write per launch from the committed ncu --set full capture of this kernel
+            with open(os.path.join(ROOT, "profiles", fn)) as f:
+                traffic = json.load(f)[key]["traffic_bytes"]
+            traffic_src = f"profiles/{fn} (ncu --set full, one launch)"
+            break
+        except Exception:
+            pass
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "peak_kind": pk_kind,
             "kernel": f"bsra {eng.selected_kernel()} (one launch per run(), contraction fused)",
             "algorithmic_bytes_per_launch": by["total"], "launch_ms": launch_ms,
-            "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, one launch)"}
+            "traffic_source": traffic_src}
 
     # ---- e2e through the public API with host buffers
     e2e = None
@@ -615,68 +871,47 @@ def main():
         e2e_ms, h2d, d2h = e2e_steps(L, eng, max(3, args.steps // 4), 2)
         e2e_ms = max_over_ranks(e2e_ms, world)
         e2e = {"value": world * step_bytes / (e2e_ms * 1e-3) / 1e12, "unit": "TB/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+               "how": "per step: plan() on host, then one graph replay of {H2D q[r] (copy stream) -> run(r) -> "
+                      "D2H o[r], lse[r] (copy stream)} for every layer r, copies overlapping other layers' kernels"}
+    del L, eng
+    torch.cuda.empty_cache()
+
+    # ---- secondary: configs[1] with the batch fixed and KV heads split over the ranks (N > 1)
+    head_sharded = None
+    if world > 1:
+        head_sharded = bench_decode_head_sharded(dev, pk, args, world, rank)
+        torch.cuda.empty_cache()
 
     # ---- secondary: the same decode step with an fp8 (E4M3) KV cache (NEXT-2)
     fp8 = None
     if not args.no_fp8:
-        del L
-        torch.cuda.empty_cache()
         fp8 = bench_fp8_decode(dev, pk, args, world, rank, ms)
         torch.cuda.empty_cache()
 
     # ---- secondary: configs[2] ragged causal prefill TFLOP/s (one layer, per-launch events)
     prefill = None
     if not args.no_prefill:
-        try:
-            del L
-        except NameError:
-            pass
+        prefill = bench_prefill(dev, pk, args, world, rank)
         torch.cuda.empty_cache()
-        wl3 = synth.c3_prefill_llama70b()
-        L3 = Layered(wl3, 2, dev, seed_base=1000 * rank)
-        e3 = L3.engine(num_ctas=148, kernel=args.kernel, tile_q=args.prefill_tile)
-        p_ms = per_launch_ms(L3, e3, reps=3)
-        fl = causal_flops(wl3)
-        tf = fl / (p_ms * 1e-3) / 1e12
-        prefill = {"value": tf, "unit": "TFLOP/s", "workload": "c3_prefill_llama70b (configs[2])",
-                   "ms_per_layer": p_ms, "frac": tf / pk["bf16_tflops"], "peak": pk["bf16_tflops"],
-                   "kernel": e3.selected_kernel(), "tile_q": int(e3.export_plan()[3]), "flops_per_layer": fl}
-        del L3
-        torch.cuda.empty_cache()
-        if not args.no_fp8:  # the same prefill with an E4M3 KV cache (NEXT-2): gather pass + tcgen05 prefill
-            import dataclasses
-            L3f = Layered(dataclasses.replace(wl3, kv_dtype="e4m3"), 2, dev, seed_base=1000 * rank)
-            e3f = L3f.engine(num_ctas=148, kernel=args.kernel, tile_q=args.prefill_tile)
-            pf_ms = per_launch_ms(L3f, e3f, reps=3)
-            prefill["fp8_kv"] = {"ms_per_layer": pf_ms, "value": fl / (pf_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
-                                 "kernel": e3f.selected_kernel(), "launches_per_run": e3f.last_launches(),
-                                 "vs_bf16_kv": p_ms / pf_ms}
-            del L3f
-            torch.cuda.empty_cache()
 
     composable = None
     if not args.no_composable:
-        try:
-            del L
-        except NameError:
-            pass
-        torch.cuda.empty_cache()
-        composable = bench_composable(dev, pk)
+        composable = bench_composable(dev, pk, world, rank)
         torch.cuda.empty_cache()
 
     contiguous = None
     if not args.no_contiguous and world == 1:
-        torch.cuda.empty_cache()
         contiguous = bench_contiguous(dev, pk)
+        torch.cuda.empty_cache()
+
+    sched = None
+    if not args.no_sched and world == 1:
+        sched = bench_scheduler(dev, pk, args)
+        torch.cuda.empty_cache()
 
     long_ctx = None
     if not args.no_long:
-        try:
-            del L
-        except NameError:
-            pass
-        torch.cuda.empty_cache()
         long_ctx = bench_long_context(dev, pk, world, rank, local)
         torch.cuda.empty_cache()
 
@@ -684,22 +919,20 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         inp_cpu = synth.make_inputs(wl, device="cpu")
         v, th, sample = oracle_cpu_baseline(wl, host_inputs(inp_cpu))
-        cpu = {"value": v, "unit": "TB/s", "cores": th, "kind": "oracle", "sample": sample}
+        cpu = {"value": v, "unit": "TB/s", "cores": th, "kind": "oracle", "sample": sample, "cpu_model": cpu_model(),
+               "single_thread": oracle_single_thread()}
 
     if rank == 0:
         out = {
-            "metric": "paged decode HBM TB/s (configs[1], Llama-3-8B shape, batch 128) & prefill TFLOP/s (configs[2])",
+            "metric": METRIC,
             "value": value, "unit": "TB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic",
-            "config": {"workload": "c2_decode_llama8b (BASELINE configs[1])", "global_batch": wl.batch * world,
-                       "layers_per_step": args.layers, "kv_tokens_per_layer": int(wl.kv_lens.sum()),
-                       "num_ctas": eng.cfg.num_ctas, "parallelism": f"requests sharded x{world}",
-                       "l2": "inputs larger than L2 (621 MB KV per layer > 126 MB L2); no flush",
-                       "graph": not args.no_graph},
+            "ms_per_step": ms, "per_rank_ms": per_rank, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": headline_config(world, args.layers, args.num_ctas, not args.no_graph),
             "frac_of_hbm_peak": value / world * 1e3 / pk["hbm_gbs"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "prefill": prefill,
-            "composable": composable, "long_context": long_ctx, "contiguous_kv": contiguous, "decode_fp8": fp8,
+            "decode_head_sharded": head_sharded, "composable": composable, "long_context": long_ctx,
+            "contiguous_kv": contiguous, "decode_fp8": fp8, "scheduler": sched,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         }
         emit(out)
