@@ -248,6 +248,34 @@ def head_slice(inp: Inputs, h0: int, h1: int) -> Inputs:
     return dataclasses.replace(inp, wl=wl2, q=q, k_pool=k, v_pool=v, k_strides=st, v_strides=st)
 
 
+def request_subset(inp: Inputs, reqs) -> Inputs:
+    """Requests `reqs` of `inp` as a self-contained Inputs (data movement only): their q rows, and
+    a compact pool holding exactly their pages in BSR order (so a check of a few requests of a
+    multi-GB workload copies only those pages to the host). Paged inputs, any layout."""
+    wl = inp.wl
+    reqs = [int(r) for r in reqs]
+    idx = inp.kv_page_indices
+    sel = torch.cat([idx[int(inp.kv_page_indptr[i]):int(inp.kv_page_indptr[i + 1])] for i in reqs]).long()
+    n = [int(inp.kv_page_indptr[i + 1] - inp.kv_page_indptr[i]) for i in reqs]
+    ip = np.concatenate([[0], np.cumsum(n)]).astype(np.int32)
+    qi = np.concatenate([[0], np.cumsum([int(wl.qo_lens[i]) for i in reqs])]).astype(np.int32)
+    q = torch.cat([inp.q[int(inp.qo_indptr[i]):int(inp.qo_indptr[i + 1])] for i in reqs])
+
+    def pages(pool, st):
+        npg = pool.numel() // max(1, st[0])
+        view = torch.as_strided(pool, (npg, st[0]), (st[0], 1))
+        return view[sel.to(pool.device)].contiguous().view(-1)
+
+    wl2 = dataclasses.replace(wl, qo_lens=wl.qo_lens[reqs].copy(), kv_lens=wl.kv_lens[reqs].copy())
+    cm, mbi = inp.custom_mask, inp.mask_bit_indptr
+    if cm is not None:
+        raise ValueError("request_subset: custom masks are not re-packed")
+    return dataclasses.replace(inp, wl=wl2, qo_indptr=qi, kv_page_indptr=ip,
+                               kv_last_page_len=inp.kv_last_page_len[reqs].copy(),
+                               kv_page_indices=torch.arange(len(sel), dtype=torch.int32, device=idx.device),
+                               q=q, k_pool=pages(inp.k_pool, inp.k_strides), v_pool=pages(inp.v_pool, inp.v_strides))
+
+
 @dataclasses.dataclass
 class RaggedKV:
     """The same keys / values as a paged Inputs, laid out contiguously:

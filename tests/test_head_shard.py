@@ -196,3 +196,15 @@ def test_small_head_sharded_all_rows(cuda_device):
     whole = oracle.attention_from_inputs(inp)
     for P in (1, 2, 3, 8):
         assert_close(_gpu_head_sharded(inp, P, num_ctas=37), whole, "bf16", what=f"P={P}")
+
+
+def test_request_subset_is_data_movement_only():
+    """synth.request_subset (used to check a few requests of multi-GB workloads) gives the oracle
+    exactly the rows of those requests (bitwise)."""
+    wl = synth.Workload("x", 8, 2, 32, 4, "bf16", "causal", np.array([2, 1, 3], np.int32),
+                        np.array([9, 40, 3], np.int32))
+    inp = synth.make_inputs(wl)
+    full = oracle.attention_from_inputs(inp)
+    sub = oracle.attention_from_inputs(synth.request_subset(inp, [1, 2]))
+    rows = rows_of_requests(inp, [1, 2])
+    assert np.array_equal(full[0][rows], sub[0]) and np.array_equal(full[1][rows], sub[1])
