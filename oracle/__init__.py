@@ -59,8 +59,10 @@ def _load():
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                             ctypes.c_double, ctypes.c_double, P, P, P, P, P,
                                             ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_double,
-                                            ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                             P, ctypes.c_int, P, P, ctypes.c_int]
+        lib.orc_rope_rotate.restype = None
+        lib.orc_rope_rotate.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double]
         lib.orc_merge.restype = None
         lib.orc_merge.argtypes = [ctypes.c_int64, ctypes.c_int, P, P, P, P, P, P]
         lib.orc_alibi_slope.restype = ctypes.c_double
@@ -100,13 +102,15 @@ def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indi
                     k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
                     mask_bit_indptr=None, sm_scale, window: int = 0, soft_cap: float = 0.0, alibi: bool = False,
                     kv_dtype: Optional[str] = None, k_scale: float = 1.0, v_scale: float = 1.0,
+                    rope_theta: float = 0.0, rope_scale: float = 1.0,
                     req_list: Optional[Sequence[int]] = None, num_threads: int = 0, out=None):
     """float64 oracle (C). Array arguments are host numpy arrays; ``q``/pools hold raw
     element bits (float32, uint16 bits for f16/bf16, uint8 bytes for e4m3 pools).
     ``kv_dtype`` (default: ``dtype``) is the pools' dtype; K/V values are scaled by
     ``k_scale`` / ``v_scale`` (the fp8 KV cache). Returns (o, lse) float64 with
     shapes [sum l_qo, H_qo, D] and [sum l_qo, H_qo]. With ``req_list`` only those requests
-    are computed (other rows stay NaN)."""
+    are computed (other rows stay NaN). ``rope_theta`` > 0 applies RoPE to q and k before the
+    logits (rotate-half pairs, positions: key t -> t, query row r -> l_kv - l_qo + r; R31)."""
     lib = _load()
     qo_indptr = np.ascontiguousarray(qo_indptr, np.int32)
     kv_page_indptr = np.ascontiguousarray(kv_page_indptr, np.int32)
@@ -131,7 +135,8 @@ def paged_attention(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indi
                                  _ptr(kv_page_indices), H_qo, H_kv, D, page_size, DT_CODE[dtype],
                                  DT_CODE[kv_dtype or dtype], float(k_scale), float(v_scale), _ptr(q),
                                  _ptr(k_pool), _ptr(v_pool), _ptr(ks), _ptr(vs), MASK_CODE[mask], _ptr(cm),
-                                 _ptr(mb), float(sm_scale), int(window), float(soft_cap), int(bool(alibi)), _ptr(rl),
+                                 _ptr(mb), float(sm_scale), int(window), float(soft_cap), int(bool(alibi)),
+                                 float(rope_theta), float(rope_scale), _ptr(rl),
                                  0 if rl is None else len(rl), _ptr(o),
                                  _ptr(lse), int(num_threads))
     if rc != 0:
@@ -151,7 +156,7 @@ def attention_from_inputs(inp, req_list=None, num_threads=0):
         custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
         mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap,
         alibi=wl.alibi, kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale,
-        req_list=req_list, num_threads=num_threads)
+        rope_theta=wl.rope_theta, rope_scale=wl.rope_scale, req_list=req_list, num_threads=num_threads)
 
 
 # ------------------------------------------------------------- brute force ---
@@ -183,12 +188,14 @@ def to_float64(bits: np.ndarray, dtype: str) -> np.ndarray:
 def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices, q, k_pool, v_pool,
                 k_strides, v_strides, H_qo, H_kv, D, page_size, dtype, mask="none", custom_mask=None,
                 mask_bit_indptr=None, sm_scale, window=0, soft_cap=0.0, alibi=False, kv_dtype=None, k_scale=1.0,
-                v_scale=1.0):
+                v_scale=1.0, rope_theta=0.0, rope_scale=1.0):
     """NumPy brute force (tiny inputs): dense un-paged K/V per request, the full masked
     score matrix, float64 softmax. Same definition as the C oracle, different code.
     fp8 KV: pools of ``kv_dtype`` scaled by k_scale / v_scale.
     Variants (PAPER.md:228): window W > 0 keeps keys t >= l_kv - l_qo + r - W + 1 (R26);
-    soft_cap c > 0 maps the scaled scores through c * tanh(S / c) (R27)."""
+    soft_cap c > 0 maps the scaled scores through c * tanh(S / c) (R27).
+    RoPE (R31), written in complex form (different code from the C oracle's real rotation): the
+    pair (x_i, x_{i+D/2}) is the complex number x_i + j x_{i+D/2}, multiplied by e^{j pos theta_i}."""
     qf = to_float64(q, dtype).reshape(-1, H_qo, D)
     kflat = k_scale * to_float64(k_pool, kv_dtype or dtype).reshape(-1)
     vflat = v_scale * to_float64(v_pool, kv_dtype or dtype).reshape(-1)
@@ -219,7 +226,11 @@ def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices,
         Vd = vflat[vidx]
         Kr = np.repeat(Kd, g, axis=1)  # GQA: head h uses kv head h // g
         Vr = np.repeat(Vd, g, axis=1)
-        S = sm_scale * np.einsum("rhd,thd->hrt", qf[q0:q1], Kr)  # [H, lq, lk]
+        Q = qf[q0:q1]
+        if rope_theta > 0:
+            Q = rope_complex(Q, lk - lq + np.arange(lq), rope_theta, rope_scale)
+            Kr = rope_complex(Kr, np.arange(lk), rope_theta, rope_scale)
+        S = sm_scale * np.einsum("rhd,thd->hrt", Q, Kr)  # [H, lq, lk]
         if soft_cap > 0:
             S = soft_cap * np.tanh(S / soft_cap)
         if alibi:  # slope_h * (t - p), p = l_kv - l_qo + r (R30)
@@ -247,6 +258,24 @@ def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices,
     return o, lse
 
 
+def rope_complex(x, pos, rope_theta, rope_scale=1.0):
+    """RoPE as a complex rotation: x [n, H, D] real with positions pos [n]; z_i = x_i + j x_{i+D/2}
+    times e^{j pos theta_i}, theta_i = rope_theta^(-2i/D) / rope_scale (R31)."""
+    D = x.shape[-1]
+    h = D // 2
+    theta = np.power(float(rope_theta), -2.0 * np.arange(h) / D) / rope_scale
+    z = x[..., :h] + 1j * x[..., h:]
+    z = z * np.exp(1j * np.asarray(pos, np.float64)[:, None, None] * theta[None, None, :])
+    return np.concatenate([z.real, z.imag], axis=-1)
+
+
+def rope_rotate(x, pos, rope_theta, rope_scale=1.0):
+    """The C oracle's RoPE rotation of one vector (float64), for the closed-form pins."""
+    x = np.ascontiguousarray(x, np.float64).copy()
+    _load().orc_rope_rotate(_ptr(x), x.size, float(pos), float(rope_theta), float(rope_scale))
+    return x
+
+
 def brute_force_from_inputs(inp):
     from synth import raw_bits
     wl = inp.wl
@@ -257,7 +286,8 @@ def brute_force_from_inputs(inp):
         H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype, mask=wl.mask,
         custom_mask=None if inp.custom_mask is None else inp.custom_mask.cpu().numpy(),
         mask_bit_indptr=inp.mask_bit_indptr, sm_scale=inp.sm_scale, window=wl.window, soft_cap=wl.soft_cap,
-        alibi=wl.alibi, kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale)
+        alibi=wl.alibi, kv_dtype=wl.kv_dtype or wl.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale,
+        rope_theta=wl.rope_theta, rope_scale=wl.rope_scale)
 
 
 # --------------------------------------------------------------------- ⊕ ---

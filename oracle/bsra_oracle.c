@@ -103,6 +103,22 @@ static double orc_load(const void* base, int dtype, int64_t idx) {
 
 int orc_version(void) { return 1; }
 
+/* RoPE (Su et al., "RoFormer"; the paper's Query/KeyTransform, "fuse ... RoPE"),
+ * rotate-half pairing (R31): for i < D/2, theta_i = rope_theta^(-2i/D) / rope_scale and
+ * angle a = pos * theta_i (float64, exact positions); the pair (x_i, x_{i+D/2}) becomes
+ * (x_i cos a - x_{i+D/2} sin a, x_{i+D/2} cos a + x_i sin a). In place. */
+void orc_rope_rotate(double* x, int D, double pos, double rope_theta, double rope_scale) {
+  const int h = D / 2;
+  for (int i = 0; i < h; ++i) {
+    const double theta = pow(rope_theta, -2.0 * i / D) / rope_scale;
+    const double a = pos * theta;
+    const double c = cos(a), sn = sin(a);
+    const double x0 = x[i], x1 = x[i + h];
+    x[i] = x0 * c - x1 * sn;
+    x[i + h] = x1 * c + x0 * sn;
+  }
+}
+
 /* ALiBi slope of qo head h of H (Press et al. 2022; R30). */
 double orc_alibi_slope(int h, int H) {
   int n = 1;
@@ -138,10 +154,12 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
                         const void* k_pool, const void* v_pool, const int64_t* k_strides,
                         const int64_t* v_strides, int mask_mode, const uint8_t* custom_mask,
                         const int64_t* mask_bit_indptr, double sm_scale, int window, double soft_cap, int alibi,
+                        double rope_theta, double rope_scale,
                         const int32_t* req_list, int n_req_list, double* o_out, double* lse_out,
                         int num_threads) {
   if (batch < 0 || H_qo <= 0 || H_kv <= 0 || H_qo % H_kv != 0 || D <= 0 || page_size <= 0) return 1;
   if (mask_mode == ORC_MASK_CUSTOM && (!custom_mask || !mask_bit_indptr)) return 2;
+  if (rope_theta > 0.0 && (D % 2 != 0 || !(rope_scale > 0.0))) return 5;
   const int g = H_qo / H_kv;
   const int nreq = req_list ? n_req_list : batch;
 
@@ -172,6 +190,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
     double* s = NULL;   /* scores of visible tokens, logical order */
     int32_t* vis = NULL; /* visible token ids */
     int64_t cap = 0;
+    double qr[1024], kr[1024]; /* RoPE-rotated q row / k row (D <= 1024) */
 #pragma omp for schedule(dynamic, 1)
     for (int64_t wi = 0; wi < nwork; ++wi) {
       const int i = (int)work[2 * wi];
@@ -215,6 +234,10 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
           continue;
         }
         const int64_t qbase = (row * H_qo + h) * (int64_t)D;
+        if (rope_theta > 0.0) { /* QueryTransform: the query row sits at position l_kv - l_qo + r */
+          for (int d = 0; d < D; ++d) qr[d] = orc_load(q, dtype, qbase + d);
+          orc_rope_rotate(qr, D, (double)(l_kv - l_qo + r), rope_theta, rope_scale);
+        }
         /* pass 1: scores and their max */
         double m = -INFINITY;
         for (int64_t a = 0; a < nv; ++a) {
@@ -222,6 +245,11 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
           const int64_t p = kv_page_indices[kv_page_indptr[i] + t / page_size];
           const int64_t kb = p * k_strides[0] + (t % page_size) * k_strides[1] + hk * k_strides[2];
           double dot = 0.0;
+          if (rope_theta > 0.0) { /* KeyTransform: key t sits at position t */
+            for (int d = 0; d < D; ++d) kr[d] = k_scale * orc_load(k_pool, kv_dtype, kb + d);
+            orc_rope_rotate(kr, D, (double)t, rope_theta, rope_scale);
+            for (int d = 0; d < D; ++d) dot += qr[d] * kr[d];
+          } else
           for (int d = 0; d < D; ++d) dot += orc_load(q, dtype, qbase + d) * (k_scale * orc_load(k_pool, kv_dtype, kb + d));
           s[a] = sm_scale * dot;
           if (soft_cap > 0.0) s[a] = soft_cap * tanh(s[a] / soft_cap);

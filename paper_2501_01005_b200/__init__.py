@@ -378,33 +378,50 @@ class Dist:
 class ComposableDecode:
     """Composable formats: the KV of n branches that share a prefix is
     described as two BSR matrices over one pool — a shared-prefix block read once for all n
-    query rows (large B_r: one "request" with l_qo = n, tensor-core tile) and per-branch suffix
-    blocks (B_r = 1) — one engine ("wrapper") each; the two attention states are combined with
-    ⊕ (bsra_merge_states). Three C-ABI launches per layer, all graph-capturable."""
+    query rows (large B_r: one "request" with l_qo = n, tensor-core tile; with g = 4 and n = 64
+    the 256 fused rows are one paired 256-row tile, so every prefix K/V tile staged in shared
+    memory serves all branches) and per-branch suffix blocks (B_r = 1) — one engine ("wrapper")
+    each; the two attention states are combined with ⊕ (bsra_merge_states).
+
+    concurrent: the two engines run at the same time on disjoint SM sets — the prefix engine's
+    persistent grid takes `prefix_ctas` SMs (tensor-bound tiles), the suffix engine the other
+    `suffix_ctas` (HBM-bound) — forked on a side stream and joined before the ⊕, so the prefix's
+    tensor work overlaps the suffix's HBM streaming (the joint plan of SURVEY §8(f) NEXT-4 as two
+    co-resident persistent grids). All launches are graph-capturable."""
 
     def __init__(self, *, H_qo, H_kv, D, page_size, n_branch, dtype="bf16", device=0, prefix_ctas=0,
-                 suffix_ctas=0, kernel="auto"):
+                 suffix_ctas=0, kernel="auto", prefix_tiles=(64, 128, 256), balance=True, concurrent=False,
+                 pdl=False):
         self.n, self.H_qo, self.D = n_branch, H_qo, D
+        self.concurrent = concurrent
         self.prefix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
                                          max_batch=1, max_total_qo_rows=n_branch, num_ctas=prefix_ctas,
-                                         tile_set=(64, 128), kernel=kernel), device)
+                                         tile_set=prefix_tiles, kernel=kernel, balance_ctas=balance, pdl=pdl), device)
         self.suffix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
                                          max_batch=n_branch, max_total_qo_rows=n_branch, num_ctas=suffix_ctas,
-                                         tile_q=16, kernel=kernel), device)
+                                         tile_q=16, kernel=kernel, max_qo_len=1, pdl=pdl), device)
         dev = f"cuda:{device}"
         self.o_p = torch.empty((n_branch, H_qo, D), device=dev)
         self.l_p = torch.empty((n_branch, H_qo), device=dev)
         self.o_s = torch.empty((n_branch, H_qo, D), device=dev)
         self.l_s = torch.empty((n_branch, H_qo), device=dev)
+        self.side = torch.cuda.Stream(device=dev) if concurrent else None
 
     def plan(self, prefix: dict, suffix: dict, sm_scale=0.0, stream=None):
         self.prefix.plan(prefix["qo_indptr"], prefix["kv_page_indptr"], prefix["kv_last_page_len"], sm_scale, stream)
         self.suffix.plan(suffix["qo_indptr"], suffix["kv_page_indptr"], suffix["kv_last_page_len"], sm_scale, stream)
 
     def run(self, q, k_pool, v_pool, strides, prefix_indices, suffix_indices, o, lse=None, stream=None):
-        self.prefix.run(q, k_pool, v_pool, strides, strides, prefix_indices, self.o_p, self.l_p, stream=stream)
-        self.suffix.run(q, k_pool, v_pool, strides, strides, suffix_indices, self.o_s, self.l_s, stream=stream)
-        merge_states(self.o_p, self.l_p, self.o_s, self.l_s, o_out=o, lse_out=lse, stream=stream)
+        st = stream if stream is not None else torch.cuda.current_stream()
+        if self.concurrent:
+            self.side.wait_stream(st)
+            self.prefix.run(q, k_pool, v_pool, strides, strides, prefix_indices, self.o_p, self.l_p, stream=self.side)
+            self.suffix.run(q, k_pool, v_pool, strides, strides, suffix_indices, self.o_s, self.l_s, stream=st)
+            st.wait_stream(self.side)
+        else:
+            self.prefix.run(q, k_pool, v_pool, strides, strides, prefix_indices, self.o_p, self.l_p, stream=st)
+            self.suffix.run(q, k_pool, v_pool, strides, strides, suffix_indices, self.o_s, self.l_s, stream=st)
+        merge_states(self.o_p, self.l_p, self.o_s, self.l_s, o_out=o, lse_out=lse, stream=st)
         return o, lse
 
     def launches(self) -> int:

@@ -288,7 +288,9 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
           D.tok0 = ctok0[k];
         }
         if (kq == k) D.page[j] = page;
-        __syncwarp();
+        // bar.sync (not __syncwarp): orders every lane's descriptor writes before lane 0's arrive
+        // in a form compute-sanitizer's racecheck tracks through the mbarrier hand-off
+        ptx::named_bar_sync(6, 32);
         if (lane == 0) ptx::mbar_arrive(&desc_full[slot]);
         if (lane == 0) BSRA_TRACE(10, pos);
         ++pos;
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         }
       }
       if (isK && (D.flags & 1)) qphase ^= kPair ? 3u : (1u << D.w);
-      __syncwarp();
+      ptx::named_bar_sync(3 + warp, 32);  // every lane's descriptor reads precede the release
       if (lane == 0) ptx::mbar_arrive(&desc_empty[slot]);  // descriptor fields are in registers
       if (lane == 0) {
         ptx::mbar_wait(&emptyx[stage], ephase);
@@ -467,6 +469,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         issue_pv(1, vst, flags & 1);
         ptx::mma_commit_warp(&empty_v[vst]);
         if (flags & 2) ptx::mma_commit_warp(&bar_o[1]);
+        ptx::named_bar_sync(5, 32);  // all lanes' descriptor reads precede the release
         ptx::mbar_arrive_warp(&desc_empty[slot]);
         if (++vst == kVStages) {
           vst = 0;
@@ -536,6 +539,7 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
         issue_pv(w, vst, flags & 1);
         ptx::mma_commit_warp(&empty_v[vst]);
         if (flags & 2) ptx::mma_commit_warp(&bar_o[w]);
+        ptx::named_bar_sync(5, 32);  // all lanes' descriptor reads precede the release
         ptx::mbar_arrive_warp(&desc_empty[slot]);
         if (++vst == kVStages) {
           vst = 0;

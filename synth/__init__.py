@@ -51,6 +51,8 @@ class Workload:
     soft_cap: float = 0.0  # logits soft-cap c (0 = off), R27
     kv_dtype: str = ""     # "" = dtype; "e4m3" = fp8 KV cache with fp16/bf16 q and o (R28)
     alibi: bool = False    # ALiBi bias (R30)
+    rope_theta: float = 0.0  # RoPE base (0 = off), R31
+    rope_scale: float = 1.0  # RoPE position interpolation factor
 
     @property
     def batch(self) -> int:
