@@ -649,6 +649,41 @@ def bench_scheduler(dev, pk, args):
     return out
 
 
+def bench_quest(dev, pk):
+    """SURVEY §8(f) NEXT-4 Quest workload: fine-grained block-sparse decode,
+    block 16, 32/32 heads, d 128, batch 1; each head keeps `page_budget` pages of its seq_len/16
+    (synth.quest_decode). Per-launch latency (median of 9, CUDA events) through the decode
+    kernel; the paper's H100 latencies quoted as context, not as a target."""
+    paper_h100_us = {(4096, 64): 20.299, (4096, 256): 44.383, (32768, 64): 22.371, (32768, 512): 68.478}
+    out = {"unit": "us per launch", "paper": "FlashInfer on H100 SXM5, Table eval-sparsity-flashinfer"}
+    for (S, P), ref in paper_h100_us.items():
+        wl, extra = synth.quest_decode(S, P)
+        inp = synth.make_inputs(wl, device=dev, extra_pages=extra)
+        import paper_2501_01005_b200 as bsra
+        cfg = bsra.make_config(H_qo=1, H_kv=1, D=128, page_size=16, dtype="bf16", max_batch=wl.batch,
+                               max_total_qo_rows=wl.batch, num_ctas=148, tile_q=16, max_qo_len=1)
+        e = bsra.Engine(cfg, torch.cuda.current_device())
+        o = torch.empty((wl.batch, 1, 128), device=dev, dtype=torch.bfloat16)
+        lse = torch.empty((wl.batch, 1), device=dev)
+        e.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+        ts = []
+        for k in range(12):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            e.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse)
+            b.record()
+            torch.cuda.synchronize()
+            if k >= 3:
+                ts.append(a.elapsed_time(b))
+        us = float(np.median(ts)) * 1e3
+        by = decode_bytes(wl)["total"]
+        out[f"seq{S}_budget{P}"] = {"us": us, "TB/s": by / (us * 1e-6) / 1e12, "bytes": by,
+                                    "paper_h100_us": ref, "kernel": e.selected_kernel()}
+        del inp, e
+        torch.cuda.empty_cache()
+    return out
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -805,6 +840,7 @@ def main():
     ap.add_argument("--no-fp8", action="store_true", help="skip the fp8 (E4M3) KV-cache decode line")
     ap.add_argument("--no-sched", action="store_true", help="skip the scheduler / balance-ablation fields")
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--no-quest", action="store_true", help="skip the Quest block-sparse decode line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     maybe_relaunch(args)
@@ -910,6 +946,11 @@ def main():
         sched = bench_scheduler(dev, pk, args)
         torch.cuda.empty_cache()
 
+    quest = None
+    if not args.no_quest and world == 1:
+        quest = bench_quest(dev, pk)
+        torch.cuda.empty_cache()
+
     long_ctx = None
     if not args.no_long:
         long_ctx = bench_long_context(dev, pk, world, rank, local)
@@ -932,7 +973,7 @@ def main():
             "frac_of_hbm_peak": value / world * 1e3 / pk["hbm_gbs"],
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "prefill": prefill,
             "decode_head_sharded": head_sharded, "composable": composable, "long_context": long_ctx,
-            "contiguous_kv": contiguous, "decode_fp8": fp8, "scheduler": sched,
+            "contiguous_kv": contiguous, "decode_fp8": fp8, "scheduler": sched, "quest": quest,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         }
         emit(out)

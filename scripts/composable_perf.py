@@ -24,14 +24,15 @@ def graph_ms(fn, s, reps=20):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         fn()
-    for _ in range(3):
-        g.replay()
-    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(s)
-    for _ in range(reps):
-        g.replay()
-    b.record(s)
+    with torch.cuda.stream(s):  # replay() launches on the current stream
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        a.record(s)
+        for _ in range(reps):
+            g.replay()
+        b.record(s)
     torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
 

@@ -92,6 +92,22 @@ def c3_prefill_llama70b(batch: int = 16, seed: int = SEED_LEN, mask: str = "caus
     return Workload("c3_prefill_llama70b", 64, 8, 128, 16, "bf16", mask, qo, qo.copy())
 
 
+def quest_decode(seq_len: int = 32768, page_budget: int = 512, batch: int = 1, heads: int = 32):
+    """Quest fine-grained block-sparse decode (tables eval-sparsity-*): block
+    size 16, 32 qo / 32 kv heads, head_dim 128. Quest keeps `page_budget` of each head's
+    seq_len/16 pages (query-aware, per head), so every (request, head) is its own BSR row over
+    the heads' common pool: a workload of batch*heads single-head "requests" (H_qo = H_kv = 1),
+    each with page_budget pages drawn from a pool of batch*heads*seq_len/16 pages (the full
+    cache). Returns (workload, extra_pages) for make_inputs(extra_pages=...). Page selection
+    itself (Quest's criticality estimate) is out of scope: the kept pages are a seeded random
+    subset, which gives the scattered gather the kernel sees."""
+    n = batch * heads
+    budget = min(page_budget, seq_len // 16)
+    wl = Workload(f"quest_{seq_len}_{budget}", 1, 1, 128, 16, "bf16", "none", np.ones(n, np.int32),
+                  np.full(n, budget * 16, np.int32))
+    return wl, n * (seq_len // 16) - n * budget
+
+
 def c5_long_decode(batch: int = 4, kv_len: int = 524288) -> Workload:
     """BASELINE.json configs[4]: long-context decode, 32/8 heads, d 128, page 16, kv 512K."""
     return Workload("c5_long_decode", 32, 8, 128, 16, "bf16", "none",

@@ -118,3 +118,23 @@ def test_headline_graph_four_layers(cuda_device):
         eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o2, l2)
         torch.cuda.synchronize()
         assert torch.equal(o2, o) and torch.equal(l2, lse), f"layer {r}: graph replay != eager run"
+
+
+@pytest.mark.parametrize("S,P", [(4096, 64), (32768, 512)])
+def test_quest_block_sparse_decode(cuda_device, S, P):
+    """Quest workload: 32 single-head rows, each over `P` scattered pages of a
+    32 x S/16-page pool, through the decode kernel as the bench runs it; sampled rows vs oracle."""
+    wl, extra = synth.quest_decode(S, P)
+    inp = synth.make_inputs(wl, device=cuda_device, extra_pages=extra)
+    cfg = bsra.make_config(H_qo=1, H_kv=1, D=128, page_size=16, dtype="bf16", max_batch=wl.batch,
+                           max_total_qo_rows=wl.batch, num_ctas=148, tile_q=16, max_qo_len=1)
+    eng = bsra.Engine(cfg, 0)
+    o = torch.full((wl.batch, 1, 128), float("nan"), device=cuda_device, dtype=torch.bfloat16)
+    lse = torch.full((wl.batch, 1), float("nan"), device=cuda_device)
+    eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+    eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse)
+    torch.cuda.synchronize()
+    assert eng.selected_kernel() == "tc_decode"
+    reqs = [0, 13, 31]
+    ref = oracle.attention_from_inputs(synth.request_subset(inp, reqs))
+    assert_close((o[reqs].float().cpu().numpy(), lse[reqs].cpu().numpy()), ref, "bf16", what=f"quest {S}/{P}")
