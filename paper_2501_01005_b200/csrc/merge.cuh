@@ -92,28 +92,33 @@ __device__ __forceinline__ void fused_contraction(const AttnParams& p, const Pla
       for (int j = 0; j < kPer; ++j) acc[j] = 0.f;
       float tot = 0.f;
       if (m != -INFINITY) {
-        for (int s = s0; s < s1; ++s) {
-          const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
-          const float w = __expf(__ldcg(p.part_lse + prow) - m);  // 0 for an empty partial
-          tot += w;
-          if constexpr (kPer % 4 == 0) {
-            const float4* src = reinterpret_cast<const float4*>(p.part_o + prow * D + lane * kPer);
+        for (int sb = s0; sb < s1; sb += 8) {
+          float v[8][kPer], wt[8];
 #pragma unroll
-            for (int j = 0; j < kPer / 4; ++j) {
-              const float4 v = __ldcg(src + j);
-              acc[4 * j] = fmaf(w, v.x, acc[4 * j]);
-              acc[4 * j + 1] = fmaf(w, v.y, acc[4 * j + 1]);
-              acc[4 * j + 2] = fmaf(w, v.z, acc[4 * j + 2]);
-              acc[4 * j + 3] = fmaf(w, v.w, acc[4 * j + 3]);
+          for (int u = 0; u < 8; ++u) {  // the group's loads first (8 rows in flight) ...
+            const int s = sb + u;
+            wt[u] = 0.f;
+            if (s < s1) {
+              const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
+              wt[u] = __expf(__ldcg(p.part_lse + prow) - m);  // 0 for an empty partial
+              const float* src = p.part_o + prow * D + lane * kPer;
+#pragma unroll
+              for (int j = 0; j < kPer; ++j) v[u][j] = __ldcg(src + j);
             }
-          } else {
-            const float* src = p.part_o + prow * D + lane * kPer;
+          }
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) acc[j] = fmaf(w, __ldcg(src + j), acc[j]);
+          for (int u = 0; u < 8; ++u) {  // ... then the fold in slot order
+            if (sb + u < s1) {
+              tot += wt[u];
+#pragma unroll
+              for (int j = 0; j < kPer; ++j) acc[j] = fmaf(wt[u], v[u][j], acc[j]);
+            }
           }
         }
       }
       const float inv = tot > 0.f ? 1.f / tot : 0.f;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) acc[j] *= inv;
       const float lse = tot > 0.f ? m + __logf(tot) : -INFINITY;
       const int f = qt * pv.T_q + r;
       const int tok = f / p.g, head = kvh * p.g + f % p.g;
@@ -121,11 +126,11 @@ __device__ __forceinline__ void fused_contraction(const AttnParams& p, const Pla
       if (p.o_f32) {
         float* dst = reinterpret_cast<float*>(p.o) + orow * D + lane * kPer;
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) dst[j] = acc[j] * inv;
+        for (int j = 0; j < kPer; ++j) dst[j] = acc[j];
       } else {
         TO* dst = reinterpret_cast<TO*>(p.o) + orow * D + lane * kPer;
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) dst[j] = from_float<TO>(acc[j] * inv);
+        for (int j = 0; j < kPer; ++j) dst[j] = from_float<TO>(acc[j]);
       }
       if (p.lse && lane == 0) p.lse[orow] = lse;
     }
@@ -133,8 +138,12 @@ __device__ __forceinline__ void fused_contraction(const AttnParams& p, const Pla
   asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");  // s_flag reuse
 }
 
-// Standalone contraction (engines whose tiles can be 64/128 rows, where a merge list is too big
-// for the one CTA that completes it): one warp per (list, row), left fold in plan order.
+// Standalone contraction (engines whose tiles can be 64/128/256 rows, where a merge list is too
+// big for the one CTA that completes it): one warp per (list, row). Same closed form and the same
+// operation order as fused_contraction (so the two placements are bitwise identical): the lanes
+// read the slots' lse in parallel, form m = max and the weights w_s = e^{lse_s - m}; then the
+// slots' rows are accumulated in plan order (R17) with 8 independent row loads in flight per
+// warp (a dependent ⊕ chain would leave one load in flight and make the stage latency-bound).
 template <typename TO, int D>
 __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant__ AttnParams p) {
   constexpr int kPer = D / 32;
@@ -149,20 +158,46 @@ __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant_
     const int f = qt * pv.T_q + r;
     if (f >= lq * p.g) continue;
     const int tok = f / p.g, head = kvh * p.g + f % p.g;
-    float acc[kPer], acc_lse = -INFINITY;
+    const int s0 = pv.list_indptr[li], s1 = pv.list_indptr[li + 1];
+    float m = -INFINITY;
+    for (int s = s0 + lane; s < s1; s += 32) m = fmaxf(m, p.part_lse[(int64_t)pv.list_slot[s] * p.T_slot + r]);
+    m = warp_max(m);
+    float acc[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) acc[j] = 0.f;
-    for (int s = pv.list_indptr[li]; s < pv.list_indptr[li + 1]; ++s) {
-      const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
-      float o[kPer];
-      const float* src = p.part_o + prow * D + lane * kPer;
+    float tot = 0.f;
+    if (m != -INFINITY) {
+      for (int sb = s0; sb < s1; sb += 8) {
+        float v[8][kPer], wt[8];
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) o[j] = src[j];
-      oplus<kPer>(acc, acc_lse, o, p.part_lse[prow]);
+        for (int u = 0; u < 8; ++u) {  // issue the group's loads first
+          const int s = sb + u;
+          wt[u] = 0.f;
+          if (s < s1) {
+            const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
+            wt[u] = __expf(p.part_lse[prow] - m);  // 0 for an empty partial
+            const float* src = p.part_o + prow * D + lane * kPer;
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) v[u][j] = src[j];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // then accumulate in slot order
+          if (sb + u < s1) {
+            tot += wt[u];
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) acc[j] = fmaf(wt[u], v[u][j], acc[j]);
+          }
+        }
+      }
     }
+    const float inv = tot > 0.f ? 1.f / tot : 0.f;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) acc[j] *= inv;
+    const float lse = tot > 0.f ? m + __logf(tot) : -INFINITY;
     const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
     store_row<TO, D>(p.o, orow, lane, acc, p.o_f32);
-    if (p.lse && lane == 0) p.lse[orow] = acc_lse;
+    if (p.lse && lane == 0) p.lse[orow] = lse;
   }
 }
 

@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   uint64_t* o_free = p_full + 2;         // [2] epilogue read O^T buffer b (1 arrival)
   uint64_t* epi_full = o_free + 2;       // [2] item's row sums / max handed to the epilogue (4 warps)
   uint64_t* epi_empty = epi_full + 2;    // [2] epilogue consumed hand-off buffer b (1 arrival)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_empty + 2);
+  uint64_t* o_full = epi_empty + 2;      // [2] the item's last PV into O^T buffer b completed (commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [4 warps][kN]
   int* vflags = reinterpret_cast<int*>(red + 4 * kN);     // [2][4] vote flags
   float* hsum = reinterpret_cast<float*>(vflags + 8);      // [2][4 warps][kN] row-sum partials
@@ -161,6 +162,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       ptx::mbar_init(&o_free[b], 1);
       ptx::mbar_init(&epi_full[b], 4);
       ptx::mbar_init(&epi_empty[b], 1);
+      ptx::mbar_init(&o_full[b], 1);
     }
     ptx::fence_barrier_init();
   }
@@ -243,8 +245,10 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     }
   } else if (warp == 5) {
     // ================================ MMA issuer ================================
-    // S^T(t) as soon as K(t) landed and the softmax has read the S^T buffer; PV(t-1) once P(t-1)
-    // is written: the MMA issue latency stays off the softmax chain.
+    // One flat stream of tiles across the CTA's items: S(k) as soon as K(k) landed and the softmax
+    // has read the S^T buffer, then PV(k-1) once P(k-1) is written. At an item boundary the next
+    // item's first S is issued BEFORE the previous item's last PV, so the softmax warps go on to
+    // the next item while that PV runs (the epilogue waits for it through o_full).
     const uint32_t fmt = kF16 ? 0u : 1u;
     const uint32_t idS = ptx::idesc_f16(fmt, 128, kN, 0, 0);  // A = K (K-major), B = Q (K-major)
     const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
@@ -253,20 +257,29 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     uint32_t fphase = 0;
     uint32_t ofph[2] = {1, 1};
     uint32_t sfph[2] = {1, 1}, pfph[2] = {0, 0}, qphase[2] = {0, 0};
-    auto issue_pv = [&](int ti, int st) {  // PV of the item's tile ti, staged in ring stage st
+    struct PendingPV {
+      int st, ti, ob;
+      bool last, valid;
+    } pend = {0, 0, 0, false, false};
+    auto issue_pv = [&](const PendingPV& x) {  // PV of tile x.ti of an item, staged in ring stage x.st
       ptx::mbar_wait(&p_full[pb], pfph[pb]);
       pfph[pb] ^= 1;
+      if (x.ti == 0) {  // the item's first PV overwrites O[ob]: the epilogue two items back read it
+        ptx::mbar_wait(&o_free[x.ob], ofph[x.ob]);
+        ofph[x.ob] ^= 1;
+      }
       ptx::tc_fence_after();
-      const uint64_t a0 = ptx::smem_desc_sw128(sbase + st * kStageBytes + kKVBytes, kHalfBytes, 1024);
+      const uint64_t a0 = ptx::smem_desc_sw128(sbase + x.st * kStageBytes + kKVBytes, kHalfBytes, 1024);
       const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffP + pb * kPBytes, 16, 1024);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t sbo = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
-        ptx::mma_f16_ss_warp(tmem + 32 + ob * 16, a0 + (uint64_t)(kk * 128), b0 + sbo, idO,
-                             (ti > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_f16_ss_warp(tmem + 32 + x.ob * 16, a0 + (uint64_t)(kk * 128), b0 + sbo, idO,
+                             (x.ti > 0 || kk > 0) ? 1u : 0u);
       }
-      ptx::mma_commit_warp(&empty[st]);  // K/V stage free once these MMAs complete
+      ptx::mma_commit_warp(&empty[x.st]);  // K/V stage free once these MMAs complete
       ptx::mma_commit_warp(&bar_pv[pb]);
+      if (x.last) ptx::mma_commit_warp(&o_full[x.ob]);  // O[ob] final: the epilogue may read it
       pb ^= 1;
     };
     for (int it = it0; it < it1; ++it) {
@@ -279,7 +292,6 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         continue;
       }
       const uint64_t bq = ptx::smem_desc_sw128(sbase + kOffQ + qb * kQBytes, 16, 1024);
-      int pstage = 0;
       for (int ti = 0; ti < d.ntiles; ++ti) {
         ptx::mbar_wait(&full[stage], fphase);
         ptx::mbar_wait(&s_free[sb], sfph[sb]);
@@ -295,22 +307,17 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
         ptx::mma_commit_warp(&bar_s[sb]);
         if (ti + 1 == d.ntiles) ptx::mma_commit_warp(&empty_q[qb]);  // last reader of this Q buffer
         sb ^= 1;
-        if (ti == 0) {  // the item's first PV overwrites O[ob]: the epilogue two items back read it
-          ptx::mbar_wait(&o_free[ob], ofph[ob]);
-          ofph[ob] ^= 1;
-        } else {
-          issue_pv(ti - 1, pstage);
-        }
-        pstage = stage;
+        if (pend.valid) issue_pv(pend);
+        pend = {stage, ti, ob, ti + 1 == d.ntiles, true};
         if (++stage == kStages) {
           stage = 0;
           fphase ^= 1;
         }
       }
-      issue_pv(d.ntiles - 1, pstage);
       qb ^= 1;
       ob ^= 1;
     }
+    if (pend.valid) issue_pv(pend);
   } else if (warp <= 4) {
     // ============================ softmax warps (1..4) ============================
     const int ct = threadIdx.x - 32;         // 0..127
@@ -473,9 +480,8 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
           fphase ^= 1;
         }
       }
-      wait_pv(0);
-      wait_pv(1);  // every PV of the item completed: O[ob] is final
-      // ---- hand the item to the epilogue warps: per-warp row-sum partials and the running max
+      // ---- hand the item to the epilogue warps: per-warp row-sum partials and the running max (the
+      // item's last PV may still run: the epilogue waits for it on o_full, so the softmax warps go on)
       float x[kC];
 #pragma unroll
       for (int c = 0; c < kC; ++c) {
@@ -512,6 +518,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       float ov[kC], l[kC], mm[kC];
       if (d.ntiles > 0) {
         ptx::mbar_wait(&epi_full[ob], efph[ob]);
+        ptx::mbar_wait(&o_full[ob], efph[ob]);  // the item's last PV completed
         efph[ob] ^= 1;
         ptx::tc_fence_after();
         ptx::tmem_ld<kC>(tmem + lane_addr + 32 + ob * 16, ov);
