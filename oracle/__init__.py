@@ -61,6 +61,8 @@ def _load():
                                             ctypes.c_int, P, P, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                                             ctypes.c_int, ctypes.c_double, ctypes.c_double,
                                             P, ctypes.c_int, P, P, ctypes.c_int]
+        lib.orc_round_dtype.restype = ctypes.c_double
+        lib.orc_round_dtype.argtypes = [ctypes.c_double, ctypes.c_int]
         lib.orc_rope_rotate.restype = None
         lib.orc_rope_rotate.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double]
         lib.orc_merge.restype = None
@@ -227,9 +229,9 @@ def brute_force(*, qo_indptr, kv_page_indptr, kv_last_page_len, kv_page_indices,
         Kr = np.repeat(Kd, g, axis=1)  # GQA: head h uses kv head h // g
         Vr = np.repeat(Vd, g, axis=1)
         Q = qf[q0:q1]
-        if rope_theta > 0:
-            Q = rope_complex(Q, lk - lq + np.arange(lq), rope_theta, rope_scale)
-            Kr = rope_complex(Kr, np.arange(lk), rope_theta, rope_scale)
+        if rope_theta > 0:  # transformed q / k are tensors of the input dtype (R31)
+            Q = round_to_dtype(rope_complex(Q, lk - lq + np.arange(lq), rope_theta, rope_scale), dtype)
+            Kr = round_to_dtype(rope_complex(Kr, np.arange(lk), rope_theta, rope_scale), dtype)
         S = sm_scale * np.einsum("rhd,thd->hrt", Q, Kr)  # [H, lq, lk]
         if soft_cap > 0:
             S = soft_cap * np.tanh(S / soft_cap)
@@ -267,6 +269,27 @@ def rope_complex(x, pos, rope_theta, rope_scale=1.0):
     z = x[..., :h] + 1j * x[..., h:]
     z = z * np.exp(1j * np.asarray(pos, np.float64)[:, None, None] * theta[None, None, :])
     return np.concatenate([z.real, z.imag], axis=-1)
+
+
+def round_to_dtype(x, dtype):
+    """Round float64 values to the nearest `dtype` value, ties to even, via numpy's own float
+    types (f32, f16) and, for bf16, the f32 bit pattern rounded to its top 16 bits (different code
+    from the C oracle's orc_round_dtype). Inputs are O(1): no overflow handling."""
+    x = np.asarray(x, np.float64)
+    if dtype == "f32":
+        return x.astype(np.float32).astype(np.float64)
+    if dtype == "f16":
+        return x.astype(np.float16).astype(np.float64)
+    # bf16: exact in two steps only when the f32 rounding cannot create a tie; use the f64 bits
+    b = x.view(np.uint64).astype(np.uint64)
+    # keep 1 + 7 fraction bits of the f64 significand (52 - 7 = 45 dropped bits), RN-even
+    lsb = (b >> np.uint64(45)) & np.uint64(1)
+    b = (b + np.uint64((1 << 44) - 1) + lsb) & ~np.uint64((1 << 45) - 1)
+    return b.view(np.float64)
+
+
+def round_dtype_c(x: float, dtype: str) -> float:
+    return _load().orc_round_dtype(float(x), DT_CODE[dtype])
 
 
 def rope_rotate(x, pos, rope_theta, rope_scale=1.0):

@@ -107,6 +107,22 @@ int orc_version(void) { return 1; }
  * rotate-half pairing (R31): for i < D/2, theta_i = rope_theta^(-2i/D) / rope_scale and
  * angle a = pos * theta_i (float64, exact positions); the pair (x_i, x_{i+D/2}) becomes
  * (x_i cos a - x_{i+D/2} sin a, x_{i+D/2} cos a + x_i sin a). In place. */
+/* Round to the nearest value of a storage dtype (ties to even): ORC_F32 -> float; ORC_F16 /
+ * ORC_BF16 -> 11 / 8 significant bits with minimum normal exponent -14 / -126 (subnormals keep
+ * that spacing). The plain definition, used for the transformed q / k (R31). */
+double orc_round_dtype(double x, int dtype) {
+  if (dtype == ORC_F32) return (double)(float)x;
+  if (x == 0.0 || !isfinite(x)) return x;
+  const int p = dtype == ORC_F16 ? 11 : 8;
+  const int emin = dtype == ORC_F16 ? -14 : -126;
+  int e;
+  frexp(x, &e); /* |x| = m 2^e, 0.5 <= m < 1: leading bit 2^(e-1) */
+  int lead = e - 1;
+  if (lead < emin) lead = emin;
+  const double q = ldexp(1.0, lead - (p - 1)); /* spacing of representable values */
+  return nearbyint(x / q) * q;                 /* default rounding mode: to nearest, ties even */
+}
+
 void orc_rope_rotate(double* x, int D, double pos, double rope_theta, double rope_scale) {
   const int h = D / 2;
   for (int i = 0; i < h; ++i) {
@@ -159,7 +175,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
                         int num_threads) {
   if (batch < 0 || H_qo <= 0 || H_kv <= 0 || H_qo % H_kv != 0 || D <= 0 || page_size <= 0) return 1;
   if (mask_mode == ORC_MASK_CUSTOM && (!custom_mask || !mask_bit_indptr)) return 2;
-  if (rope_theta > 0.0 && (D % 2 != 0 || !(rope_scale > 0.0))) return 5;
+  if (rope_theta > 0.0 && (D % 2 != 0 || !(rope_scale > 0.0) || kv_dtype == ORC_E4M3)) return 5;
   const int g = H_qo / H_kv;
   const int nreq = req_list ? n_req_list : batch;
 
@@ -237,6 +253,8 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
         if (rope_theta > 0.0) { /* QueryTransform: the query row sits at position l_kv - l_qo + r */
           for (int d = 0; d < D; ++d) qr[d] = orc_load(q, dtype, qbase + d);
           orc_rope_rotate(qr, D, (double)(l_kv - l_qo + r), rope_theta, rope_scale);
+          /* the transformed query is a query tensor of the input dtype (R31): rounded RN */
+          for (int d = 0; d < D; ++d) qr[d] = orc_round_dtype(qr[d], dtype);
         }
         /* pass 1: scores and their max */
         double m = -INFINITY;
@@ -248,6 +266,7 @@ int orc_paged_attention(int batch, const int32_t* qo_indptr, const int32_t* kv_p
           if (rope_theta > 0.0) { /* KeyTransform: key t sits at position t */
             for (int d = 0; d < D; ++d) kr[d] = k_scale * orc_load(k_pool, kv_dtype, kb + d);
             orc_rope_rotate(kr, D, (double)t, rope_theta, rope_scale);
+            for (int d = 0; d < D; ++d) kr[d] = orc_round_dtype(kr[d], dtype);
             for (int d = 0; d < D; ++d) dot += qr[d] * kr[d];
           } else
           for (int d = 0; d < D; ++d) dot += orc_load(q, dtype, qbase + d) * (k_scale * orc_load(k_pool, kv_dtype, kb + d));

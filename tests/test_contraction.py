@@ -112,7 +112,7 @@ def test_fused_and_standalone_contraction_bitwise(cuda_device):
     outs = []
     for tiles in ((16,), (16, 64)):
         cfg = bsra.make_config(H_qo=32, H_kv=8, D=128, page_size=16, dtype="bf16", max_batch=4, max_total_qo_rows=4,
-                               num_ctas=148, tile_set=tiles, tile_q=16)
+                               num_ctas=148, tile_set=tiles)  # the heuristic picks T_q = 16 in both
         eng = bsra.Engine(cfg, 0)
         o = torch.empty((4, 32, 128), device=cuda_device, dtype=torch.bfloat16)
         lse = torch.empty((4, 32), device=cuda_device)
@@ -121,5 +121,6 @@ def test_fused_and_standalone_contraction_bitwise(cuda_device):
         torch.cuda.synchronize()
         outs.append((o, lse, eng.export_plan(), eng.last_launches()))
     assert outs[0][3] == 1 and outs[1][3] == 2  # fused vs separate contraction launch
+    assert outs[0][2][3] == 16 and outs[1][2][3] == 16
     assert np.array_equal(outs[0][2], outs[1][2]) and outs[0][2][7] > 0  # same plan, with splits
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
