@@ -162,6 +162,8 @@ class Layered:
         wl = self.wl
         if wl.kv_dtype:
             kw = dict(kw, kv_dtype=wl.kv_dtype, k_scale=self.inp0.k_scale, v_scale=self.inp0.v_scale)
+        if wl.rope_theta:
+            kw = dict(kw, rope_theta=wl.rope_theta, rope_scale=wl.rope_scale)
         cfg = self.bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
                                     mask=wl.mask, max_batch=wl.batch, max_total_qo_rows=int(wl.qo_lens.sum()),
                                     max_total_kv_tokens=int(wl.kv_lens.astype(np.int64).sum()), **kw)
@@ -411,6 +413,34 @@ def bench_fp8_decode(dev, pk, args, world, rank, bf16_ms):
             "kv_tokens_per_s": tokens / (ms * 1e-3), "speedup_vs_bf16_kv": bf16_ms / ms,
             "launch_ms": launch_ms, "frac": by["total"] / (launch_ms * 1e-3) / 1e9 / pk["hbm_gbs"],
             "kernel": eng.selected_kernel(), "algorithmic_bytes_per_launch": by["total"]}
+
+
+def bench_rope_decode(dev, pk, args, world, rank, plain_ms):
+    """SURVEY §8(f) NEXT-3 fused RoPE (R31): the configs[1] decode step with q and
+    k rotated inside the decode kernel (Llama-3 theta 500000; the cache holds un-rotated keys, as
+    StreamingLLM needs). Same layers / graph / timing as the headline; `overhead` = the step time
+    relative to the plain step (same bytes)."""
+    import dataclasses
+    wl = dataclasses.replace(synth.c2_decode_llama8b(), rope_theta=500000.0)
+    L = Layered(wl, args.layers, dev, seed_base=1000 * rank)
+    eng = L.engine(num_ctas=args.num_ctas, tile_q=16, kernel=args.kernel, pdl=not args.no_pdl, max_qo_len=1)
+    s, one_step, _ = time_device_steps(L, eng, args.steps, args.warmup, not args.no_graph)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        a.record(s)
+        for _ in range(args.steps):
+            one_step()
+        b.record(s)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(a.elapsed_time(b) / args.steps, world)
+    by = decode_bytes(wl)
+    launch_ms = per_launch_ms(L, eng)
+    return {"workload": "c2_decode_llama8b (configs[1]) with fused RoPE (theta 500000)", "unit": "TB/s",
+            "value": world * by["total"] * args.layers / (ms * 1e-3) / 1e12, "ms_per_step": ms,
+            "step_time_vs_plain": ms / plain_ms, "launch_ms": launch_ms,
+            "frac": by["total"] / (launch_ms * 1e-3) / 1e9 / pk["hbm_gbs"], "kernel": eng.selected_kernel()}
 
 
 def bench_composable(dev, pk, world=1, rank=0, layers=16, reps=20):
@@ -841,6 +871,7 @@ def main():
     ap.add_argument("--no-sched", action="store_true", help="skip the scheduler / balance-ablation fields")
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-quest", action="store_true", help="skip the Quest block-sparse decode line")
+    ap.add_argument("--no-rope", action="store_true", help="skip the fused-RoPE decode line")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     maybe_relaunch(args)
@@ -925,6 +956,12 @@ def main():
         fp8 = bench_fp8_decode(dev, pk, args, world, rank, ms)
         torch.cuda.empty_cache()
 
+    # ---- secondary: the same decode step with fused RoPE (NEXT-3)
+    rope = None
+    if not args.no_rope:
+        rope = bench_rope_decode(dev, pk, args, world, rank, ms)
+        torch.cuda.empty_cache()
+
     # ---- secondary: configs[2] ragged causal prefill TFLOP/s (one layer, per-launch events)
     prefill = None
     if not args.no_prefill:
@@ -974,6 +1011,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "prefill": prefill,
             "decode_head_sharded": head_sharded, "composable": composable, "long_context": long_ctx,
             "contiguous_kv": contiguous, "decode_fp8": fp8, "scheduler": sched, "quest": quest,
+            "decode_rope": rope,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         }
         emit(out)

@@ -110,7 +110,17 @@ typedef struct {
    *                        plan and capture tracking (bsra_run) guards graphs against growth. */
   int32_t max_total_kv_tokens;
   int32_t max_qo_len;
-  int32_t reserved[4];       /* must be zero                                                    */
+  /* Fused RoPE (the paper's Query/KeyTransform, "fuse normalization, RoPE ... into the
+   * attention kernel"; the StreamingLLM kernel of P:329-338; R31). rope_theta > 0 rotates
+   * q and k inside the kernel before the logits: rotate-half pairs (i, i + D/2), frequency
+   * theta_i = rope_theta^(-2i/D) / rope_scale, key t of a request at position t (its index in the
+   * request's KV), query row r at l_kv - l_qo + r; the rotated q / k are rounded to `dtype` like
+   * any query / key tensor (the MMA operand type). The K/V cache holds UN-rotated keys.
+   * rope_scale 0 => 1. Not with an E4M3 KV cache (EUNSUPPORTED). Decode tiles (T_q = 16) rotate in
+   * the tcgen05 decode kernel; other tiles run on the CUDA-core kernel. 0 = off. */
+  float rope_theta;
+  float rope_scale;
+  int32_t reserved[2];       /* must be zero                                                    */
 } bsra_config;
 
 /* flags: BSRA_FLAG_PDL launches the tcgen05 kernels with programmatic dependent launch: a run()

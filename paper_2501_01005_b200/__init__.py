@@ -40,7 +40,7 @@ class Config(ctypes.Structure):
                 ("sliding_window", ctypes.c_int32), ("logits_soft_cap", ctypes.c_float),
                 ("kv_dtype", ctypes.c_int32), ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float),
                 ("alibi", ctypes.c_int32), ("max_total_kv_tokens", ctypes.c_int32), ("max_qo_len", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 4)]
+                ("rope_theta", ctypes.c_float), ("rope_scale", ctypes.c_float), ("reserved", ctypes.c_int32 * 2)]
 
 
 FLAG_PDL = 1  # BSRA_FLAG_PDL (include/bsra.h)
@@ -119,12 +119,13 @@ def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="n
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
                 kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False, window=0,
                 soft_cap=0.0, kv_dtype=None, k_scale=0.0, v_scale=0.0, alibi=False, balance_ctas=False,
-                max_total_kv_tokens=0, max_qo_len=0) -> Config:
+                max_total_kv_tokens=0, max_qo_len=0, rope_theta=0.0, rope_scale=0.0) -> Config:
     """window: sliding window W (0 = off, DESIGN.md R26); soft_cap: logits soft-cap c (0 = off, R27);
     kv_dtype "e4m3": fp8 KV cache with per-tensor scales k_scale / v_scale (0 = 1; R28);
     max_total_kv_tokens / max_qo_len: engine bounds (include/bsra.h)."""
     c = Config()
     c.max_total_kv_tokens, c.max_qo_len = int(max_total_kv_tokens), int(max_qo_len)
+    c.rope_theta, c.rope_scale = float(rope_theta), float(rope_scale)
     if kv_dtype:
         c.kv_dtype = DTYPE[kv_dtype] if isinstance(kv_dtype, str) else kv_dtype
     c.k_scale, c.v_scale = float(k_scale), float(v_scale)

@@ -92,6 +92,16 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
           Vec<T>::to_float(u, qv + c * kVecN);
         }
       }
+      if (p.rope) {  // QueryTransform (R31): the row sits at position l_kv - l_qo + tok
+#pragma unroll
+        for (int i = 0; i < D / 2; ++i) {
+          float sn, cs;
+          rope_sincos(causal_lim, p.rope_f[i], sn, cs);
+          const float x = qv[i], y = qv[i + D / 2];
+          qv[i] = to_f<T>(from_float<T>(x * cs - y * sn));  // a query tensor of dtype T
+          qv[i + D / 2] = to_f<T>(from_float<T>(y * cs + x * sn));
+        }
+      }
       float m = -INFINITY, dsum = 0.f;
       float acc[kPer];
 #pragma unroll
@@ -123,12 +133,24 @@ __global__ void __launch_bounds__(kSimtWarps * 32) attn_simt_kernel(const __grid
         if (vis) {
           const uint4* krow = reinterpret_cast<const uint4*>(sk[st] + lane * S::kRowBytes);
           float dot = 0.f;
+          if (p.rope) {  // KeyTransform (R31): key t at position t, rotated then rounded to T
+            const TKV* kr = reinterpret_cast<const TKV*>(krow);
 #pragma unroll
-          for (int c = 0; c < D / kVecK; ++c) {
-            float kf[kVecK];
-            Vec<TKV>::to_float(krow[c], kf);
+            for (int i = 0; i < D / 2; ++i) {
+              float sn, cs;
+              rope_sincos(t, p.rope_f[i], sn, cs);
+              const float x = to_f<TKV>(kr[i]), y = to_f<TKV>(kr[i + D / 2]);
+              dot = fmaf(qv[i], to_f<T>(from_float<T>(x * cs - y * sn)), dot);
+              dot = fmaf(qv[i + D / 2], to_f<T>(from_float<T>(y * cs + x * sn)), dot);
+            }
+          } else {
 #pragma unroll
-            for (int e = 0; e < kVecK; ++e) dot = fmaf(qv[c * kVecK + e], kf[e], dot);
+            for (int c = 0; c < D / kVecK; ++c) {
+              float kf[kVecK];
+              Vec<TKV>::to_float(krow[c], kf);
+#pragma unroll
+              for (int e = 0; e < kVecK; ++e) dot = fmaf(qv[c * kVecK + e], kf[e], dot);
+            }
           }
           float sr = p.soft_cap > 0.f ? soft_cap_raw(p, dot) : dot;  // soft-cap (R27)
           if (p.alibi) sr += slope * (float)(t - causal_lim);         // ALiBi (R30): t - p

@@ -47,7 +47,21 @@ struct AttnParams {
   // ALiBi (R30): raw score s += slope_h / logit_scale * (t - p)
   int32_t alibi;
   float inv_logit_scale;
+  // RoPE (P:228 / P:329-338, R31): pair (i, i + D/2) turns by pos * theta_i; rope_f[i] =
+  // theta_i / 2pi as a 0.64 fixed-point fraction of a turn, so (pos * rope_f[i]) mod 2^64 is the
+  // angle's fraction of a turn, exact for every position
+  int32_t rope;
+  uint64_t rope_f[64];
 };
+
+// sin / cos of the RoPE angle pos * theta (frequency f = theta / 2pi in 2^-64 turns): the 64-bit
+// product wraps modulo one turn exactly, its top 32 bits (signed) are the angle in [-pi, pi) to
+// 2^-31 of a turn, and __sincosf is accurate to ~2^-21 on that range (no large-argument loss).
+__device__ __forceinline__ void rope_sincos(int64_t pos, uint64_t f, float& sn, float& cs) {
+  const uint64_t u = (uint64_t)pos * f;
+  const float a = (float)(int32_t)(u >> 32) * 1.4629180792671596e-09f;  // 2pi / 2^32
+  __sincosf(a, &sn, &cs);
+}
 
 // LogitsTransform soft-cap on a raw score (R27): s -> c * tanh(s / c), c in raw units.
 // tanh x = 1 - 2 / (2^(2x log2 e) + 1): one ex2 and one rcp (absolute error ~1e-7, i.e. ~c*1e-7

@@ -86,7 +86,10 @@ bsra_status validate_config(const bsra_config& c) {
     return fail(BSRA_EINVAL, "k_scale / v_scale must be finite and >= 0");
   if (c.alibi != 0 && c.alibi != 1) return fail(BSRA_EINVAL, "alibi must be 0 or 1");
   if (c.max_total_kv_tokens < 0 || c.max_qo_len < 0) return fail(BSRA_EINVAL, "negative bounds");
-  for (int i = 0; i < 4; ++i)
+  if (!(c.rope_theta >= 0.f) || !std::isfinite(c.rope_theta) || !(c.rope_scale >= 0.f) || !std::isfinite(c.rope_scale))
+    return fail(BSRA_EINVAL, "rope_theta / rope_scale must be finite and >= 0");
+  if (c.rope_theta > 0.f && kv_is_f8(c)) return fail(BSRA_EUNSUPPORTED, "RoPE with an E4M3 KV cache");
+  for (int i = 0; i < 2; ++i)
     if (c.reserved[i]) return fail(BSRA_EINVAL, "reserved fields must be zero");
   return BSRA_OK;
 }
@@ -165,6 +168,7 @@ struct bsra_engine {
   int32_t max_qo = 0;
   int32_t kc = 16;  // decode kernel's live fused columns for the current plan
   float k_scale = 1.f, v_scale = 1.f;  // fp8 KV dequantisation scales (bsra_set_kv_scales)
+  uint64_t rope_f[64] = {};            // RoPE: theta_i / 2pi in 2^-64 turns (R31), i < D/2
   // fp8 KV with prefill tiles (f8_gather.cuh): the current plan addresses a 16-bit gathered copy
   // in the workspace's f8 region ([2][lay.f8_rows, H_kv, 128])
   bool f8_prefill = false;
@@ -226,6 +230,14 @@ bsra_status bsra_engine_create(const bsra_config* cfg, int32_t device, void* d_w
   e->cfg.num_ctas = nc;
   e->k_scale = cfg->k_scale > 0.f ? cfg->k_scale : 1.f;
   e->v_scale = cfg->v_scale > 0.f ? cfg->v_scale : 1.f;
+  if (cfg->rope_theta > 0.f) {  // RoPE frequencies as exact fractions of a turn: pos * F mod 2^64
+    const long double two_pi = 6.283185307179586476925286766559L;
+    const long double scale = cfg->rope_scale > 0.f ? (long double)cfg->rope_scale : 1.0L;
+    for (int i = 0; i < cfg->head_dim / 2; ++i) {
+      const long double theta = powl((long double)cfg->rope_theta, -2.0L * i / cfg->head_dim) / scale;
+      e->rope_f[i] = (uint64_t)llroundl(ldexpl(theta / two_pi, 64));
+    }
+  }
   e->device = device;
   if (query_sms(device, &e->sms) != BSRA_OK) e->sms = 148;
   e->lay = lay;
@@ -570,6 +582,8 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
   p.scale_log2 = logit_scale * bsra::kLog2e;
   p.alibi = c.alibi;
   p.inv_logit_scale = 1.f / logit_scale;  // ALiBi bias in raw q.k units (R30)
+  p.rope = c.rope_theta > 0.f ? 1 : 0;
+  std::memcpy(p.rope_f, e->rope_f, sizeof(p.rope_f));
 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int grid = c.num_ctas;
@@ -638,6 +652,7 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     tl.ragged = ragged;
     tl.total_kv = kv_extent;
     tl.f8kv = !kv16;
+    tl.rope = p.rope != 0;
     const char* why = "";
     int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
     if (rc < 0)

@@ -30,6 +30,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "merge.cuh"
 #include "ptx.cuh"
@@ -81,10 +83,12 @@ constexpr int kPBytes = 2 * kN * 128;        // P^T: 2 token-halves x 16 rows x 
 constexpr int kOffQ = kStages * kStageBytes;
 constexpr int kOffP = kOffQ + 2 * kQBytes;   // two P^T buffers
 constexpr int kOffBar = kOffP + 2 * kPBytes;
-constexpr int kOffRed = kOffBar + 256;
+constexpr int kOffRed = kOffBar + 512;
 // red [4][kN], vote flags [2][4], epilogue hand-off sums [2][4][kN] and max [2][kN]; + alignment slack
 constexpr int kSmemBytes = kOffRed + 1024 + 1024;
 constexpr int kThreads = 320;  // producer, 4 softmax warps, MMA warp, 4 epilogue warps
+constexpr int kThreadsRope = 448;  // + 4 RoPE warps (thread = K row) in the fused-RoPE variant
+constexpr int threads_for(bool rope) { return rope ? kThreadsRope : kThreads; }
 constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T double buffer at 32 / 48
 constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
 }  // namespace dec
@@ -113,10 +117,33 @@ __device__ __forceinline__ DecItem dec_item(const PlanView& pv, int it, int g) {
   return d;
 }
 
+// RoPE of one 16-byte chunk pair in shared memory (R31): 8 elements of the first half (d = i0..i0+7)
+// and their partners d + 64 in the second half, rotated by pos * theta_i and rounded back to the
+// operand type (the MMA reads them in place).
+template <bool kF16>
+__device__ __forceinline__ void rope_chunk(uint8_t* lo, uint8_t* hi, int64_t pos, const uint64_t* f, int i0) {
+  using T = typename std::conditional<kF16, __half, __nv_bfloat16>::type;
+  uint4 a = *reinterpret_cast<uint4*>(lo), b = *reinterpret_cast<uint4*>(hi);
+  T* x = reinterpret_cast<T*>(&a);
+  T* y = reinterpret_cast<T*>(&b);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    float sn, cs;
+    rope_sincos(pos, f[i0 + e], sn, cs);
+    const float xv = to_f<T>(x[e]), yv = to_f<T>(y[e]);
+    x[e] = from_float<T>(xv * cs - yv * sn);
+    y[e] = from_float<T>(yv * cs + xv * sn);
+  }
+  *reinterpret_cast<uint4*>(lo) = a;
+  *reinterpret_cast<uint4*>(hi) = b;
+}
+
 // kF16: fp16 q / o (else bf16) at compile time: one code path per instantiation (instruction
-// fetch stalls measured on the fp8 kernel when both were inlined)
-template <int kC, int kMask, bool kF16>
-__global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
+// fetch stalls measured on the fp8 kernel when both were inlined). kRope: fused RoPE (R31) —
+// four more warps rotate each landed K tile in shared memory (thread = token row) and each item's
+// Q tile before the MMA warp reads them (krot / qrot barriers replace full / full_q for S).
+template <int kC, int kMask, bool kF16, bool kRope>
+__global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
   using namespace dec;
   const AttnParams& p = tp.p;
   extern __shared__ uint8_t smem_raw[];
@@ -134,7 +161,9 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
   uint64_t* epi_full = o_free + 2;       // [2] item's row sums / max handed to the epilogue (4 warps)
   uint64_t* epi_empty = epi_full + 2;    // [2] epilogue consumed hand-off buffer b (1 arrival)
   uint64_t* o_full = epi_empty + 2;      // [2] the item's last PV into O^T buffer b completed (commit)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+  uint64_t* krot = o_full + 2;           // [kStages] kRope: K tile of the stage rotated
+  uint64_t* qrot = krot + kStages;       // [2] kRope: Q buffer rotated
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qrot + 2);
   float* red = reinterpret_cast<float*>(smem + kOffRed);  // [4 warps][kN]
   int* vflags = reinterpret_cast<int*>(red + 4 * kN);     // [2][4] vote flags
   float* hsum = reinterpret_cast<float*>(vflags + 8);      // [2][4 warps][kN] row-sum partials
@@ -149,6 +178,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&krot[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&full_q[b], 1);
@@ -163,6 +193,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       ptx::mbar_init(&epi_full[b], 4);
       ptx::mbar_init(&epi_empty[b], 1);
       ptx::mbar_init(&o_full[b], 1);
+      ptx::mbar_init(&qrot[b], 1);
     }
     ptx::fence_barrier_init();
   }
@@ -284,7 +315,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
     };
     for (int it = it0; it < it1; ++it) {
       const DecItem d = dec_item(pv, it, g);
-      ptx::mbar_wait(&full_q[qb], qphase[qb]);
+      ptx::mbar_wait(kRope ? &qrot[qb] : &full_q[qb], qphase[qb]);
       qphase[qb] ^= 1;
       if (d.ntiles == 0) {
         ptx::mbar_arrive_warp(&empty_q[qb]);
@@ -293,7 +324,7 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       }
       const uint64_t bq = ptx::smem_desc_sw128(sbase + kOffQ + qb * kQBytes, 16, 1024);
       for (int ti = 0; ti < d.ntiles; ++ti) {
-        ptx::mbar_wait(&full[stage], fphase);
+        ptx::mbar_wait(kRope ? &krot[stage] : &full[stage], fphase);
         ptx::mbar_wait(&s_free[sb], sfph[sb]);
         sfph[sb] ^= 1;
         ptx::tc_fence_after();
@@ -504,7 +535,48 @@ __global__ void __launch_bounds__(dec::kThreads, 1) tc_decode_kernel(const __gri
       if (lane == 0) ptx::mbar_arrive(&epi_full[ob]);
       ob ^= 1;
     }
-  } else {
+  } else if (kRope && warp >= 10) {
+    // ====== RoPE warps (10..13): rotate Q (per item) and K (per tile) in shared memory (R31) ======
+    const int rt = threadIdx.x - dec::kThreads;  // 0..127: K token row / (Q row, chunk)
+    int stage = 0, qb = 0;
+    uint32_t fphase = 0, qph[2] = {0, 0};
+    const uint64_t* f = p.rope_f;
+    for (int it = it0; it < it1; ++it) {
+      const DecItem d = dec_item(pv, it, g);
+      ptx::mbar_wait(&full_q[qb], qph[qb]);
+      qph[qb] ^= 1;
+      {  // Q: 16 rows x 8 chunk pairs; fused row c is token (row0 + c) / g at l_kv - l_qo + token
+        const int c = rt >> 3, ch = rt & 7;
+        if (d.ntiles > 0 && c < kC && c < d.nrows) {
+          uint8_t* q0 = smem + kOffQ + qb * kQBytes + c * 128 + ((ch ^ (c & 7)) << 4);
+          rope_chunk<kF16>(q0, q0 + kN * 128, d.lk - d.lq + (d.row0 + c) / g, f, ch * 8);
+        }
+        ptx::fence_proxy_async();  // generic-proxy writes visible to the tensor core
+        ptx::named_bar_sync(3, 128);
+        if (rt == 0) ptx::mbar_arrive(&qrot[qb]);
+      }
+      qb ^= 1;
+      for (int ti = 0; ti < d.ntiles; ++ti) {
+        ptx::mbar_wait(&full[stage], fphase);
+        const int64_t t0 = d.kb + (int64_t)ti * kTile;
+        if (t0 + rt < d.ke) {  // key t0 + rt at position t0 + rt; both 64-column halves
+          uint8_t* k0 = smem + stage * kStageBytes + rt * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const int off = (ch ^ (rt & 7)) << 4;
+            rope_chunk<kF16>(k0 + off, k0 + kHalfBytes + off, t0 + rt, f, ch * 8);
+          }
+        }
+        ptx::fence_proxy_async();
+        ptx::named_bar_sync(3, 128);
+        if (rt == 0) ptx::mbar_arrive(&krot[stage]);
+        if (++stage == kStages) {
+          stage = 0;
+          fphase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 6) {
     // ====== epilogue warps (6..9): thread = TMEM lane = head-dim row d of O^T; normalise, write ======
     const int et = threadIdx.x - 192;        // 0..127
     const int q4 = warp & 3;

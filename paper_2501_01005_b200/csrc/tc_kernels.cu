@@ -63,7 +63,7 @@ bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int64_t
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int kC, int kMask, bool kF8>
+template <int kC, int kMask, bool kF8, bool kRope = false>
 cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
   static bool attr = false;
   if constexpr (kF8) {  // fp8 KV cache: K in TMEM, converter warps (tc_decode_f8.cuh)
@@ -80,21 +80,31 @@ cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
     return launch_tc(tc_decode_f8_kernel<kC, kMask, false>, grid, f8d::threads_for(kC), f8d::kSmemBytes, st, tp);
   } else {
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false>,
+    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false, kRope>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true, kRope>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              dec::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true>, grid, dec::kThreads, dec::kSmemBytes, st, tp);
-  return launch_tc(tc_decode_kernel<kC, kMask, false>, grid, dec::kThreads, dec::kSmemBytes, st, tp);
+  const int nt = dec::threads_for(kRope);
+  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true, kRope>, grid, nt, dec::kSmemBytes, st, tp);
+  return launch_tc(tc_decode_kernel<kC, kMask, false, kRope>, grid, nt, dec::kSmemBytes, st, tp);
   }
 }
 
 template <int kC, bool kF8>
 cudaError_t launch_decode_m(int mask, const TcParams& tp, int grid, cudaStream_t st) {
+  if constexpr (!kF8) {
+    if (tp.p.rope) {  // fused RoPE variant (R31)
+      switch (mask) {
+        case 0: return launch_decode_t<kC, 0, false, true>(tp, grid, st);
+        case 1: return launch_decode_t<kC, 1, false, true>(tp, grid, st);
+        default: return launch_decode_t<kC, 2, false, true>(tp, grid, st);
+      }
+    }
+  }
   switch (mask) {
     case 0: return launch_decode_t<kC, 0, kF8>(tp, grid, st);
     case 1: return launch_decode_t<kC, 1, kF8>(tp, grid, st);
@@ -159,6 +169,7 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     return 1;
   }
   if (L.f8kv) { *why = "fp8 KV with T_q > 16 runs on the CUDA-core kernel"; return 0; }
+  if (L.rope) { *why = "fused RoPE with T_q > 16 runs on the CUDA-core kernel"; return 0; }
   if (L.T_q == 64 || L.T_q == 128 || L.T_q == 256) {
     return tc_prefill_launch(p, L, st, name, why, B);
   }

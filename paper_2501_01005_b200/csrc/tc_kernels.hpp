@@ -19,6 +19,7 @@ struct TcLaunch {
   bool ragged = false;     // contiguous KV [N, H_kv, D] (p.kv_ragged)
   int64_t total_kv = 0;    // ragged: the token extent of the k / v maps
   bool f8kv = false;       // K/V pools in E4M3 (fp8 KV cache, R28)
+  bool rope = false;       // fused RoPE (R31): decode tiles only
 };
 
 // Launches the tcgen05 kernel for this plan if one applies (bf16/f16, D = 128, supported page
