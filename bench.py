@@ -381,6 +381,21 @@ def bench_contiguous(dev, pk, reps=9):
         contig = timed(lambda: re_.run_ragged(inp.q, rk.k, rk.v, rk.k_strides, rk.v_strides, o, lse))
         out[key] = {"paged_us": paged, "contiguous_us": contig,
                     "page_table_overhead_pct": 100.0 * (paged / contig - 1.0)}
+        if tq == 16:  # decode: the cp.async row gather at B_c = 16 and at B_c = 1 (P:436's setting)
+            ce = bsra.Engine(bsra.make_config(page_size=wl.page_size, cp_gather=True, **kw), torch.cuda.current_device())
+            ce.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+            out[key]["paged_cp_gather_us"] = timed(lambda: ce.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides,
+                                                                  inp.v_strides, inp.kv_page_indices, o, lse))
+            import dataclasses
+            wl1 = dataclasses.replace(wl, page_size=1)
+            i1 = synth.make_inputs(wl1, device=dev)
+            e1 = bsra.Engine(bsra.make_config(page_size=1, **kw), torch.cuda.current_device())
+            e1.plan(i1.qo_indptr, i1.kv_page_indptr, i1.kv_last_page_len, i1.sm_scale)
+            out[key]["paged_page_size_1_us"] = timed(lambda: e1.run(i1.q, i1.k_pool, i1.v_pool, i1.k_strides,
+                                                                    i1.v_strides, i1.kv_page_indices, o, lse))
+            out[key]["page_size_1_overhead_pct"] = 100.0 * (out[key]["paged_page_size_1_us"] / contig - 1.0)
+            out[key]["page_size_1_kernel"] = e1.selected_kernel()
+            del ce, i1, e1
         del inp, rk, pe, re_, o, lse
         torch.cuda.empty_cache()
     return out

@@ -62,6 +62,11 @@ __device__ __forceinline__ void rope_sincos(int64_t pos, uint64_t f, float& sn, 
   const float a = (float)(int32_t)(u >> 32) * 1.4629180792671596e-09f;  // 2pi / 2^32
   __sincosf(a, &sn, &cs);
 }
+// The same angle through the correctly rounded sincosf (for constants a recurrence reuses)
+__device__ __forceinline__ void rope_sincos_precise(int64_t pos, uint64_t f, float& sn, float& cs) {
+  const uint64_t u = (uint64_t)pos * f;
+  sincosf((float)(int32_t)(u >> 32) * 1.4629180792671596e-09f, &sn, &cs);
+}
 
 // LogitsTransform soft-cap on a raw score (R27): s -> c * tanh(s / c), c in raw units.
 // tanh x = 1 - 2 / (2^(2x log2 e) + 1): one ex2 and one rcp (absolute error ~1e-7, i.e. ~c*1e-7
@@ -231,6 +236,18 @@ __device__ __forceinline__ float to_f<__nv_fp8_e4m3>(__nv_fp8_e4m3 x) { return f
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+// 16-byte cp.async with zero fill: src_bytes = 0 writes 16 zero bytes and reads nothing
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+// arrive on an mbarrier once all of this thread's prior cp.async copies have completed (the
+// barrier's expected count includes this arrival: .noinc)
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(bar))
+               : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>

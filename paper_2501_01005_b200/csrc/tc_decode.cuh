@@ -47,6 +47,7 @@ struct TcParams {
   int32_t q_hb, q_tb;
   int32_t f16;      // 1 = fp16 inputs, 0 = bf16
   int32_t pdl;      // launched with programmatic dependent launch (host-side launch choice)
+  int32_t cp;       // decode: gather K/V rows with 16-byte cp.async (any page size) instead of TMA boxes
   int32_t dbg;      // BSRA_EXPERIMENTS builds only ($BSRA_DEBUG_PREFILL timing modes); 0 otherwise
 };
 
@@ -87,7 +88,7 @@ constexpr int kOffRed = kOffBar + 512;
 // red [4][kN], vote flags [2][4], epilogue hand-off sums [2][4][kN] and max [2][kN]; + alignment slack
 constexpr int kSmemBytes = kOffRed + 1024 + 1024;
 constexpr int kThreads = 320;  // producer, 4 softmax warps, MMA warp, 4 epilogue warps
-constexpr int kThreadsRope = 448;  // + 4 RoPE warps (thread = K row) in the fused-RoPE variant
+constexpr int kThreadsRope = 576;  // + 8 RoPE warps (two per SM sub-partition) in the fused-RoPE variant
 constexpr int threads_for(bool rope) { return rope ? kThreadsRope : kThreads; }
 constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T double buffer at 32 / 48
 constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
@@ -140,8 +141,8 @@ __device__ __forceinline__ void rope_chunk(uint8_t* lo, uint8_t* hi, int64_t pos
 
 // kF16: fp16 q / o (else bf16) at compile time: one code path per instantiation (instruction
 // fetch stalls measured on the fp8 kernel when both were inlined). kRope: fused RoPE (R31) —
-// four more warps rotate each landed K tile in shared memory (thread = token row) and each item's
-// Q tile before the MMA warp reads them (krot / qrot barriers replace full / full_q for S).
+// eight more warps rotate each landed K tile in shared memory and each item's Q tile before the
+// MMA warp reads them (krot / qrot barriers replace full / full_q for S).
 template <int kC, int kMask, bool kF16, bool kRope>
 __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
   using namespace dec;
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], tp.cp ? 32 : 1);  // cp.async gather: one arrival per producer lane
       ptx::mbar_init(&empty[s], 1);
       ptx::mbar_init(&krot[s], 1);
     }
@@ -239,35 +240,76 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       }
       qphase[qb] ^= 1;
       qb ^= 1;
-      // ---- K/V tiles: lane j handles sub-block j (one page, or 128 tokens of a big page)
+      // ---- K/V tiles
       for (int ti = 0; ti < d.ntiles; ++ti) {
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
-        const int n = (int)imin64(kTile, d.ke - t0);
-        const int nsub = (n + B - 1) / B;
-        int page = 0, off = 0;
-        if (lane < nsub) {
-          const int64_t tok = t0 + (int64_t)lane * B;
-          if (p.kv_ragged) {  // contiguous KV: token coordinate, no page table
-            off = (int)(d.page_begin + tok);
-          } else {
-            page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
-            off = (int)(tok % p.page_size);
-          }
-        }
-        if (lane == 0) {
+        if (tp.cp) {
+          // 16-byte cp.async gather, any page size (small pages, B_c not dividing 128): per
+          // instruction the warp moves 4 token rows x 128 B (lane = chunk c of row sub), written
+          // at the SW128 position TMA would use; rows past the chunk are zero-filled (no read).
+          const int c8 = lane & 7, sub = lane >> 3;
           ptx::mbar_wait(&empty[stage], ephase);
-          ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * 512);
+          const uint32_t sK = ptx::smem_u32(smem + stage * kStageBytes), sV = sK + kKVBytes;
+          const uint16_t* kg = reinterpret_cast<const uint16_t*>(p.k);
+          const uint16_t* vg = reinterpret_cast<const uint16_t*>(p.v);
+#pragma unroll 1
+          for (int rb0 = 0; rb0 < kTile / 4; rb0 += 8) {
+            int64_t ko[8], vo[8];
+            bool ok[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {  // the 8 rows' page ids first (independent loads)
+              const int64_t t = t0 + 4 * (rb0 + u) + sub;
+              ok[u] = t < d.ke;
+              int64_t pg = 0, sl;
+              if (p.kv_ragged) {
+                sl = d.page_begin + t;
+              } else {
+                pg = ok[u] ? __ldg(p.page_indices + d.page_begin + t / p.page_size) : 0;
+                sl = t % p.page_size;
+              }
+              ko[u] = ok[u] ? pg * p.ks0 + sl * p.ks1 + (int64_t)d.kvh * p.ks2 + c8 * 8 : 0;
+              vo[u] = ok[u] ? pg * p.vs0 + sl * p.vs1 + (int64_t)d.kvh * p.vs2 + c8 * 8 : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int r = 4 * (rb0 + u) + sub;
+              const uint32_t sw = (uint32_t)(r * 128 + ((c8 ^ (r & 7)) << 4));
+              cp_async16_zfill(sK + sw, kg + ko[u], ok[u]);
+              cp_async16_zfill(sK + kHalfBytes + sw, kg + ko[u] + 64, ok[u]);
+              cp_async16_zfill(sV + sw, vg + vo[u], ok[u]);
+              cp_async16_zfill(sV + kHalfBytes + sw, vg + vo[u] + 64, ok[u]);
+            }
+          }
+          cp_async_mbar_arrive_noinc(&full[stage]);
+        } else {
+          // TMA: lane j handles sub-block j (one page, or 128 tokens of a big page)
+          const int n = (int)imin64(kTile, d.ke - t0);
+          const int nsub = (n + B - 1) / B;
+          int page = 0, off = 0;
+          if (lane < nsub) {
+            const int64_t tok = t0 + (int64_t)lane * B;
+            if (p.kv_ragged) {  // contiguous KV: token coordinate, no page table
+              off = (int)(d.page_begin + tok);
+            } else {
+              page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
+              off = (int)(tok % p.page_size);
+            }
+          }
+          if (lane == 0) {
+            ptx::mbar_wait(&empty[stage], ephase);
+            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * 512);
+          }
+          __syncwarp();
+          if (lane < nsub) {
+            uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
+            uint8_t* vd = kd + kKVBytes;
+            ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
+            ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
+            ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
+            ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        if (lane < nsub) {
-          uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
-          uint8_t* vd = kd + kKVBytes;
-          ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
-          ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
-          ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
-          ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
-        }
-        __syncwarp();
         if (++stage == kStages) {
           stage = 0;
           ephase ^= 1;
@@ -327,6 +369,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ptx::mbar_wait(kRope ? &krot[stage] : &full[stage], fphase);
         ptx::mbar_wait(&s_free[sb], sfph[sb]);
         sfph[sb] ^= 1;
+        if (tp.cp) ptx::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core reads
         ptx::tc_fence_after();
         const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes, 16, 1024);
 #pragma unroll
@@ -536,39 +579,71 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       ob ^= 1;
     }
   } else if (kRope && warp >= 10) {
-    // ====== RoPE warps (10..13): rotate Q (per item) and K (per tile) in shared memory (R31) ======
-    const int rt = threadIdx.x - dec::kThreads;  // 0..127: K token row / (Q row, chunk)
+    // ====== RoPE warps (10..17): rotate Q (per item) and K (per tile) in shared memory (R31) ======
+    const int rt = threadIdx.x - dec::kThreads;  // 0..255
     int stage = 0, qb = 0;
     uint32_t fphase = 0, qph[2] = {0, 0};
     const uint64_t* f = p.rope_f;
+    const int ri = rt & 63, rgrp = rt >> 6;  // K: pair index and row group (rows = rgrp mod 4)
+    float s2, c2;
+    rope_sincos_precise(4, f[ri], s2, c2);  // the per-step rotation by 4 theta_i (1 ulp)
     for (int it = it0; it < it1; ++it) {
       const DecItem d = dec_item(pv, it, g);
       ptx::mbar_wait(&full_q[qb], qph[qb]);
       qph[qb] ^= 1;
       {  // Q: 16 rows x 8 chunk pairs; fused row c is token (row0 + c) / g at l_kv - l_qo + token
         const int c = rt >> 3, ch = rt & 7;
-        if (d.ntiles > 0 && c < kC && c < d.nrows) {
+        if (d.ntiles > 0 && rt < 128 && c < kC && c < d.nrows) {
           uint8_t* q0 = smem + kOffQ + qb * kQBytes + c * 128 + ((ch ^ (c & 7)) << 4);
           rope_chunk<kF16>(q0, q0 + kN * 128, d.lk - d.lq + (d.row0 + c) / g, f, ch * 8);
         }
         ptx::fence_proxy_async();  // generic-proxy writes visible to the tensor core
-        ptx::named_bar_sync(3, 128);
+        ptx::named_bar_sync(3, 256);
         if (rt == 0) ptx::mbar_arrive(&qrot[qb]);
       }
       qb ^= 1;
       for (int ti = 0; ti < d.ntiles; ++ti) {
         ptx::mbar_wait(&full[stage], fphase);
+        // K: thread = (pair i, row group); it walks rows grp, grp + 4, ... of the tile, so the
+        // angle (t0 + r) theta_i advances by the constant 4 theta_i: one sincos per tile and a
+        // rotation recurrence per row (fp32, 32 steps: ~1e-6 relative drift, far below the bf16
+        // rounding of the rotated key). Lanes = consecutive pairs: 2-byte accesses to one row's
+        // 64-byte run, conflict-free.
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
-        if (t0 + rt < d.ke) {  // key t0 + rt at position t0 + rt; both 64-column halves
-          uint8_t* k0 = smem + stage * kStageBytes + rt * 128;
+        float cs, sn;
+        rope_sincos(t0 + rgrp, f[ri], sn, cs);
+        uint8_t* kst = smem + stage * kStageBytes;
+        const int cofs = (ri & 7) << 1;  // byte offset of element ri inside its 16-byte chunk
+        using T = typename std::conditional<kF16, __half, __nv_bfloat16>::type;
+#pragma unroll 1
+        for (int r0 = rgrp; r0 < kTile; r0 += 32) {  // 8 rows per batch: loads, math, stores
+          T xv[8], yv[8];                             // (explicit batches: a store does not block
+#pragma unroll                                        //  the next rows' loads on may-alias)
+          for (int u = 0; u < 8; ++u) {
+            const int r = r0 + 4 * u;
+            const int off = r * 128 + (((ri >> 3) ^ (r & 7)) << 4) + cofs;
+            xv[u] = *reinterpret_cast<const T*>(kst + off);
+            yv[u] = *reinterpret_cast<const T*>(kst + kHalfBytes + off);
+          }
 #pragma unroll
-          for (int ch = 0; ch < 8; ++ch) {
-            const int off = (ch ^ (rt & 7)) << 4;
-            rope_chunk<kF16>(k0 + off, k0 + kHalfBytes + off, t0 + rt, f, ch * 8);
+          for (int u = 0; u < 8; ++u) {
+            const float x = to_f<T>(xv[u]), y = to_f<T>(yv[u]);
+            xv[u] = from_float<T>(x * cs - y * sn);
+            yv[u] = from_float<T>(y * cs + x * sn);
+            const float c1 = cs * c2 - sn * s2;  // angle += 4 theta_i
+            sn = sn * c2 + cs * s2;
+            cs = c1;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = r0 + 4 * u;
+            const int off = r * 128 + (((ri >> 3) ^ (r & 7)) << 4) + cofs;
+            *reinterpret_cast<T*>(kst + off) = xv[u];
+            *reinterpret_cast<T*>(kst + kHalfBytes + off) = yv[u];
           }
         }
         ptx::fence_proxy_async();
-        ptx::named_bar_sync(3, 128);
+        ptx::named_bar_sync(3, 256);
         if (rt == 0) ptx::mbar_arrive(&krot[stage]);
         if (++stage == kStages) {
           stage = 0;

@@ -147,9 +147,13 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
   const int ps = L.page_size;
   // contiguous KV: any tile start is one 128-token box at a token coordinate
   const int B = L.ragged ? 128 : std::min(ps, 128);
-  if (!L.ragged) {
-    if (!(ps >= 8 && (128 % ps == 0 || ps % 128 == 0))) { *why = "page size must divide 128 (>= 8) or be a multiple of 128"; return 0; }
-    if (L.align % B) { *why = "chunk alignment not a multiple of the page box"; return 0; }
+  // pages a TMA box cannot tile (B_c < 8, or B_c neither dividing nor a multiple of 128): decode
+  // tiles gather rows with 16-byte cp.async instead (any page size, any chunk alignment)
+  const bool box_ok = L.ragged || (ps >= 8 && (128 % ps == 0 || ps % 128 == 0) && L.align % B == 0);
+  const bool cp_gather = L.T_q == 16 && !L.f8kv && (!box_ok || L.force_cp);
+  if (!box_ok && !cp_gather) {
+    *why = "page size must divide 128 (>= 8) or be a multiple of 128 (prefill / fp8 tiles)";
+    return 0;
   }
   if (L.T_q == 16) {
     TcParams tp;
@@ -160,7 +164,9 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     tp.q_tb = g <= 16 ? 16 / g : 1;
     tp.f16 = L.f16;
     tp.pdl = L.pdl;
-    if (!make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) || !make_kv_maps(tp, p, L, B)) {
+    tp.cp = cp_gather ? 1 : 0;
+    if (!make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) ||
+        (!cp_gather && !make_kv_maps(tp, p, L, B))) {
       *why = "cuTensorMapEncodeTiled failed";
       return -1;
     }

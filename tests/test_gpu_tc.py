@@ -216,3 +216,59 @@ def test_tc_pdl_back_to_back_layers(cuda_device, tile_q):
         inp.kv_page_indices = i0.kv_page_indices
         assert_close((o.float().cpu().numpy(), l.cpu().numpy()), oracle.attention_from_inputs(inp), "bf16",
                      what="pdl layer")
+
+
+# ---- cp.async row gather: page sizes a TMA box cannot tile (P:138-139 arbitrary B_c)
+def _cp_case(cuda_device, *, ps, layout="NHD", dtype="bf16", mask="none", qo=None, kv=None, nc=37, extra=None):
+    kv = np.array(kv if kv is not None else [1, 2, 127, 129, 1000, 2049], np.int32)
+    qo = np.array(qo if qo is not None else [1] * len(kv), np.int32)
+    wl = synth.Workload("cp", 32, 8, 128, ps, dtype, mask, qo, kv)
+    inp = synth.make_inputs(wl, device=cuda_device, layout=layout)
+    gpu = run_gpu(inp, num_ctas=nc, tile_q=16, kernel="tc", **(extra or {}))
+    assert gpu[2].selected_kernel() == "tc_decode"
+    assert_close(gpu, oracle.attention_from_inputs(inp), dtype, what=f"cp gather ps={ps} {layout}")
+    return gpu
+
+
+@pytest.mark.parametrize("ps", [1, 2, 4, 5, 48, 200])
+def test_tc_decode_cp_gather_page_sizes(cuda_device, ps):
+    _cp_case(cuda_device, ps=ps)
+
+
+@pytest.mark.parametrize("nc", [1, 148])
+def test_tc_decode_cp_gather_split_and_layouts(cuda_device, nc):
+    _cp_case(cuda_device, ps=1, layout="HND", dtype="f16", nc=nc, kv=[3000, 5, 700])
+    _cp_case(cuda_device, ps=4, mask="causal", qo=[1, 4, 2], kv=[9, 300, 700], nc=nc)
+
+
+def test_tc_decode_cp_gather_bitwise_equals_tma(cuda_device):
+    """BSRA_FLAG_CP_GATHER at B_c = 16 (where TMA boxes apply): same plan, the same values land in
+    the same swizzled shared-memory rows, so o and lse are bitwise identical to the TMA gather."""
+    import torch
+    import paper_2501_01005_b200 as bsra
+    wl = synth.Workload("cpb", 32, 8, 128, 16, "bf16", "none", np.ones(5, np.int32),
+                        np.array([1, 129, 700, 2049, 4096], np.int32))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    outs = []
+    for cp in (False, True):
+        cfg = bsra.make_config(H_qo=32, H_kv=8, D=128, page_size=16, dtype="bf16", max_batch=5, max_total_qo_rows=5,
+                               num_ctas=148, tile_q=16, cp_gather=cp)
+        o, lse, eng = run_gpu(inp, bsra.Engine(cfg, 0))
+        outs.append((o, lse))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    del torch
+
+
+def test_c2_page_size_1_full_size_sampled(cuda_device):
+    """configs[1] with page size 1 (151,721 one-token pages, the App. B setting P:436) on the
+    tensor-core decode kernel; sampled requests."""
+    import dataclasses
+    from tests.helpers import rows_of_requests
+    wl = dataclasses.replace(synth.c2_decode_llama8b(), page_size=1)
+    inp = synth.make_inputs(wl, device=cuda_device)
+    gpu = run_gpu(inp, num_ctas=148, tile_q=16)
+    assert gpu[2].selected_kernel() == "tc_decode"
+    order = np.argsort(wl.kv_lens)
+    reqs = sorted({int(order[0]), int(order[64]), int(order[-1])})
+    assert_close(gpu, oracle.attention_from_inputs(inp, req_list=reqs), "bf16", rows=rows_of_requests(inp, reqs),
+                 what="c2 ps=1")
