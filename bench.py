@@ -384,8 +384,13 @@ def bench_contiguous(dev, pk, reps=9):
         if tq == 16:  # decode: the cp.async row gather at B_c = 16 and at B_c = 1 (P:436's setting)
             ce = bsra.Engine(bsra.make_config(page_size=wl.page_size, cp_gather=True, **kw), torch.cuda.current_device())
             ce.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
-            out[key]["paged_cp_gather_us"] = timed(lambda: ce.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides,
-                                                                  inp.v_strides, inp.kv_page_indices, o, lse))
+            out[key]["paged_row_gather4_us"] = timed(lambda: ce.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides,
+                                                                    inp.v_strides, inp.kv_page_indices, o, lse))
+            ca = bsra.Engine(bsra.make_config(page_size=wl.page_size, cp_gather=True, cp_async=True, **kw),
+                             torch.cuda.current_device())
+            ca.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+            out[key]["paged_row_cp_async_us"] = timed(lambda: ca.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides,
+                                                                     inp.v_strides, inp.kv_page_indices, o, lse))
             import dataclasses
             wl1 = dataclasses.replace(wl, page_size=1)
             i1 = synth.make_inputs(wl1, device=dev)
@@ -395,7 +400,7 @@ def bench_contiguous(dev, pk, reps=9):
                                                                     i1.v_strides, i1.kv_page_indices, o, lse))
             out[key]["page_size_1_overhead_pct"] = 100.0 * (out[key]["paged_page_size_1_us"] / contig - 1.0)
             out[key]["page_size_1_kernel"] = e1.selected_kernel()
-            del ce, i1, e1
+            del ce, ca, i1, e1
         del inp, rk, pe, re_, o, lse
         torch.cuda.empty_cache()
     return out

@@ -143,12 +143,16 @@ typedef struct {
  * 1.25x the mean; 144 queues give exactly 4.0). Costs ~c Algorithm-1 runs of host time per
  * plan, so it is off by default. */
 #define BSRA_FLAG_BALANCE_CTAS 4
-/* flags: BSRA_FLAG_CP_GATHER makes the tcgen05 decode kernel gather K/V rows with 16-byte cp.async
- * (4 token rows x 128 B per warp instruction, zero-filled past the chunk) for every page size,
- * instead of one TMA box per (page, 64-column half). The cp.async gather is always used where a
- * TMA box cannot tile the page (B_c < 8, or B_c neither dividing nor a multiple of 128, paged
- * engines); the flag forces it elsewhere (the page-gather study of DESIGN.md). */
+/* flags: BSRA_FLAG_CP_GATHER makes the tcgen05 decode kernel gather K/V token ROWS for every page
+ * size, instead of one TMA box per (page, 64-column half): TMA tile::gather4 (4 rows of the pool
+ * viewed as a 2-D [rows, head_dim] tensor per instruction) when K and V share strides that are
+ * whole head_dim rows (NHD / HND pools), else 16-byte cp.async (4 token rows x 128 B per warp
+ * instruction, zero-filled past the chunk). The row gather is always used where a TMA box cannot
+ * tile the page (B_c < 8, or B_c neither dividing nor a multiple of 128; paged decode tiles); the
+ * flag forces it elsewhere (the page-gather study of DESIGN.md). BSRA_FLAG_CP_ASYNC forces the
+ * cp.async flavour of the row gather (A/B and tests). */
 #define BSRA_FLAG_CP_GATHER 8
+#define BSRA_FLAG_CP_ASYNC 16
 
 typedef struct bsra_engine bsra_engine;
 

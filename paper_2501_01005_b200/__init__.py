@@ -46,7 +46,8 @@ class Config(ctypes.Structure):
 FLAG_PDL = 1  # BSRA_FLAG_PDL (include/bsra.h)
 FLAG_RAGGED_KV = 2  # BSRA_FLAG_RAGGED_KV: contiguous (ragged) K/V, no page table
 FLAG_BALANCE_CTAS = 4  # BSRA_FLAG_BALANCE_CTAS: plan with the queue count that minimises the makespan
-FLAG_CP_GATHER = 8  # BSRA_FLAG_CP_GATHER: decode kernel gathers K/V rows with cp.async
+FLAG_CP_GATHER = 8  # BSRA_FLAG_CP_GATHER: decode kernel gathers K/V rows (TMA gather4 or cp.async)
+FLAG_CP_ASYNC = 16  # BSRA_FLAG_CP_ASYNC: ... with 16-byte cp.async
 
 
 _lib = None
@@ -120,7 +121,7 @@ def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="n
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
                 kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False, window=0,
                 soft_cap=0.0, kv_dtype=None, k_scale=0.0, v_scale=0.0, alibi=False, balance_ctas=False,
-                max_total_kv_tokens=0, max_qo_len=0, rope_theta=0.0, rope_scale=0.0, cp_gather=False) -> Config:
+                max_total_kv_tokens=0, max_qo_len=0, rope_theta=0.0, rope_scale=0.0, cp_gather=False, cp_async=False) -> Config:
     """window: sliding window W (0 = off, DESIGN.md R26); soft_cap: logits soft-cap c (0 = off, R27);
     kv_dtype "e4m3": fp8 KV cache with per-tensor scales k_scale / v_scale (0 = 1; R28);
     max_total_kv_tokens / max_qo_len: engine bounds (include/bsra.h)."""
@@ -133,7 +134,7 @@ def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="n
     c.alibi = 1 if alibi else 0
     c.sliding_window, c.logits_soft_cap = int(window), float(soft_cap)
     c.flags = ((FLAG_PDL if pdl else 0) | (FLAG_RAGGED_KV if ragged_kv else 0) | (FLAG_BALANCE_CTAS if balance_ctas else 0)
-               | (FLAG_CP_GATHER if cp_gather else 0))
+               | (FLAG_CP_GATHER if cp_gather else 0) | (FLAG_CP_ASYNC if cp_async else 0))
     c.num_qo_heads, c.num_kv_heads, c.head_dim, c.page_size = H_qo, H_kv, D, page_size
     c.dtype = DTYPE[dtype] if isinstance(dtype, str) else dtype
     od = o_dtype if o_dtype is not None else dtype

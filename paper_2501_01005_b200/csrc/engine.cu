@@ -72,7 +72,8 @@ bsra_status validate_config(const bsra_config& c) {
   if (c.cost_alpha < 0 || c.cost_beta < 0) return fail(BSRA_EINVAL, "negative cost parameters");
   if (c.kv_chunk_align < 0 || c.kv_chunk_min < 0) return fail(BSRA_EINVAL, "negative chunk parameters");
   if (c.kernel < BSRA_KERNEL_AUTO || c.kernel > BSRA_KERNEL_TC) return fail(BSRA_EINVAL, "bad kernel selector");
-  if (c.flags & ~(BSRA_FLAG_PDL | BSRA_FLAG_RAGGED_KV | BSRA_FLAG_BALANCE_CTAS | BSRA_FLAG_CP_GATHER))
+  if (c.flags & ~(BSRA_FLAG_PDL | BSRA_FLAG_RAGGED_KV | BSRA_FLAG_BALANCE_CTAS | BSRA_FLAG_CP_GATHER |
+                  BSRA_FLAG_CP_ASYNC))
     return fail(BSRA_EINVAL, "unknown flag bits");
   if ((c.flags & BSRA_FLAG_RAGGED_KV) && c.page_size != 128)
     return fail(BSRA_EINVAL, "BSRA_FLAG_RAGGED_KV engines take page_size = 128 (the KV tile)");
@@ -653,7 +654,8 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     tl.total_kv = kv_extent;
     tl.f8kv = !kv16;
     tl.rope = p.rope != 0;
-    tl.force_cp = (c.flags & BSRA_FLAG_CP_GATHER) != 0;
+    tl.force_cp = (c.flags & (BSRA_FLAG_CP_GATHER | BSRA_FLAG_CP_ASYNC)) != 0;
+    tl.force_cp_async = (c.flags & BSRA_FLAG_CP_ASYNC) != 0;
     const char* why = "";
     int rc = bsra::tc_launch(p, tl, st, &e->selected, &why);
     if (rc < 0)

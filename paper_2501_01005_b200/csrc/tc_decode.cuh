@@ -47,7 +47,8 @@ struct TcParams {
   int32_t q_hb, q_tb;
   int32_t f16;      // 1 = fp16 inputs, 0 = bf16
   int32_t pdl;      // launched with programmatic dependent launch (host-side launch choice)
-  int32_t cp;       // decode: gather K/V rows with 16-byte cp.async (any page size) instead of TMA boxes
+  int32_t cp;       // decode K/V gather: 0 = TMA boxes per page, 1 = 16-byte cp.async rows, 2 = TMA gather4 rows
+  int64_t row_s0, row_s1, row_s2;  // gather4: (page, slot, head) strides in rows of the 2-D [rows, D] view
   int32_t dbg;      // BSRA_EXPERIMENTS builds only ($BSRA_DEBUG_PREFILL timing modes); 0 otherwise
 };
 
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], tp.cp ? 32 : 1);  // cp.async gather: one arrival per producer lane
+      ptx::mbar_init(&full[s], tp.cp == 1 ? 32 : 1);  // cp.async gather: one arrival per producer lane
       ptx::mbar_init(&empty[s], 1);
       ptx::mbar_init(&krot[s], 1);
     }
@@ -243,7 +244,31 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       // ---- K/V tiles
       for (int ti = 0; ti < d.ntiles; ++ti) {
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
-        if (tp.cp) {
+        if (tp.cp == 2) {
+          // TMA gather4 (sm_100): the K/V pools as 2-D [rows, D] tensors (a (page, slot, head) row
+          // is D contiguous elements); lane l loads token rows 4l .. 4l+3 of the tile, both
+          // 64-column halves of K and V: 4 instructions per lane, 128 per 64 KB tile, any page
+          // size. Rows past the chunk repeat its last row (masked in S, zeroed in V).
+          int rows[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int64_t t = imin64(t0 + 4 * lane + j, d.ke - 1);
+            const int64_t pg = __ldg(p.page_indices + d.page_begin + t / p.page_size);
+            rows[j] = (int)(pg * tp.row_s0 + (t % p.page_size) * tp.row_s1 + d.kvh * tp.row_s2);
+          }
+          if (lane == 0) {
+            ptx::mbar_wait(&empty[stage], ephase);
+            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)kStageBytes);
+          }
+          __syncwarp();
+          uint8_t* kd = smem + stage * kStageBytes + lane * 4 * 128;
+          uint8_t* vd = kd + kKVBytes;
+          ptx::tma_gather4(kd, &tp.tk, &full[stage], 0, rows[0], rows[1], rows[2], rows[3]);
+          ptx::tma_gather4(kd + kHalfBytes, &tp.tk, &full[stage], 64, rows[0], rows[1], rows[2], rows[3]);
+          ptx::tma_gather4(vd, &tp.tv, &full[stage], 0, rows[0], rows[1], rows[2], rows[3]);
+          ptx::tma_gather4(vd + kHalfBytes, &tp.tv, &full[stage], 64, rows[0], rows[1], rows[2], rows[3]);
+          __syncwarp();
+        } else if (tp.cp == 1) {
           // 16-byte cp.async gather, any page size (small pages, B_c not dividing 128): per
           // instruction the warp moves 4 token rows x 128 B (lane = chunk c of row sub), written
           // at the SW128 position TMA would use; rows past the chunk are zero-filled (no read).
@@ -369,7 +394,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ptx::mbar_wait(kRope ? &krot[stage] : &full[stage], fphase);
         ptx::mbar_wait(&s_free[sb], sfph[sb]);
         sfph[sb] ^= 1;
-        if (tp.cp) ptx::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core reads
+        if (tp.cp == 1) ptx::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core reads
         ptx::tc_fence_after();
         const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes, 16, 1024);
 #pragma unroll

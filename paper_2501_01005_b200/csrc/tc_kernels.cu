@@ -63,6 +63,20 @@ bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int64_t
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// pool as a 2-D tensor [rows, 128] (a row = one (page, slot, head) of D = 128 contiguous elements)
+// for TMA gather4: box {64 columns, 1 row}, 128B swizzle; 4 rows per instruction
+bool make_row_map(CUtensorMap* m, const void* pool, bool f16) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {128, 0x7fffffffull};
+  cuuint64_t strides[1] = {128 * 2};
+  cuuint32_t box[2] = {64, 1};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int kC, int kMask, bool kF8, bool kRope = false>
 cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
   static bool attr = false;
@@ -151,6 +165,10 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
   // tiles gather rows with 16-byte cp.async instead (any page size, any chunk alignment)
   const bool box_ok = L.ragged || (ps >= 8 && (128 % ps == 0 || ps % 128 == 0) && L.align % B == 0);
   const bool cp_gather = L.T_q == 16 && !L.f8kv && (!box_ok || L.force_cp);
+  // row gather flavour: TMA gather4 when K and V share strides that are whole D-element rows (the
+  // NHD / HND pools), else 16-byte cp.async
+  const bool rows_ok = !L.ragged && p.ks0 == p.vs0 && p.ks1 == p.vs1 && p.ks2 == p.vs2 && p.ks0 % 128 == 0 &&
+                       p.ks1 % 128 == 0 && p.ks2 % 128 == 0;
   if (!box_ok && !cp_gather) {
     *why = "page size must divide 128 (>= 8) or be a multiple of 128 (prefill / fp8 tiles)";
     return 0;
@@ -164,9 +182,16 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     tp.q_tb = g <= 16 ? 16 / g : 1;
     tp.f16 = L.f16;
     tp.pdl = L.pdl;
-    tp.cp = cp_gather ? 1 : 0;
-    if (!make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb) ||
-        (!cp_gather && !make_kv_maps(tp, p, L, B))) {
+    tp.cp = cp_gather ? (rows_ok && !L.force_cp_async ? 2 : 1) : 0;
+    bool maps_ok = make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb);
+    if (tp.cp == 0) maps_ok = maps_ok && make_kv_maps(tp, p, L, B);
+    if (tp.cp == 2) {
+      tp.row_s0 = p.ks0 / 128;
+      tp.row_s1 = p.ks1 / 128;
+      tp.row_s2 = p.ks2 / 128;
+      maps_ok = maps_ok && make_row_map(&tp.tk, p.k, L.f16) && make_row_map(&tp.tv, p.v, L.f16);
+    }
+    if (!maps_ok) {
       *why = "cuTensorMapEncodeTiled failed";
       return -1;
     }

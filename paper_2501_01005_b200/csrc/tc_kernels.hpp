@@ -20,7 +20,8 @@ struct TcLaunch {
   int64_t total_kv = 0;    // ragged: the token extent of the k / v maps
   bool f8kv = false;       // K/V pools in E4M3 (fp8 KV cache, R28)
   bool rope = false;       // fused RoPE (R31): decode tiles only
-  bool force_cp = false;   // decode: cp.async row gather even where TMA boxes apply (BSRA_FLAG_CP_GATHER)
+  bool force_cp = false;   // decode: row gather even where TMA boxes apply (BSRA_FLAG_CP_GATHER)
+  bool force_cp_async = false;  // row gather by cp.async even where TMA gather4 applies (tests, A/B)
 };
 
 // Launches the tcgen05 kernel for this plan if one applies (bf16/f16, D = 128, supported page

@@ -11,14 +11,15 @@ TOL = {"f32": (1e-5, 1e-5), "f16": (1e-2, 1e-3), "bf16": (1e-2, 1e-3)}  # fp8 KV
 
 
 def engine_for(wl, *, num_ctas=0, tile_q=0, tile_set=(16, 64, 128, 256), kernel="auto", o_dtype=None, max_batch=None,
-               max_rows=None, max_kv=None, device=0, cp_gather=False):
+               max_rows=None, max_kv=None, device=0, cp_gather=False, cp_async=False):
     cfg = bsra.make_config(H_qo=wl.H_qo, H_kv=wl.H_kv, D=wl.D, page_size=wl.page_size, dtype=wl.dtype,
                            o_dtype=o_dtype, mask=wl.mask, max_batch=max_batch or max(1, wl.batch),
                            max_total_qo_rows=max_rows or max(1, int(wl.qo_lens.sum())), num_ctas=num_ctas,
                            tile_set=tile_set, tile_q=tile_q, kernel=kernel, kv_dtype=wl.kv_dtype or None,
                            window=wl.window, soft_cap=wl.soft_cap, alibi=wl.alibi,
                            max_total_kv_tokens=max(0, max_kv) if max_kv is not None else int(wl.kv_lens.astype(np.int64).sum()),
-                           cp_gather=cp_gather, rope_theta=wl.rope_theta, rope_scale=wl.rope_scale)
+                           cp_gather=cp_gather, cp_async=cp_async, rope_theta=wl.rope_theta,
+                           rope_scale=wl.rope_scale)
     return bsra.Engine(cfg, device)
 
 

@@ -220,6 +220,7 @@ def test_tc_pdl_back_to_back_layers(cuda_device, tile_q):
 
 # ---- cp.async row gather: page sizes a TMA box cannot tile (P:138-139 arbitrary B_c)
 def _cp_case(cuda_device, *, ps, layout="NHD", dtype="bf16", mask="none", qo=None, kv=None, nc=37, extra=None):
+    """extra: engine_for keywords (cp_async forces the cp.async flavour of the row gather)."""
     kv = np.array(kv if kv is not None else [1, 2, 127, 129, 1000, 2049], np.int32)
     qo = np.array(qo if qo is not None else [1] * len(kv), np.int32)
     wl = synth.Workload("cp", 32, 8, 128, ps, dtype, mask, qo, kv)
@@ -230,9 +231,10 @@ def _cp_case(cuda_device, *, ps, layout="NHD", dtype="bf16", mask="none", qo=Non
     return gpu
 
 
+@pytest.mark.parametrize("cp_async", [False, True], ids=["gather4", "cp_async"])
 @pytest.mark.parametrize("ps", [1, 2, 4, 5, 48, 200])
-def test_tc_decode_cp_gather_page_sizes(cuda_device, ps):
-    _cp_case(cuda_device, ps=ps)
+def test_tc_decode_cp_gather_page_sizes(cuda_device, ps, cp_async):
+    _cp_case(cuda_device, ps=ps, extra=dict(cp_async=cp_async))
 
 
 @pytest.mark.parametrize("nc", [1, 148])
@@ -250,12 +252,13 @@ def test_tc_decode_cp_gather_bitwise_equals_tma(cuda_device):
                         np.array([1, 129, 700, 2049, 4096], np.int32))
     inp = synth.make_inputs(wl, device=cuda_device)
     outs = []
-    for cp in (False, True):
+    for cp, ca in ((False, False), (True, False), (True, True)):  # TMA boxes, gather4, cp.async
         cfg = bsra.make_config(H_qo=32, H_kv=8, D=128, page_size=16, dtype="bf16", max_batch=5, max_total_qo_rows=5,
-                               num_ctas=148, tile_q=16, cp_gather=cp)
+                               num_ctas=148, tile_q=16, cp_gather=cp, cp_async=ca)
         o, lse, eng = run_gpu(inp, bsra.Engine(cfg, 0))
         outs.append((o, lse))
-    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    for k in (1, 2):
+        assert np.array_equal(outs[0][0], outs[k][0]) and np.array_equal(outs[0][1], outs[k][1])
     del torch
 
 
