@@ -144,7 +144,9 @@ __device__ __forceinline__ void rope_chunk(uint8_t* lo, uint8_t* hi, int64_t pos
 // fetch stalls measured on the fp8 kernel when both were inlined). kRope: fused RoPE (R31) —
 // eight more warps rotate each landed K tile in shared memory and each item's Q tile before the
 // MMA warp reads them (krot / qrot barriers replace full / full_q for S).
-template <int kC, int kMask, bool kF16, bool kRope>
+// kRow: K/V row gather (tp.cp = 1 cp.async, 2 TMA gather4) instead of per-page TMA boxes — its own
+// instantiation, so the box kernel carries none of that code.
+template <int kC, int kMask, bool kF16, bool kRope, bool kRow = false>
 __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
   using namespace dec;
   const AttnParams& p = tp.p;
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], tp.cp == 1 ? 32 : 1);  // cp.async gather: one arrival per producer lane
+      ptx::mbar_init(&full[s], kRow && tp.cp == 1 ? 32 : 1);  // cp.async gather: one arrival per lane
       ptx::mbar_init(&empty[s], 1);
       ptx::mbar_init(&krot[s], 1);
     }
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       // ---- K/V tiles
       for (int ti = 0; ti < d.ntiles; ++ti) {
         const int64_t t0 = d.kb + (int64_t)ti * kTile;
-        if (tp.cp == 2) {
+        if (kRow && tp.cp == 2) {
           // TMA gather4 (sm_100): the K/V pools as 2-D [rows, D] tensors (a (page, slot, head) row
           // is D contiguous elements); lane l loads token rows 4l .. 4l+3 of the tile, both
           // 64-column halves of K and V: 4 instructions per lane, 128 per 64 KB tile, any page
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           ptx::tma_gather4(vd, &tp.tv, &full[stage], 0, rows[0], rows[1], rows[2], rows[3]);
           ptx::tma_gather4(vd + kHalfBytes, &tp.tv, &full[stage], 64, rows[0], rows[1], rows[2], rows[3]);
           __syncwarp();
-        } else if (tp.cp == 1) {
+        } else if (kRow) {
           // 16-byte cp.async gather, any page size (small pages, B_c not dividing 128): per
           // instruction the warp moves 4 token rows x 128 B (lane = chunk c of row sub), written
           // at the SW128 position TMA would use; rows past the chunk are zero-filled (no read).
@@ -394,7 +396,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ptx::mbar_wait(kRope ? &krot[stage] : &full[stage], fphase);
         ptx::mbar_wait(&s_free[sb], sfph[sb]);
         sfph[sb] ^= 1;
-        if (tp.cp == 1) ptx::fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core reads
+        if (kRow && tp.cp == 1) ptx::fence_proxy_async();  // cp.async (generic-proxy) writes -> tensor core
         ptx::tc_fence_after();
         const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes, 16, 1024);
 #pragma unroll

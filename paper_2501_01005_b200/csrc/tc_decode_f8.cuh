@@ -68,7 +68,7 @@ constexpr uint32_t kTmemCols = 256;             // S^T 0 / 16, O^T 32 / 48 (item
 constexpr uint32_t kColO = 32, kColK = 64;
 constexpr float kRescaleThresh = 8.f;
 static_assert(kSmemBytes <= 227 * 1024, "one CTA per SM");
-static_assert(8 * (2 * kF8St + 2 * kKSt + 2 * kVSt + 16) + 8 <= kOffRed - kOffBar, "mbarrier area");
+static_assert(8 * (2 * kF8St + 2 * kKSt + 2 * kVSt + 18) + 8 <= kOffRed - kOffBar, "mbarrier area");
 }  // namespace f8d
 
 __device__ __forceinline__ int imin(int a, int b) { return a < b ? a : b; }
@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
   uint64_t* o_free = q_ready + 2;         // [2] epilogue read O^T buffer b (1 arrival)
   uint64_t* epi_full = o_free + 2;        // [2] item's row sums / max handed over (4 warps)
   uint64_t* epi_empty = epi_full + 2;     // [2] epilogue consumed hand-off buffer b (1 arrival)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(epi_empty + 2);
+  uint64_t* o_full = epi_empty + 2;       // [2] the item's last PV into O^T buffer b completed (commit)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
   float* red = reinterpret_cast<float*>(smem + kOffRed);
   int* vflags = reinterpret_cast<int*>(red + 4 * kN);  // [2][4] vote flags
   float* hsum = reinterpret_cast<float*>(vflags + 8);   // [2][4 warps][kN]
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
       ptx::mbar_init(&o_free[b], 1);
       ptx::mbar_init(&epi_full[b], 4);
       ptx::mbar_init(&epi_empty[b], 1);
+      ptx::mbar_init(&o_full[b], 1);
     }
     ptx::fence_barrier_init();
   }
@@ -372,9 +374,19 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
     uint32_t kph = 0, vph = 0;
     uint32_t ofph[2] = {1, 1};
     uint32_t sfph[2] = {1, 1}, pfph[2] = {0, 0}, qrph[2] = {0, 0};
-    auto issue_pv = [&](int ti) {  // PV of the item's tile ti (P^T buffer pb, V stage vst)
+    // One flat tile stream across items (as tc_decode): the next item's first S goes out before
+    // the previous item's last PV, and the epilogue waits for that PV on o_full.
+    struct PendingPV {
+      int ti, ob;
+      bool last, valid;
+    } pend = {0, 0, false, false};
+    auto issue_pv = [&](const PendingPV& x) {  // PV of tile x.ti of an item (P^T buffer pb, V stage vst)
       ptx::mbar_wait(&p_full[pb], pfph[pb]);
       pfph[pb] ^= 1;
+      if (x.ti == 0) {  // the item's first PV overwrites O[ob]: the epilogue two items back read it
+        ptx::mbar_wait(&o_free[x.ob], ofph[x.ob]);
+        ofph[x.ob] ^= 1;
+      }
       ptx::mbar_wait(&vfull[vst], vph);
       ptx::tc_fence_after();
       const uint64_t a0 = ptx::smem_desc_sw128(sbase + kOffV + vst * kVBytes, kHalfBytes, 1024);
@@ -382,11 +394,12 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t sbo = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
-        ptx::mma_f16_ss_warp(tmem + kColO + ob * 16, a0 + (uint64_t)(kk * 128), b0 + sbo, idO,
-                             (ti > 0 || kk > 0) ? 1u : 0u);
+        ptx::mma_f16_ss_warp(tmem + kColO + x.ob * 16, a0 + (uint64_t)(kk * 128), b0 + sbo, idO,
+                             (x.ti > 0 || kk > 0) ? 1u : 0u);
       }
       ptx::mma_commit_warp(&vempty[vst]);
       ptx::mma_commit_warp(&bar_pv[pb]);
+      if (x.last) ptx::mma_commit_warp(&o_full[x.ob]);  // O[ob] final: the epilogue may read it
       if (++vst == kVSt) {
         vst = 0;
         vph ^= 1;
@@ -422,18 +435,14 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
           kph ^= 1;
         }
         sb ^= 1;
-        // ---- PV of the previous tile (its P is being written while S(ti) runs)
-        if (ti == 0) {  // the item's first PV overwrites O[ob]: the epilogue two items back read it
-          ptx::mbar_wait(&o_free[ob], ofph[ob]);
-          ofph[ob] ^= 1;
-        } else {
-          issue_pv(ti - 1);
-        }
+        // ---- PV of the previous tile in the stream (its P is being written while S(ti) runs)
+        if (pend.valid) issue_pv(pend);
+        pend = {ti, ob, ti + 1 == d.ntiles, true};
       }
-      issue_pv(d.ntiles - 1);
       qb ^= 1;
       ob ^= 1;
     }
+    if (pend.valid) issue_pv(pend);
   } else if (warp < kWM) {
     // ========================== softmax warps (9..12) ==========================
     const int ct = threadIdx.x - 32 * kWS0;
@@ -601,9 +610,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
         pbuf ^= 1;
         sbuf ^= 1;
       }
-      wait_pv(0);
-      wait_pv(1);  // every PV of the item completed: O[ob] is final
-      qb ^= 1;
+      qb ^= 1;  // (the item's last PV may still run: the epilogue waits for it on o_full)
       // ---- hand the item to the epilogue warps: per-warp row-sum partials and the running max
       float x[kC];
 #pragma unroll
@@ -643,6 +650,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
       float ov[kC], l[kC], mm[kC];
       if (d.ntiles > 0) {
         ptx::mbar_wait(&epi_full[ob], efph[ob]);
+        ptx::mbar_wait(&o_full[ob], efph[ob]);  // the item's last PV completed
         efph[ob] ^= 1;
         ptx::tc_fence_after();
         ptx::tmem_ld<kC>(tmem + lane_addr + kColO + ob * 16, ov);

@@ -77,7 +77,7 @@ bool make_row_map(CUtensorMap* m, const void* pool, bool f16) {
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int kC, int kMask, bool kF8, bool kRope = false>
+template <int kC, int kMask, bool kF8, bool kRope = false, bool kRow = false>
 cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
   static bool attr = false;
   if constexpr (kF8) {  // fp8 KV cache: K in TMEM, converter warps (tc_decode_f8.cuh)
@@ -94,23 +94,30 @@ cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
     return launch_tc(tc_decode_f8_kernel<kC, kMask, false>, grid, f8d::threads_for(kC), f8d::kSmemBytes, st, tp);
   } else {
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false, kRope>,
+    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false, kRope, kRow>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true, kRope>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             dec::kSmemBytes);
+    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true, kRope, kRow>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int nt = dec::threads_for(kRope);
-  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true, kRope>, grid, nt, dec::kSmemBytes, st, tp);
-  return launch_tc(tc_decode_kernel<kC, kMask, false, kRope>, grid, nt, dec::kSmemBytes, st, tp);
+  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true, kRope, kRow>, grid, nt, dec::kSmemBytes, st, tp);
+  return launch_tc(tc_decode_kernel<kC, kMask, false, kRope, kRow>, grid, nt, dec::kSmemBytes, st, tp);
   }
 }
 
 template <int kC, bool kF8>
 cudaError_t launch_decode_m(int mask, const TcParams& tp, int grid, cudaStream_t st) {
   if constexpr (!kF8) {
+    if (tp.cp) {  // row gather variant (page sizes TMA boxes cannot tile)
+      switch (mask) {
+        case 0: return launch_decode_t<kC, 0, false, false, true>(tp, grid, st);
+        case 1: return launch_decode_t<kC, 1, false, false, true>(tp, grid, st);
+        default: return launch_decode_t<kC, 2, false, false, true>(tp, grid, st);
+      }
+    }
     if (tp.p.rope) {  // fused RoPE variant (R31)
       switch (mask) {
         case 0: return launch_decode_t<kC, 0, false, true>(tp, grid, st);
@@ -164,13 +171,13 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
   // pages a TMA box cannot tile (B_c < 8, or B_c neither dividing nor a multiple of 128): decode
   // tiles gather rows with 16-byte cp.async instead (any page size, any chunk alignment)
   const bool box_ok = L.ragged || (ps >= 8 && (128 % ps == 0 || ps % 128 == 0) && L.align % B == 0);
-  const bool cp_gather = L.T_q == 16 && !L.f8kv && (!box_ok || L.force_cp);
+  const bool cp_gather = L.T_q == 16 && !L.f8kv && !L.rope && (!box_ok || L.force_cp);
   // row gather flavour: TMA gather4 when K and V share strides that are whole D-element rows (the
   // NHD / HND pools), else 16-byte cp.async
   const bool rows_ok = !L.ragged && p.ks0 == p.vs0 && p.ks1 == p.vs1 && p.ks2 == p.vs2 && p.ks0 % 128 == 0 &&
                        p.ks1 % 128 == 0 && p.ks2 % 128 == 0;
   if (!box_ok && !cp_gather) {
-    *why = "page size must divide 128 (>= 8) or be a multiple of 128 (prefill / fp8 tiles)";
+    *why = "page size must divide 128 (>= 8) or be a multiple of 128 (prefill / fp8 / RoPE tiles)";
     return 0;
   }
   if (L.T_q == 16) {

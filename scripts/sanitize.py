@@ -37,6 +37,14 @@ def main():
                             np.array([300, 17], np.int32), kv_dtype="e4m3"), dict(num_ctas=4, tile_q=16)),
         ("fp8 gather + prefill", W("f", 64, 8, 128, 16, "bf16", "causal", np.array([70, 1], np.int32),
                                    np.array([70, 300], np.int32), kv_dtype="e4m3"), dict(num_ctas=4, tile_q=128)),
+        ("tc_decode RoPE", W("r", 32, 8, 128, 16, "bf16", "causal", np.array([1, 3], np.int32),
+                             np.array([300, 70], np.int32), rope_theta=10000.0), dict(num_ctas=6, tile_q=16)),
+        ("tc_decode gather4 B_c=1", W("g", 32, 8, 128, 1, "bf16", "none", np.ones(2, np.int32),
+                                      np.array([200, 33], np.int32)), dict(num_ctas=4, tile_q=16)),
+        ("tc_decode cp.async B_c=4", W("c", 32, 8, 128, 4, "bf16", "none", np.ones(2, np.int32),
+                                       np.array([200, 33], np.int32)), dict(num_ctas=4, tile_q=16, cp_async=True)),
+        ("simt RoPE prefill", W("s", 32, 8, 128, 16, "bf16", "causal", np.array([20, 1], np.int32),
+                                np.array([20, 90], np.int32), rope_theta=10000.0), dict(num_ctas=4, tile_q=64)),
     ]
     for name, wl, kw in cases:
         inp = synth.make_inputs(wl, device=dev)
