@@ -146,8 +146,11 @@ __device__ __forceinline__ void rope_chunk(uint8_t* lo, uint8_t* hi, int64_t pos
 // MMA warp reads them (krot / qrot barriers replace full / full_q for S).
 // kRow: K/V row gather (tp.cp = 1 cp.async, 2 TMA gather4) instead of per-page TMA boxes — its own
 // instantiation, so the box kernel carries none of that code.
-template <int kC, int kMask, bool kF16, bool kRope, bool kRow = false>
+// kD: head_dim 128 (two 64-column SW128 halves per row) or 64 (one half: the S MMA takes K = 64,
+// the PV MMA keeps M = 128 with O^T rows 64..127 unused and never stored).
+template <int kC, int kMask, bool kF16, bool kRope, bool kRow = false, int kD = 128>
 __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
+  static_assert(kD == 128 || (kD == 64 && !kRope && !kRow), "head_dim 64: box gather, no RoPE");
   using namespace dec;
   const AttnParams& p = tp.p;
   extern __shared__ uint8_t smem_raw[];
@@ -234,12 +237,12 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       // ---- Q tile: 16 fused rows = q_tb tokens x q_hb heads, two 64-column halves
       if (lane == 0) {
         ptx::mbar_wait(&empty_q[qb], qphase[qb]);
-        ptx::mbar_arrive_expect_tx(&full_q[qb], kQBytes);
+        ptx::mbar_arrive_expect_tx(&full_q[qb], kD == 128 ? kQBytes : kQBytes / 2);
         const int head0 = d.kvh * g + (g > kN ? d.row0 % g : 0);
         const int tok0 = (int)d.qo_begin + d.row0 / g;
         uint8_t* qdst = smem + kOffQ + qb * kQBytes;
         ptx::tma_load_3d(qdst, &tp.tq, &full_q[qb], 0, head0, tok0);
-        ptx::tma_load_3d(qdst + kN * 128, &tp.tq, &full_q[qb], 64, head0, tok0);
+        if (kD == 128) ptx::tma_load_3d(qdst + kN * 128, &tp.tq, &full_q[qb], 64, head0, tok0);
       }
       qphase[qb] ^= 1;
       qb ^= 1;
@@ -324,16 +327,16 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           }
           if (lane == 0) {
             ptx::mbar_wait(&empty[stage], ephase);
-            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * 512);
+            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * (kD * 4));
           }
           __syncwarp();
           if (lane < nsub) {
             uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
             uint8_t* vd = kd + kKVBytes;
             ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
-            ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
+            if (kD == 128) ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
             ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
-            ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
+            if (kD == 128) ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
           }
           __syncwarp();
         }
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ptx::tc_fence_after();
         const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes, 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
+        for (int kk = 0; kk < kD / 16; ++kk) {
           const uint64_t sa = (uint64_t)((kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2);
           const uint64_t sbo = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
           ptx::mma_f16_ss_warp(tmem + sb * 16, a0 + sa, bq + sbo, idS, kk > 0);
@@ -720,7 +723,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       }
 #pragma unroll
       for (int c = 0; c < kC; ++c) {
-        if (c < d.nrows) {
+        if (c < d.nrows && row < kD) {
           const bool empty_row = !(l[c] > 0.f);
           const float val = empty_row ? 0.f : ov[c] / l[c];
           const float lse = empty_row ? -INFINITY : (mm[c] + __log2f(l[c])) * kLn2;
@@ -728,21 +731,21 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           const int tok = f / g, head = d.kvh * g + f % g;
           if (d.slot < 0) {
             const int64_t orow = (d.qo_begin + tok) * p.H_qo + head;
-            if (p.o_f32) reinterpret_cast<float*>(p.o)[orow * 128 + row] = val;
-            else if constexpr (kF16) reinterpret_cast<__half*>(p.o)[orow * 128 + row] = __float2half_rn(val);
-            else reinterpret_cast<__nv_bfloat16*>(p.o)[orow * 128 + row] = __float2bfloat16_rn(val);
+            if (p.o_f32) reinterpret_cast<float*>(p.o)[orow * kD + row] = val;
+            else if constexpr (kF16) reinterpret_cast<__half*>(p.o)[orow * kD + row] = __float2half_rn(val);
+            else reinterpret_cast<__nv_bfloat16*>(p.o)[orow * kD + row] = __float2bfloat16_rn(val);
             if (p.lse && row == 0) p.lse[orow] = lse;
           } else {
             const int64_t prow = (int64_t)d.slot * p.T_slot + c;
-            p.part_o[prow * 128 + row] = val;
+            p.part_o[prow * kD + row] = val;
             if (row == 0) p.part_lse[prow] = lse;
           }
         }
       }
       if (d.slot >= 0 && p.fused_merge) {  // split item: the CTA completing its merge list folds it
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
-        if constexpr (kF16) fused_contraction<__half, 128>(p, pv, d.slot, et, 128, 2, s_flag);
-        else fused_contraction<__nv_bfloat16, 128>(p, pv, d.slot, et, 128, 2, s_flag);
+        if constexpr (kF16) fused_contraction<__half, kD>(p, pv, d.slot, et, 128, 2, s_flag);
+        else fused_contraction<__nv_bfloat16, kD>(p, pv, d.slot, et, 128, 2, s_flag);
       }
     }
   }

@@ -31,11 +31,11 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
 
 // q [N, H_qo, 128] contiguous: dims (d, head, token), box (64, hb, tb), 128B swizzle
-bool make_q_map(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, int hb, int tb) {
+bool make_q_map(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, int hb, int tb, int D = 128) {
   auto enc = get_encode();
   if (!enc) return false;
-  cuuint64_t dims[3] = {128, (cuuint64_t)H_qo, (cuuint64_t)std::max<int64_t>(N, 1)};
-  cuuint64_t strides[2] = {128 * 2, (cuuint64_t)H_qo * 128 * 2};
+  cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)H_qo, (cuuint64_t)std::max<int64_t>(N, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)D * 2, (cuuint64_t)H_qo * D * 2};
   cuuint32_t box[3] = {64, (cuuint32_t)hb, (cuuint32_t)tb};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(q),
@@ -48,11 +48,11 @@ bool make_q_map(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, in
 // Contiguous KV uses the same view with slot = token (extent N, clipped there) and one page.
 // f8: E4M3 pools (1-byte elements), box (128, 1, B, 1) = one 128-byte row per token.
 bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int64_t page_size, int64_t s0, int64_t s1,
-                   int64_t s2, int B, int64_t npages = 0x7fffffff, bool f8 = false) {
+                   int64_t s2, int B, int64_t npages = 0x7fffffff, bool f8 = false, int D = 128) {
   auto enc = get_encode();
   if (!enc) return false;
   const cuuint64_t es_b = f8 ? 1 : 2;
-  cuuint64_t dims[4] = {128, (cuuint64_t)H_kv, (cuuint64_t)std::max<int64_t>(page_size, 1), (cuuint64_t)npages};
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)H_kv, (cuuint64_t)std::max<int64_t>(page_size, 1), (cuuint64_t)npages};
   cuuint64_t strides[3] = {(cuuint64_t)s2 * es_b, (cuuint64_t)s1 * es_b, (cuuint64_t)s0 * es_b};
   cuuint32_t box[4] = {f8 ? 128u : 64u, 1, (cuuint32_t)B, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
@@ -77,7 +77,7 @@ bool make_row_map(CUtensorMap* m, const void* pool, bool f16) {
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int kC, int kMask, bool kF8, bool kRope = false, bool kRow = false>
+template <int kC, int kMask, bool kF8, bool kRope = false, bool kRow = false, int kD = 128>
 cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
   static bool attr = false;
   if constexpr (kF8) {  // fp8 KV cache: K in TMEM, converter warps (tc_decode_f8.cuh)
@@ -94,23 +94,30 @@ cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
     return launch_tc(tc_decode_f8_kernel<kC, kMask, false>, grid, f8d::threads_for(kC), f8d::kSmemBytes, st, tp);
   } else {
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false, kRope, kRow>,
+    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false, kRope, kRow, kD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true, kRope, kRow>,
+    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true, kRope, kRow, kD>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int nt = dec::threads_for(kRope);
-  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true, kRope, kRow>, grid, nt, dec::kSmemBytes, st, tp);
-  return launch_tc(tc_decode_kernel<kC, kMask, false, kRope, kRow>, grid, nt, dec::kSmemBytes, st, tp);
+  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true, kRope, kRow, kD>, grid, nt, dec::kSmemBytes, st, tp);
+  return launch_tc(tc_decode_kernel<kC, kMask, false, kRope, kRow, kD>, grid, nt, dec::kSmemBytes, st, tp);
   }
 }
 
 template <int kC, bool kF8>
 cudaError_t launch_decode_m(int mask, const TcParams& tp, int grid, cudaStream_t st) {
   if constexpr (!kF8) {
+    if (tp.p.D == 64) {  // head_dim 64 (box gather only)
+      switch (mask) {
+        case 0: return launch_decode_t<kC, 0, false, false, false, 64>(tp, grid, st);
+        case 1: return launch_decode_t<kC, 1, false, false, false, 64>(tp, grid, st);
+        default: return launch_decode_t<kC, 2, false, false, false, 64>(tp, grid, st);
+      }
+    }
     if (tp.cp) {  // row gather variant (page sizes TMA boxes cannot tile)
       switch (mask) {
         case 0: return launch_decode_t<kC, 0, false, false, true>(tp, grid, st);
@@ -154,15 +161,18 @@ bool make_q_map_ext(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N
 // K and V maps for a launch: paged pools, or contiguous KV (token extent L.total_kv, one page)
 bool make_kv_maps(TcParams& tp, const AttnParams& p, const TcLaunch& L, int B) {
   if (L.ragged)
-    return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.total_kv, p.ks1, p.ks1, p.ks2, B, 1, L.f8kv) &&
-           make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.total_kv, p.vs1, p.vs1, p.vs2, B, 1, L.f8kv);
-  return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.page_size, p.ks0, p.ks1, p.ks2, B, 0x7fffffff, L.f8kv) &&
-         make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.page_size, p.vs0, p.vs1, p.vs2, B, 0x7fffffff, L.f8kv);
+    return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.total_kv, p.ks1, p.ks1, p.ks2, B, 1, L.f8kv, p.D) &&
+           make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.total_kv, p.vs1, p.vs1, p.vs2, B, 1, L.f8kv, p.D);
+  return make_pool_map(&tp.tk, p.k, L.f16, p.H_kv, L.page_size, p.ks0, p.ks1, p.ks2, B, 0x7fffffff, L.f8kv, p.D) &&
+         make_pool_map(&tp.tv, p.v, L.f16, p.H_kv, L.page_size, p.vs0, p.vs1, p.vs2, B, 0x7fffffff, L.f8kv, p.D);
 }
 
 int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const char** name, const char** why) {
   *why = "";
-  if (p.D != 128) { *why = "head_dim != 128"; return 0; }
+  if (p.D != 128 && !(p.D == 64 && L.T_q == 16 && !L.f8kv && !L.rope)) {
+    *why = "head_dim 64 runs on tensor cores only for bf16/f16 decode tiles without RoPE";
+    return 0;
+  }
   const int g = p.g;
   if (!is_pow2(g)) { *why = "group size not a power of two"; return 0; }
   const int ps = L.page_size;
@@ -171,7 +181,7 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
   // pages a TMA box cannot tile (B_c < 8, or B_c neither dividing nor a multiple of 128): decode
   // tiles gather rows with 16-byte cp.async instead (any page size, any chunk alignment)
   const bool box_ok = L.ragged || (ps >= 8 && (128 % ps == 0 || ps % 128 == 0) && L.align % B == 0);
-  const bool cp_gather = L.T_q == 16 && !L.f8kv && !L.rope && (!box_ok || L.force_cp);
+  const bool cp_gather = L.T_q == 16 && !L.f8kv && !L.rope && p.D == 128 && (!box_ok || L.force_cp);
   // row gather flavour: TMA gather4 when K and V share strides that are whole D-element rows (the
   // NHD / HND pools), else 16-byte cp.async
   const bool rows_ok = !L.ragged && p.ks0 == p.vs0 && p.ks1 == p.vs1 && p.ks2 == p.vs2 && p.ks0 % 128 == 0 &&
@@ -190,7 +200,7 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     tp.f16 = L.f16;
     tp.pdl = L.pdl;
     tp.cp = cp_gather ? (rows_ok && !L.force_cp_async ? 2 : 1) : 0;
-    bool maps_ok = make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb);
+    bool maps_ok = make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb, p.D);
     if (tp.cp == 0) maps_ok = maps_ok && make_kv_maps(tp, p, L, B);
     if (tp.cp == 2) {
       tp.row_s0 = p.ks0 / 128;

@@ -55,10 +55,9 @@ def main():
     variants.append(("base_pdl", dict(prefix_tiles=(64, 128), balance=False, prefix_ctas=148, suffix_ctas=148,
                                       pdl=True)))
     variants.append(("pair_pdl", dict(prefix_ctas=148, suffix_ctas=148, pdl=True)))
-    for c in (48, 64, 80):
+    for c in (56, 64, 72):
         variants.append((f"conc_{c}", dict(prefix_ctas=c, suffix_ctas=148 - c, concurrent=True)))
-        variants.append((f"conc_{c}_t128", dict(prefix_ctas=c, suffix_ctas=148 - c, concurrent=True,
-                                                prefix_tiles=(64, 128))))
+        variants.append((f"conc_{c}_pdl", dict(prefix_ctas=c, suffix_ctas=148 - c, concurrent=True, pdl=True)))
     for name, kw in variants:
         comp = bsra.ComposableDecode(H_qo=32, H_kv=8, D=128, page_size=16, n_branch=n, **kw)
         comp.plan(c0.prefix, c0.suffix, c0.sm_scale)

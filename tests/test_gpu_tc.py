@@ -275,3 +275,28 @@ def test_c2_page_size_1_full_size_sampled(cuda_device):
     reqs = sorted({int(order[0]), int(order[64]), int(order[-1])})
     assert_close(gpu, oracle.attention_from_inputs(inp, req_list=reqs), "bf16", rows=rows_of_requests(inp, reqs),
                  what="c2 ps=1")
+
+
+# ---- head_dim 64 on the tcgen05 decode kernel (SURVEY §5 AOT set D in {64, 128})
+@pytest.mark.parametrize("H,ps,mask,qo", [((32, 8), 16, "none", None), ((16, 2), 8, "causal", [1, 4, 2, 3]),
+                                          ((64, 8), 64, "none", None), ((8, 8), 16, "custom", [2, 1, 1, 4])])
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+def test_tc_decode_head_dim_64(cuda_device, H, ps, mask, qo, dtype):
+    kv = np.array([1, 130, 700, 2049], np.int32)
+    qo = np.array(qo if qo is not None else [1] * 4, np.int32)
+    wl = synth.Workload("d64", H[0], H[1], 64, ps, dtype, mask, qo, kv)
+    inp = synth.make_inputs(wl, device=cuda_device)
+    for nc in (7, 148):
+        gpu = run_gpu(inp, num_ctas=nc, tile_q=16, kernel="tc")
+        assert gpu[2].selected_kernel() == "tc_decode"
+        assert_close(gpu, oracle.attention_from_inputs(inp), dtype, what=f"d64 {H} ps={ps} {mask} nc={nc}")
+
+
+def test_tc_decode_head_dim_64_matches_simt(cuda_device):
+    """Cross-kernel: the same D = 64 decode through the CUDA-core kernel agrees within tolerance."""
+    wl = synth.Workload("d64x", 32, 8, 64, 16, "bf16", "none", np.ones(3, np.int32), np.array([33, 700, 5000], np.int32))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    a = run_gpu(inp, num_ctas=148, tile_q=16, kernel="tc")
+    b = run_gpu(inp, num_ctas=148, tile_q=16, kernel="simt")
+    assert a[2].selected_kernel() == "tc_decode" and b[2].selected_kernel() == "simt"
+    assert np.max(np.abs(a[0] - b[0])) < 1e-2 and np.max(np.abs(a[1] - b[1])) < 1e-3
