@@ -475,9 +475,9 @@ def bench_composable(dev, pk, world=1, rank=0, layers=16, reps=20):
     c0 = cis[0]
     n = c0.q.shape[0]
     # prefix (paired 256-row tiles, tensor-bound) and suffix (HBM-bound) grids run concurrently on
-    # 64 + 84 SMs (scripts/composable_perf.py split sweep), PDL between consecutive launches
+    # 64 + 84 SMs (scripts/composable_perf.py split sweep; PDL measured slower in this mode)
     comp = bsra.ComposableDecode(H_qo=c0.H_qo, H_kv=c0.H_kv, D=c0.D, page_size=c0.page_size, n_branch=n,
-                                 prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=True)
+                                 prefix_ctas=64, suffix_ctas=84, concurrent=True)
     comp.plan(c0.prefix, c0.suffix, c0.sm_scale)
     pi = torch.from_numpy(c0.prefix["kv_page_indices"]).to(dev)
     si = torch.from_numpy(c0.suffix["kv_page_indices"]).to(dev)

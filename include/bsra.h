@@ -215,6 +215,28 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
                      const uint8_t* custom_mask, const int64_t* mask_bit_indptr, void* o, float* lse,
                      void* stream);
 
+/* Device-side inspector (the paper's future work, "move the scheduler to device"): one
+ * kernel builds, from DEVICE BSR arrays, the same plan image bsra_plan builds on the host (bit for
+ * bit: same Algorithm 1, same tie-breaks), enqueued on `stream` — so a step's plan can be captured
+ * in a CUDA graph with its run() calls and needs no host round trip.
+ *   batch                  requests (host int, <= max_batch)
+ *   d_qo_indptr, d_kv_page_indptr [batch+1], d_kv_last_page_len [batch]: DEVICE int32, read when
+ *                          the kernel runs (stream order)
+ * Requirements (the host must know the launch choices without the plan): paged engine, a fixed
+ * tile (cfg.tile_q), cfg.max_qo_len for decode tiles, no BSRA_FLAG_BALANCE_CTAS, no fp8 prefill
+ * tiles, num_ctas <= 512, at most 16,384 rows and 16,384 work items; the q buffer of later runs
+ * must hold max_total_qo_rows rows. Errors found on the device (malformed arrays, bounds, too
+ * large) leave an empty plan — run() then writes nothing — and a code that
+ * bsra_plan_device_status returns (1 malformed, 2 bounds, 3 too large).
+ * Host errors: EINVAL, EUNSUPPORTED (requirements), EBOUNDS (batch > max_batch). */
+bsra_status bsra_plan_device(bsra_engine* e, int32_t batch, const int32_t* d_qo_indptr,
+                             const int32_t* d_kv_page_indptr, const int32_t* d_kv_last_page_len, float sm_scale,
+                             void* stream);
+
+/* Synchronises `stream` and returns the device planner's status code (0 = OK) for the current plan
+ * (0 for host-built plans). */
+bsra_status bsra_plan_device_status(bsra_engine* e, void* stream, int32_t* code);
+
 /* Declares that every CUDA graph captured over run() calls of `e` has been destroyed (or will
  * be re-captured): clears the launch choices recorded at capture, so the next plan may change
  * them. Host only. Errors: EINVAL (NULL engine). */

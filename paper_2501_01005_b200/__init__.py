@@ -52,7 +52,7 @@ FLAG_CP_ASYNC = 16  # BSRA_FLAG_CP_ASYNC: ... with 16-byte cp.async
 
 _lib = None
 EXPORTS = ["bsra_version", "bsra_num_sms", "bsra_workspace_bytes", "bsra_engine_create", "bsra_engine_destroy",
-           "bsra_plan", "bsra_run", "bsra_graph_release", "bsra_set_kv_scales", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
+           "bsra_plan", "bsra_run", "bsra_graph_release", "bsra_plan_device", "bsra_plan_device_status", "bsra_set_kv_scales", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
            "bsra_plan_host", "bsra_plan_export",
            "bsra_plan_stats", "bsra_last_run_launches", "bsra_selected_kernel", "bsra_last_error",
            "bsra_dist_unique_id", "bsra_dist_create", "bsra_dist_destroy", "bsra_dist_scratch_bytes",
@@ -79,6 +79,8 @@ def lib():
             "bsra_run": (I32, [P, P, P, P, P, P, P, P, P, P, P, P]),
             "bsra_set_kv_scales": (I32, [P, ctypes.c_float, ctypes.c_float]),
             "bsra_graph_release": (I32, [P]),
+            "bsra_plan_device": (I32, [P, I32, P, P, P, ctypes.c_float, P]),
+            "bsra_plan_device_status": (I32, [P, P, ctypes.POINTER(I32)]),
             "bsra_plan_ragged": (I32, [P, I32, P, P, ctypes.c_float, P]),
             "bsra_run_ragged": (I32, [P, P, P, P, P, P, P, P, P, P, P]),
             "bsra_merge_states": (I32, [P, P, P, P, I32, I64, I32, I32, P, I32, P, P]),
@@ -213,6 +215,16 @@ class Engine:
                               ctypes.cast(vs, ctypes.c_void_p), _p(kv_page_indices), _p(custom_mask),
                               _p(mask_bit_indptr), _p(o), _p(lse), self._stream(stream)))
 
+    def plan_device(self, batch, qo_indptr, kv_page_indptr, kv_last_page_len, sm_scale: float = 0.0, stream=None):
+        """Device-side Algorithm 1 (bsra_plan_device): the arrays are device int32 tensors."""
+        _check(lib().bsra_plan_device(self._h, int(batch), _p(qo_indptr), _p(kv_page_indptr), _p(kv_last_page_len),
+                                      float(sm_scale), self._stream(stream)))
+
+    def plan_device_status(self, stream=None) -> int:
+        code = ctypes.c_int32()
+        _check(lib().bsra_plan_device_status(self._h, self._stream(stream), ctypes.byref(code)))
+        return code.value
+
     def graph_release(self):
         """Every CUDA graph captured over this engine's run() calls is gone (bsra_graph_release)."""
         _check(lib().bsra_graph_release(self._h))
@@ -239,7 +251,8 @@ class Engine:
     def export_plan(self, from_device=False, stream=None) -> np.ndarray:
         L = lib()
         n = ctypes.c_size_t()
-        _check(L.bsra_plan_export(self._h, 0, None, 0, ctypes.byref(n), None))
+        st = self._stream(stream) if from_device else None
+        _check(L.bsra_plan_export(self._h, int(from_device), None, 0, ctypes.byref(n), st))
         out = np.zeros(n.value, np.int32)
         _check(L.bsra_plan_export(self._h, int(from_device), _p(out), n.value, ctypes.byref(n),
                                   self._stream(stream) if from_device else None))

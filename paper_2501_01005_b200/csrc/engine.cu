@@ -18,6 +18,7 @@
 #include "attn_simt.cuh"
 #include "f8_gather.cuh"
 #include "merge.cuh"
+#include "plan_device.cuh"
 #include "scheduler.hpp"
 #include "tc_kernels.hpp"
 
@@ -174,6 +175,7 @@ struct bsra_engine {
   // in the workspace's f8 region ([2][lay.f8_rows, H_kv, 128])
   bool f8_prefill = false;
   int64_t f8_rows = 0;       // sum of l_kv of the current plan
+  bool device_planned = false;  // the current plan was built on the device (bsra_plan_device)
   bool captured = false;     // a run() was captured into a CUDA graph since the last release
   LaunchSig cap_sig;         // launch choices of that captured run()
   long long* trace = nullptr;  // BSRA_EXPERIMENTS builds: device buffer for kernel pipeline traces
@@ -433,6 +435,7 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
   e->image.swap(im);
   e->summary = sum;
   e->planned = true;
+  e->device_planned = false;
   e->f8_prefill = f8_prefill;
   e->f8_rows = f8_rows;
   e->sm_scale = sm_scale > 0.f ? sm_scale : 1.f / std::sqrt((float)c.head_dim);
@@ -454,6 +457,90 @@ bsra_status bsra_plan(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, c
   std::string err = bsra::lengths_from_bsr(batch, qo_indptr, kv_page_indptr, kv_last_page_len, c.page_size, qo, kv);
   if (!err.empty()) return fail(BSRA_EINVAL, err);
   return plan_core(e, qo_indptr, kv_page_indptr, qo, kv, sm_scale, stream);
+}
+
+bsra_status bsra_plan_device(bsra_engine* e, int32_t batch, const int32_t* d_qo_indptr, const int32_t* d_kv_page_indptr,
+                             const int32_t* d_kv_last_page_len, float sm_scale, void* stream) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  const bsra_config& c = e->cfg;
+  if (c.flags & BSRA_FLAG_RAGGED_KV) return fail(BSRA_EUNSUPPORTED, "device planning: paged engines only");
+  if (c.flags & BSRA_FLAG_BALANCE_CTAS) return fail(BSRA_EUNSUPPORTED, "device planning: no BSRA_FLAG_BALANCE_CTAS");
+  if (!c.tile_q) return fail(BSRA_EUNSUPPORTED, "device planning needs a fixed tile (cfg.tile_q)");
+  if (c.tile_q == 16 && c.max_qo_len <= 0)
+    return fail(BSRA_EUNSUPPORTED, "device planning of decode tiles needs cfg.max_qo_len");
+  if (kv_is_f8(c) && c.tile_q > 16) return fail(BSRA_EUNSUPPORTED, "device planning: no fp8 prefill tiles");
+  if (c.num_ctas > 512) return fail(BSRA_EUNSUPPORTED, "device planning: num_ctas > 512");
+  const int64_t alpha = c.cost_alpha ? c.cost_alpha : 1, beta = c.cost_beta ? c.cost_beta : 1;
+  if (alpha > (1 << 20) || beta > (1 << 20)) return fail(BSRA_EUNSUPPORTED, "device planning: alpha / beta > 2^20");
+  if (batch < 0) return fail(BSRA_EINVAL, "batch < 0");
+  if (batch > c.max_batch) return fail(BSRA_EBOUNDS, "batch exceeds max_batch");
+  if (batch > 0 && (!d_qo_indptr || !d_kv_page_indptr || !d_kv_last_page_len)) return fail(BSRA_EINVAL, "NULL array");
+  if (e->captured && e->cap_sig.T_q != c.tile_q)
+    return fail(BSRA_EBOUNDS, "re-plan changes a launch choice baked into a captured CUDA graph (query tile)");
+  bsra::DevPlanParams P{};
+  P.qo_indptr = d_qo_indptr;
+  P.kv_page_indptr = d_kv_page_indptr;
+  P.kv_last_page_len = d_kv_last_page_len;
+  P.image = reinterpret_cast<int32_t*>(e->ws + e->lay.off_plan);
+  P.scratch = reinterpret_cast<int32_t*>(e->ws + e->lay.off_part_o);
+  P.scratch_words = (int64_t)((e->lay.off_counters - e->lay.off_part_o) / 4);
+  P.cap_words = (int32_t)e->lay.plan_words;
+  P.batch = batch;
+  P.H_kv = c.num_kv_heads;
+  P.g = c.num_qo_heads / c.num_kv_heads;
+  P.page_size = c.page_size;
+  P.mask = c.mask;
+  P.num_ctas = c.num_ctas;
+  P.T_q = c.tile_q;
+  P.align = c.kv_chunk_align ? c.kv_chunk_align : c.page_size;
+  P.L_min = c.kv_chunk_min;
+  P.window = c.sliding_window;
+  P.max_total_qo_rows = c.max_total_qo_rows;
+  P.alpha = alpha;
+  P.beta = beta;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(bsra::plan_device_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  bsra::devplan::kSmemBytes));
+    attr = true;
+  }
+  bsra::plan_device_kernel<<<1, bsra::devplan::kThreads, bsra::devplan::kSmemBytes, st>>>(P);
+  CUDA_TRY(cudaGetLastError());
+  if (!e->counters_zeroed) {
+    CUDA_TRY(cudaMemsetAsync(e->ws + e->lay.off_counters, 0, (size_t)(e->lay.num_ctas + 1) * 4, st));
+    e->counters_zeroed = true;
+  }
+  // host-side launch choices from the engine bounds (the plan itself stays on the device)
+  const int32_t g = c.num_qo_heads / c.num_kv_heads;
+  const int64_t fused = std::min<int64_t>(16, (int64_t)std::max(1, c.max_qo_len) * g);
+  e->image.clear();
+  e->summary = bsra::PlanSummary();
+  e->summary.T_q = c.tile_q;
+  e->summary.n_items = 1;  // unknown on the host: run() validates its pointers
+  e->planned = true;
+  e->device_planned = true;
+  e->f8_prefill = false;
+  e->f8_rows = 0;
+  e->sm_scale = sm_scale > 0.f ? sm_scale : 1.f / std::sqrt((float)c.head_dim);
+  e->total_qo = c.max_total_qo_rows;
+  e->max_qo = c.max_qo_len;
+  e->kc = fused <= 4 ? 4 : fused <= 8 ? 8 : 16;
+  return BSRA_OK;
+}
+
+bsra_status bsra_plan_device_status(bsra_engine* e, void* stream, int32_t* code) {
+  if (!e || !code) return fail(BSRA_EINVAL, "NULL argument");
+  if (!e->device_planned) {
+    *code = 0;
+    return BSRA_OK;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t hdr[16];
+  CUDA_TRY(cudaMemcpyAsync(hdr, e->ws + e->lay.off_plan, sizeof(hdr), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *code = hdr[12];
+  return BSRA_OK;
 }
 
 bsra_status bsra_plan_ragged(bsra_engine* e, int32_t batch, const int32_t* qo_indptr, const int32_t* kv_indptr,
@@ -832,6 +919,21 @@ bsra_status bsra_merge_many(const float* o_parts, const float* lse_parts, int32_
 bsra_status bsra_plan_export(const bsra_engine* e, int32_t from_device, int32_t* host_buf, size_t cap_words,
                              size_t* n_words, void* stream) {
   if (!e || !n_words) return fail(BSRA_EINVAL, "NULL argument");
+  if (e->device_planned) {  // the image exists only on the device: its size from its header
+    if (!from_device) return fail(BSRA_EINVAL, "device-built plan: export with from_device = 1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int32_t h[16];
+    CUDA_TRY(cudaMemcpyAsync(h, e->ws + e->lay.off_plan, sizeof(h), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const size_t words = 16 + (size_t)(h[2] + 1) + 6 * (size_t)h[5] + (size_t)(h[6] + 1) + (size_t)h[7] +
+                         3 * (size_t)h[6] + 4 * (size_t)h[8];
+    *n_words = words;
+    if (!host_buf) return BSRA_OK;
+    if (cap_words < words) return fail(BSRA_ENOMEM, "buffer too small");
+    CUDA_TRY(cudaMemcpyAsync(host_buf, e->ws + e->lay.off_plan, words * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return BSRA_OK;
+  }
   *n_words = e->image.size();
   if (!host_buf) return BSRA_OK;
   if (cap_words < e->image.size()) return fail(BSRA_ENOMEM, "buffer too small");

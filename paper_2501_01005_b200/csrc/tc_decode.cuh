@@ -86,8 +86,10 @@ constexpr int kOffQ = kStages * kStageBytes;
 constexpr int kOffP = kOffQ + 2 * kQBytes;   // two P^T buffers
 constexpr int kOffBar = kOffP + 2 * kPBytes;
 constexpr int kOffRed = kOffBar + 512;
-// red [4][kN], vote flags [2][4], epilogue hand-off sums [2][4][kN] and max [2][kN]; + alignment slack
-constexpr int kSmemBytes = kOffRed + 1024 + 1024;
+// red [4][kN], vote flags [2][4], epilogue hand-off sums [2][4][kN] and max [2][kN]
+constexpr int kOffItems = kOffRed + 1024;
+constexpr int kStagedItems = 64;  // the CTA's first queue entries, decoded once into shared memory
+constexpr int kSmemBytes = kOffItems + kStagedItems * 80 + 1024;  // + alignment slack
 constexpr int kThreads = 320;  // producer, 4 softmax warps, MMA warp, 4 epilogue warps
 constexpr int kThreadsRope = 576;  // + 8 RoPE warps (two per SM sub-partition) in the fused-RoPE variant
 constexpr int threads_for(bool rope) { return rope ? kThreadsRope : kThreads; }
@@ -100,6 +102,8 @@ struct DecItem {
   int64_t kb, ke, lk, qo_begin, page_begin;
   int ntiles;
 };
+
+static_assert(sizeof(DecItem) <= 80, "staged item slot");
 
 __device__ __forceinline__ DecItem dec_item(const PlanView& pv, int it, int g) {
   DecItem d;
@@ -180,6 +184,12 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
   const PlanView pv = load_plan(p.plan);
   const int g = p.g;
   const int it0 = pv.cta_indptr[blockIdx.x], it1 = pv.cta_indptr[blockIdx.x + 1];
+  // Every role walks the same queue: its first kStagedItems entries are decoded once here (the
+  // plan reads of an item are ~3 dependent global loads, otherwise paid by each role at each item
+  // boundary on the critical path)
+  DecItem* staged = reinterpret_cast<DecItem*>(smem + kOffItems);
+  for (int k = threadIdx.x; k < min(kStagedItems, it1 - it0); k += blockDim.x) staged[k] = dec_item(pv, it0 + k, g);
+  auto item_at = [&](int it) { return it - it0 < kStagedItems ? staged[it - it0] : dec_item(pv, it, g); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -233,7 +243,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     uint32_t qphase[2] = {1, 1};
     int qb = 0;
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       // ---- Q tile: 16 fused rows = q_tb tokens x q_hb heads, two 64-column halves
       if (lane == 0) {
         ptx::mbar_wait(&empty_q[qb], qphase[qb]);
@@ -386,7 +396,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       pb ^= 1;
     };
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       ptx::mbar_wait(kRope ? &qrot[qb] : &full_q[qb], qphase[qb]);
       qphase[qb] ^= 1;
       if (d.ntiles == 0) {
@@ -447,7 +457,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     };
 
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       if (d.ntiles == 0) continue;  // empty item: the epilogue warps write the empty state
       const uint32_t tO = tmem + lane_addr + 32 + ob * 16;
       float m[kC], lp[kC], aslope[kC];
@@ -618,7 +628,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     float s2, c2;
     rope_sincos_precise(4, f[ri], s2, c2);  // the per-step rotation by 4 theta_i (1 ulp)
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       ptx::mbar_wait(&full_q[qb], qph[qb]);
       qph[qb] ^= 1;
       {  // Q: 16 rows x 8 chunk pairs; fused row c is token (row0 + c) / g at l_kv - l_qo + token
@@ -691,7 +701,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     uint32_t efph[2] = {0, 0};
     pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       float ov[kC], l[kC], mm[kC];
       if (d.ntiles > 0) {
         ptx::mbar_wait(&epi_full[ob], efph[ob]);
