@@ -50,6 +50,7 @@ struct Layout {
   int32_t num_ctas = 0, T_max = 0, T_min = 0;
   size_t plan_words = 0;
   size_t off_plan = 0, off_part_o = 0, off_part_lse = 0, off_counters = 0, off_aux = 0, off_f8 = 0, total = 0;
+  size_t off_devscratch = 0, devscratch_words = 0;  // device planner scratch (bsra_plan_device)
   size_t aux_words = 0;  // fp8 prefill gather: src_begin[max_batch+1], kv_off[max_batch+1]
   int64_t f8_rows = 0;   // fp8 prefill gather region: max_total_kv_tokens rows of [H_kv, 128] K and V
 };
@@ -131,6 +132,10 @@ Layout make_layout(const bsra_config& c, int32_t num_ctas) {
   if (kv_is_f8(c) && L.T_max > 16 && c.head_dim == 128 && c.kernel != BSRA_KERNEL_SIMT)
     L.f8_rows = c.max_total_kv_tokens;
   off = align_up(off + (size_t)L.f8_rows * c.num_kv_heads * 128 * 2 * sizeof(uint16_t), 256);
+  // device planner: per request 3, per row 5, per item 2 words (rows <= items <= plan_words / 6)
+  L.off_devscratch = off;
+  L.devscratch_words = 2 * L.plan_words + 3 * ((size_t)c.max_batch + 1) + (size_t)num_ctas + 64;
+  off = align_up(off + L.devscratch_words * 4, 256);
   L.total = off;
   return L;
 }
@@ -482,8 +487,8 @@ bsra_status bsra_plan_device(bsra_engine* e, int32_t batch, const int32_t* d_qo_
   P.kv_page_indptr = d_kv_page_indptr;
   P.kv_last_page_len = d_kv_last_page_len;
   P.image = reinterpret_cast<int32_t*>(e->ws + e->lay.off_plan);
-  P.scratch = reinterpret_cast<int32_t*>(e->ws + e->lay.off_part_o);
-  P.scratch_words = (int64_t)((e->lay.off_counters - e->lay.off_part_o) / 4);
+  P.scratch = reinterpret_cast<int32_t*>(e->ws + e->lay.off_devscratch);
+  P.scratch_words = (int64_t)e->lay.devscratch_words;
   P.cap_words = (int32_t)e->lay.plan_words;
   P.batch = batch;
   P.H_kv = c.num_kv_heads;

@@ -24,7 +24,7 @@ struct DevPlanParams {
   const int32_t* kv_page_indptr;  // [batch+1] device
   const int32_t* kv_last_page_len;  // [batch] device
   int32_t* image;                 // workspace plan section
-  int32_t* scratch;               // workspace partial section (free before run() in stream order)
+  int32_t* scratch;               // workspace device-planner scratch section
   int64_t scratch_words;
   int32_t cap_words;              // plan section capacity
   int32_t batch, H_kv, g, page_size, mask, num_ctas, T_q, align, L_min, window, max_total_qo_rows;
@@ -34,7 +34,7 @@ struct DevPlanParams {
 namespace devplan {
 constexpr int kThreads = 1024;
 constexpr int kMaxSort = 16384;  // items sorted in shared memory (128 KB of keys)
-constexpr int kSmemBytes = kMaxSort * 8 + 4096;
+constexpr int kSmemBytes = kMaxSort * 8 + (kThreads + 1) * 8 + 64;  // sort keys + scan scratch
 enum : int32_t { kOk = 0, kEMalformed = 1, kEBounds = 2, kETooLarge = 3 };
 }  // namespace devplan
 
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(devplan::kThreads, 1) plan_device_kernel(const
   if (B > 0 && tid == 0 && (int64_t)P.qo_indptr[B] > P.max_total_qo_rows) s_err = devplan::kEBounds;
   const int64_t R64 = dp_block_scan(rowoff, B, sh);
   if (tid == 0) rowoff[B] = (int32_t)R64;
-  if (s_err || R64 > devplan::kMaxSort) {
+  if (s_err || R64 > devplan::kMaxSort || 2 * (int64_t)B + 1 + 5 * R64 > P.scratch_words) {
     dp_fail(P, s_err ? s_err : devplan::kETooLarge);
     return;
   }
