@@ -482,7 +482,9 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&s_free[sbuf]);  // the MMA warp may reuse this S^T buffer
-        if (n < kTile && row >= n) {  // rows past the chunk: zero V so 0 * garbage cannot poison O
+        // rows past the chunk: zero V so 0 * garbage cannot poison O (the cp.async gather already
+        // zero-filled them)
+        if (n < kTile && row >= n && !(kRow && tp.cp == 1)) {
           ptx::mbar_wait(&full[stage], fphase);  // (already complete) orders the TMA writes before ours
           uint8_t* vS = smem + stage * kStageBytes + kKVBytes;
           uint4 z = make_uint4(0, 0, 0, 0);
