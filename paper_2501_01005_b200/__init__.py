@@ -408,7 +408,7 @@ class ComposableDecode:
 
     def __init__(self, *, H_qo, H_kv, D, page_size, n_branch, dtype="bf16", device=0, prefix_ctas=0,
                  suffix_ctas=0, kernel="auto", prefix_tiles=(64, 128, 256), balance=True, concurrent=False,
-                 pdl=False):
+                 pdl=False, suffix_pdl=None):
         self.n, self.H_qo, self.D = n_branch, H_qo, D
         self.concurrent = concurrent
         self.prefix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
@@ -416,7 +416,8 @@ class ComposableDecode:
                                          tile_set=prefix_tiles, kernel=kernel, balance_ctas=balance, pdl=pdl), device)
         self.suffix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
                                          max_batch=n_branch, max_total_qo_rows=n_branch, num_ctas=suffix_ctas,
-                                         tile_q=16, kernel=kernel, max_qo_len=1, pdl=pdl), device)
+                                         tile_q=16, kernel=kernel, max_qo_len=1,
+                                         pdl=pdl if suffix_pdl is None else suffix_pdl), device)
         dev = f"cuda:{device}"
         self.o_p = torch.empty((n_branch, H_qo, D), device=dev)
         self.l_p = torch.empty((n_branch, H_qo), device=dev)

@@ -514,15 +514,20 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         // first tile) do the warps reduce the tile max, rescale O and recompute P. The common
         // path has no shuffles and one barrier: a warp vote and a per-warp flag (double-buffered
         // by tile parity) read after it.
-        bool over = false;
-#pragma unroll
-        for (int c = 0; c < kC; ++c) over |= s[c] > m[c] + kRescaleThresh;
-        over = __any_sync(0xffffffffu, over);
+        // An item's first tile always takes the reduction (the running max is -inf), so it skips
+        // the vote and the speculative exp / P store / barrier of the common path.
+        const bool first = ti == 0;
         int* flags = vflags + (tpar & 1) * 4;
-        if (lane == 0) flags[q4] = over ? 1 : 0;
         float pr[kC];
+        if (!first) {
+          bool over = false;
 #pragma unroll
-        for (int c = 0; c < kC; ++c) pr[c] = s[c] == -INFINITY ? 0.f : exp2f(s[c] - m[c]);
+          for (int c = 0; c < kC; ++c) over |= s[c] > m[c] + kRescaleThresh;
+          over = __any_sync(0xffffffffu, over);
+          if (lane == 0) flags[q4] = over ? 1 : 0;
+#pragma unroll
+          for (int c = 0; c < kC; ++c) pr[c] = s[c] == -INFINITY ? 0.f : exp2f(s[c] - m[c]);
+        }
         wait_pv(pbuf);  // the PV MMA that read this P^T buffer two tiles ago is done
         // ---- P^T (K-major, SW128): row c, token `row`
         uint8_t* pa = smem + kOffP + pbuf * kPBytes + (row >> 6) * (kN * 128);
@@ -535,10 +540,12 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
             else *reinterpret_cast<__nv_bfloat16*>(pa + off) = __float2bfloat16_rn(pr[c]);
           }
         };
-        store_p();
-        ptx::fence_proxy_async();  // P (and zeroed V rows) visible to the tensor core
-        ptx::named_bar_sync(1, 128);
-        if (flags[0] | flags[1] | flags[2] | flags[3]) {  // slow path
+        if (!first) {
+          store_p();
+          ptx::fence_proxy_async();  // P (and zeroed V rows) visible to the tensor core
+          ptx::named_bar_sync(1, 128);
+        }
+        if (first || (flags[0] | flags[1] | flags[2] | flags[3])) {  // slow path
           float mx[kC];
 #pragma unroll
           for (int c = 0; c < kC; ++c) mx[c] = s[c];

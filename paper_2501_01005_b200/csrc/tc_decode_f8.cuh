@@ -56,8 +56,9 @@ constexpr int kOffQ = kOffV + kVSt * kVBytes;
 constexpr int kOffP = kOffQ + 2 * kQBytes;
 constexpr int kOffBar = kOffP + 2 * kPBytes;
 constexpr int kOffRed = kOffBar + 512;  // 38 mbarriers + tmem slot + flag
-// red [4][kN], vote flags [2][4], epilogue hand-off sums [2][4][kN] and max [2][kN]; + align slack
-constexpr int kSmemBytes = kOffRed + 1024 + 1024;
+// red [4][kN], vote flags [2][4], epilogue hand-off sums [2][4][kN] and max [2][kN]
+constexpr int kOffItems = kOffRed + 1024;  // the queue's first dec::kStagedItems plan entries (as tc_decode)
+constexpr int kSmemBytes = kOffItems + dec::kStagedItems * 80 + 1024;  // + align slack
 // Warp roles: producer, 4 K converters, kVW V converters, 4 softmax, MMA issuer, 4 epilogue.
 // kVW = 4 for kC = 4 / 8 (576 threads, 96 registers); 2 for kC = 16 (512 threads,
 // 128 registers: fewer spills of the 16-column softmax state; each V converter thread takes 2
@@ -149,6 +150,10 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
   const PlanView pv = load_plan(p.plan);
   const int g = p.g;
   const int it0 = pv.cta_indptr[blockIdx.x], it1 = pv.cta_indptr[blockIdx.x + 1];
+  DecItem* staged = reinterpret_cast<DecItem*>(smem + kOffItems);  // decoded once (see tc_decode)
+  for (int k = threadIdx.x; k < min(dec::kStagedItems, it1 - it0); k += blockDim.x)
+    staged[k] = dec_item(pv, it0 + k, g);
+  auto item_at = [&](int it) { return it - it0 < dec::kStagedItems ? staged[it - it0] : dec_item(pv, it, g); };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kF8St; ++s) {
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
     uint32_t qphase[2] = {1, 1};
     int qb = 0;
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       if (lane == 0) {
         ptx::mbar_wait(&empty_q[qb], qphase[qb]);
         ptx::mbar_arrive_expect_tx(&full_q[qb], kQBytes);
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
     int fs = 0, kb = 0;
     uint32_t f8ph = 0, keph = 1;
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       for (int ti = 0; ti < d.ntiles; ++ti) {
         ptx::mbar_wait(&f8full[fs], f8ph);
         if (row == 0) F8T(1, tpos);
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
     int fs = 0, vs = 0;
     uint32_t f8ph = 0, veph = 1;
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       for (int ti = 0; ti < d.ntiles; ++ti) {
         const int n = (int)imin64(kTile, d.ke - (d.kb + (int64_t)ti * kTile));
         ptx::mbar_wait(&f8full[fs], f8ph);
@@ -407,7 +412,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
       pb ^= 1;
     };
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       if (d.ntiles == 0) {
         qb ^= 1;  // the softmax warps still take (and release) this item's Q buffer
         continue;
@@ -465,7 +470,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
     };
 
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       if (ct == 0) F8T(6, it - it0);
       ptx::mbar_wait(&full_q[qb], qphase[qb]);
       qphase[qb] ^= 1;
@@ -646,7 +651,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
     uint32_t efph[2] = {0, 0};
     pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
     for (int it = it0; it < it1; ++it) {
-      const DecItem d = dec_item(pv, it, g);
+      const DecItem d = item_at(it);
       float ov[kC], l[kC], mm[kC];
       if (d.ntiles > 0) {
         ptx::mbar_wait(&epi_full[ob], efph[ob]);

@@ -558,21 +558,6 @@ __global__ void __launch_bounds__(pre2::kThreads, 1) tc_prefill2_kernel(const __
     const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
     const uint32_t tS = tmem + lane_addr + w * 128;
     const uint32_t tO = tmem + lane_addr + 256 + w * 128;
-    // Warm L1 with this CTA's plan entries (each WG reads an item's entry at the item's start, on
-    // the critical path: ~3 dependent loads). TMA traffic bypasses L1, so the lines stay.
-    for (int k = r; k < it1 - it0; k += 128) {
-      const int it = it0 + k;
-      ptx::prefetch_l1(pv.item_kvh + it);
-      ptx::prefetch_l1(pv.item_qtile + it);
-      ptx::prefetch_l1(pv.item_kb + it);
-      ptx::prefetch_l1(pv.item_ke + it);
-      ptx::prefetch_l1(pv.item_slot + it);
-      const int req = pv.item_req[it];
-      ptx::prefetch_l1(pv.req_qo_len + req);
-      ptx::prefetch_l1(pv.req_kv_len + req);
-      ptx::prefetch_l1(pv.req_qo_begin + req);
-      ptx::prefetch_l1(pv.req_page_begin + req);
-    }
     const float sc = p.scale_log2;
     uint32_t sph = 0, oph = 0;
     int tcount = 0;

@@ -57,7 +57,8 @@ def main():
     variants.append(("pair_pdl", dict(prefix_ctas=148, suffix_ctas=148, pdl=True)))
     for c in (56, 64, 72):
         variants.append((f"conc_{c}", dict(prefix_ctas=c, suffix_ctas=148 - c, concurrent=True)))
-        variants.append((f"conc_{c}_pdl", dict(prefix_ctas=c, suffix_ctas=148 - c, concurrent=True, pdl=True)))
+        variants.append((f"conc_{c}_spdl", dict(prefix_ctas=c, suffix_ctas=148 - c, concurrent=True,
+                                                suffix_pdl=True)))
     for name, kw in variants:
         comp = bsra.ComposableDecode(H_qo=32, H_kv=8, D=128, page_size=16, n_branch=n, **kw)
         comp.plan(c0.prefix, c0.suffix, c0.sm_scale)
