@@ -297,19 +297,24 @@ def e2e_steps(L: Layered, eng, steps, warmup):
 
 def oracle_cpu_baseline(wl, inp_host, budget_s=12.0):
     """The float64 C oracle, as it stands, on this host's cores: whole configs[1] layers
-    repeated until ~budget_s of CPU work. Returns (TB/s of KV, threads, sample text)."""
+    repeated until ~budget_s of CPU work. Returns (TB/s of KV, threads, sample text, the first
+    run's (o, lse) for the §8(d.6) parity fields)."""
     import oracle
     threads = len(os.sched_getaffinity(0))
     by = decode_bytes(wl)["total"]
     t0 = time.perf_counter()
     n = 0
+    first = None
     while True:
-        oracle.paged_attention(**inp_host, num_threads=threads)
+        r = oracle.paged_attention(**inp_host, num_threads=threads)
+        if first is None:
+            first = r
         n += 1
         el = time.perf_counter() - t0
         if el >= budget_s or n >= 200:
             break
-    return by * n / el / 1e12, threads, f"{n} full configs[1] layer(s) (batch 128, one layer each) in {el:.1f} s"
+    return (by * n / el / 1e12, threads, f"{n} full configs[1] layer(s) (batch 128, one layer each) in {el:.1f} s",
+            first)
 
 
 def host_inputs(inp):
@@ -781,7 +786,7 @@ def maybe_relaunch(args):
     (one per GPU) and pass rank 0's JSON line through. Fails loudly if fewer GPUs are visible."""
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
         return
-    if args.impl != "reference":
+    if args.impl != "reference" and os.environ.get("BSRA_BENCH_ONE_GPU") != "1":
         have = torch.cuda.device_count()
         if have < args.gpus:
             print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
@@ -800,9 +805,13 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        backend = "gloo" if args.impl == "reference" else "nccl"
-        if backend == "nccl":
-            torch.cuda.set_device(local)
+        # BSRA_BENCH_ONE_GPU=1 (tests only): every rank on cuda:0 with a gloo group, to exercise the
+        # multi-rank code paths on a one-GPU box (the NCCL-based long-context line needs --no-long)
+        one_gpu = os.environ.get("BSRA_BENCH_ONE_GPU") == "1"
+        backend = "gloo" if args.impl == "reference" or one_gpu else "nccl"
+        if torch.cuda.is_available() and args.impl != "reference":
+            torch.cuda.set_device(0 if one_gpu else local)
+            local = 0 if one_gpu else local
         dist.init_process_group(backend=backend)
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
@@ -967,7 +976,17 @@ def main():
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                "how": "per step: plan() on host, then one graph replay of {H2D q[r] (copy stream) -> run(r) -> "
                       "D2H o[r], lse[r] (copy stream)} for every layer r, copies overlapping other layers' kernels"}
-    del L, eng
+    # determinism and the §8(d.6) parity inputs: layer 0 run twice (bitwise equal), its output and plan
+    inp0, o0, l0 = L.layers[0]
+    outs = []
+    for _ in range(2):
+        o0.fill_(float("nan"))
+        L.run_layer(eng, 0)
+        torch.cuda.synchronize()
+        outs.append((o0.clone(), l0.clone()))
+    head_check = {"deterministic": bool(torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])),
+                  "o": outs[1][0].float().cpu().numpy(), "lse": outs[1][1].cpu().numpy(), "plan": eng.export_plan()}
+    del L, eng, outs
     torch.cuda.empty_cache()
 
     # ---- secondary: configs[1] with the batch fixed and KV heads split over the ranks (N > 1)
@@ -1020,11 +1039,25 @@ def main():
         torch.cuda.empty_cache()
 
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         inp_cpu = synth.make_inputs(wl, device="cpu")
-        v, th, sample = oracle_cpu_baseline(wl, host_inputs(inp_cpu))
+        v, th, sample, ref = oracle_cpu_baseline(wl, host_inputs(inp_cpu))
         cpu = {"value": v, "unit": "TB/s", "cores": th, "kind": "oracle", "sample": sample, "cpu_model": cpu_model(),
                "single_thread": oracle_single_thread()}
+        # §8(d.6) parity fields from the same oracle run: the headline layer 0 (same seeds) vs the
+        # float64 oracle on every row, and the headline plan vs the Python Algorithm 1 (bit-exact)
+        from oracle import scheduler_ref
+        fin = np.isfinite(ref[1])
+        ref_plan = scheduler_ref.plan_ref(wl.qo_lens, wl.kv_lens, g=wl.g, H_kv=wl.H_kv, num_ctas=args.num_ctas,
+                                          align=wl.page_size, T_q=16, qo_begin=inp_cpu.qo_indptr[:-1],
+                                          page_begin=inp_cpu.kv_page_indptr[:-1])
+        parity = {"workload": "configs[1] layer 0, all 128 x 32 rows, vs the float64 oracle",
+                  "max_abs_do": float(np.max(np.abs(head_check["o"] - ref[0]))),
+                  "max_abs_dlse": float(np.max(np.abs(head_check["lse"][fin] - ref[1][fin]))),
+                  "tolerance": {"o": 1e-2, "lse": 1e-3},
+                  "plan_bit_exact_vs_python_algorithm1": bool(np.array_equal(head_check["plan"], ref_plan.image)),
+                  "deterministic_run_to_run": head_check["deterministic"]}
 
     if rank == 0:
         out = {
@@ -1037,7 +1070,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "prefill": prefill,
             "decode_head_sharded": head_sharded, "composable": composable, "long_context": long_ctx,
             "contiguous_kv": contiguous, "decode_fp8": fp8, "scheduler": sched, "quest": quest,
-            "decode_rope": rope,
+            "decode_rope": rope, "parity": parity,
             "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
         }
         emit(out)
