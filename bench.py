@@ -986,6 +986,8 @@ def main():
         outs.append((o0.clone(), l0.clone()))
     head_check = {"deterministic": bool(torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])),
                   "o": outs[1][0].float().cpu().numpy(), "lse": outs[1][1].cpu().numpy(), "plan": eng.export_plan()}
+    # layer 0's own inputs on the host for the oracle leg (the CPU and CUDA generators differ)
+    head_inputs = host_inputs(inp0) if rank == 0 and world == 1 and not args.no_cpu_baseline else None
     del L, eng, outs
     torch.cuda.empty_cache()
 
@@ -1041,8 +1043,7 @@ def main():
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        inp_cpu = synth.make_inputs(wl, device="cpu")
-        v, th, sample, ref = oracle_cpu_baseline(wl, host_inputs(inp_cpu))
+        v, th, sample, ref = oracle_cpu_baseline(wl, head_inputs)
         cpu = {"value": v, "unit": "TB/s", "cores": th, "kind": "oracle", "sample": sample, "cpu_model": cpu_model(),
                "single_thread": oracle_single_thread()}
         # §8(d.6) parity fields from the same oracle run: the headline layer 0 (same seeds) vs the
@@ -1050,8 +1051,8 @@ def main():
         from oracle import scheduler_ref
         fin = np.isfinite(ref[1])
         ref_plan = scheduler_ref.plan_ref(wl.qo_lens, wl.kv_lens, g=wl.g, H_kv=wl.H_kv, num_ctas=args.num_ctas,
-                                          align=wl.page_size, T_q=16, qo_begin=inp_cpu.qo_indptr[:-1],
-                                          page_begin=inp_cpu.kv_page_indptr[:-1])
+                                          align=wl.page_size, T_q=16, qo_begin=head_inputs["qo_indptr"][:-1],
+                                          page_begin=head_inputs["kv_page_indptr"][:-1])
         parity = {"workload": "configs[1] layer 0, all 128 x 32 rows, vs the float64 oracle",
                   "max_abs_do": float(np.max(np.abs(head_check["o"] - ref[0]))),
                   "max_abs_dlse": float(np.max(np.abs(head_check["lse"][fin] - ref[1][fin]))),
