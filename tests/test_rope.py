@@ -138,3 +138,32 @@ def test_rope_c2_full_size_graph_pdl(cuda_device):
         o, l = outs[r]
         assert_close((o.float().cpu().numpy(), l.cpu().numpy()), oracle.attention_from_inputs(inp, req_list=reqs),
                      "bf16", rows=rows_of_requests(inp, reqs), what=f"rope c2 layer {r}")
+
+
+def test_rope_with_window_softcap_alibi(cuda_device):
+    """RoPE (a Query/KeyTransform) composes with the LogitsMask / LogitsTransform variants, which act
+    on the rotated logits: sliding window + soft-cap + ALiBi on the decode kernel and the CUDA-core
+    kernel (prefill tiles)."""
+    base = synth.Workload("rv", 32, 8, 128, 16, "bf16", "causal", np.array([1, 3, 2], np.int32),
+                          np.array([900, 300, 2049], np.int32))
+    wl = dataclasses.replace(_rope(base), window=256, soft_cap=30.0, alibi=True)
+    inp = synth.make_inputs(wl, device=cuda_device)
+    ref = oracle.attention_from_inputs(inp)
+    for tile_q in (16, 64):
+        cfg_kw = dict(num_ctas=37, tile_q=tile_q, window=wl.window, soft_cap=wl.soft_cap, alibi=True)
+        gpu = _run(inp, **cfg_kw)
+        assert gpu[2].selected_kernel() == ("tc_decode" if tile_q == 16 else "simt")
+        assert_close(gpu, ref, "bf16", what=f"rope + variants T_q={tile_q}")
+
+
+def test_rope_contiguous_kv(cuda_device):
+    """RoPE on the contiguous (ragged) KV layout: positions are logical token indices either way."""
+    from tests.test_ragged_kv import run_ragged
+    wl = _rope(synth.Workload("rr", 32, 8, 128, 16, "bf16", "none", np.ones(3, np.int32),
+                              np.array([1, 700, 2049], np.int32)))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    cfg = bsra.make_config(H_qo=32, H_kv=8, D=128, page_size=128, dtype="bf16", max_batch=3, max_total_qo_rows=3,
+                           num_ctas=64, tile_q=16, ragged_kv=True, rope_theta=wl.rope_theta)
+    gpu = run_ragged(inp, bsra.Engine(cfg, 0))
+    assert gpu[2].selected_kernel() == "tc_decode"
+    assert_close(gpu, oracle.attention_from_inputs(inp), "bf16", what="rope contiguous KV")
