@@ -672,6 +672,7 @@ def bench_scheduler(dev, pk, args):
         rows = wl.batch * wl.H_kv
         res = {}
         for name, kw in (("algorithm1", dict(num_ctas=args.num_ctas)),
+                         ("algorithm1_queue_balanced", dict(num_ctas=args.num_ctas, balance_ctas=True)),
                          ("no_split_lpt", dict(num_ctas=args.num_ctas, kv_chunk_min=1 << 30)),
                          ("row_per_cta", dict(num_ctas=rows, kv_chunk_min=1 << 30))):
             eng = L.engine(tile_q=16, kernel=args.kernel, **kw)

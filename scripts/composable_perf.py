@@ -55,10 +55,8 @@ def main():
     variants.append(("base_pdl", dict(prefix_tiles=(64, 128), balance=False, prefix_ctas=148, suffix_ctas=148,
                                       pdl=True)))
     variants.append(("pair_pdl", dict(prefix_ctas=148, suffix_ctas=148, pdl=True)))
-    for c in (56, 64, 72):
-        variants.append((f"conc_{c}", dict(prefix_ctas=c, suffix_ctas=148 - c, concurrent=True)))
-        variants.append((f"conc_{c}_spdl", dict(prefix_ctas=c, suffix_ctas=148 - c, concurrent=True,
-                                                suffix_pdl=True)))
+    for pc, sc in ((64, 84), (84, 64), (20, 128), (44, 104), (64, 64)):
+        variants.append((f"conc_{pc}_{sc}", dict(prefix_ctas=pc, suffix_ctas=sc, concurrent=True)))
     for name, kw in variants:
         comp = bsra.ComposableDecode(H_qo=32, H_kv=8, D=128, page_size=16, n_branch=n, **kw)
         comp.plan(c0.prefix, c0.suffix, c0.sm_scale)
