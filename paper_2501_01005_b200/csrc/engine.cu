@@ -953,7 +953,7 @@ bsra_status bsra_plan_export(const bsra_engine* e, int32_t from_device, int32_t*
 }
 
 bsra_status bsra_plan_stats(const bsra_engine* e, int64_t* cta_cost, int32_t cap, int64_t* makespan) {
-  if (!e || !e->planned) return fail(BSRA_EINVAL, "no plan");
+  if (!e || !e->planned || e->image.empty()) return fail(BSRA_EINVAL, "no host plan (device-built plans: export them)");
   const int32_t* im = e->image.data();
   const int nc = im[2], T_q = im[3], n_items = im[5];
   const int64_t alpha = e->cfg.cost_alpha ? e->cfg.cost_alpha : 1, beta = e->cfg.cost_beta ? e->cfg.cost_beta : 1;
