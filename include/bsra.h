@@ -153,6 +153,12 @@ typedef struct {
  * cp.async flavour of the row gather (A/B and tests). */
 #define BSRA_FLAG_CP_GATHER 8
 #define BSRA_FLAG_CP_ASYNC 16
+/* flags: BSRA_FLAG_DEFER_CONTRACTION (engines whose tiles can exceed 16 rows, i.e. whose split
+ * rows are merged by the separate contraction kernel): bsra_run launches only the attention
+ * kernel; the split rows' partial states stay in the workspace until bsra_contract folds them.
+ * This lets the contraction of one format fold a second format's state in the same pass
+ * (composable formats: prefix ⊕ suffix). */
+#define BSRA_FLAG_DEFER_CONTRACTION 32
 
 typedef struct bsra_engine bsra_engine;
 
@@ -214,6 +220,20 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
                      const int64_t* k_strides, const int64_t* v_strides, const int32_t* kv_page_indices,
                      const uint8_t* custom_mask, const int64_t* mask_bit_indptr, void* o, float* lse,
                      void* stream);
+
+/* Contraction stage of the last bsra_run of a BSRA_FLAG_DEFER_CONTRACTION engine,
+ * enqueued on `stream` (stream order after that run): every merge list of the current plan is
+ * folded with ⊕ in plan order (R17) into o / lse (layout as bsra_run's o / lse; o in `o_dtype`,
+ * BSRA_F32 / BSRA_F16 / BSRA_BF16, which may differ from the engine's o_dtype). With
+ * o_extra / lse_extra (DEVICE fp32 [total_qo_rows, H_qo, head_dim] / [total_qo_rows, H_qo], the
+ * layout of o) each folded row is further ⊕-combined with the extra state of the same output row,
+ * in the same closed form (the composable formats' prefix ⊕ suffix). Rows the run
+ * wrote through (unsplit items, App. D.2) are not touched, so an extra state requires a plan in
+ * which every item is split (bsra_plan_stats / the image: n_slots == n_items): BSRA_EUNSUPPORTED
+ * otherwise. o_extra / lse_extra: both or neither. May be captured in a CUDA graph with the run.
+ * Errors: EINVAL (no deferred run, flag not set, NULL o, bad o_dtype), EUNSUPPORTED. */
+bsra_status bsra_contract(bsra_engine* e, const float* o_extra, const float* lse_extra, void* o, int32_t o_dtype,
+                          float* lse, void* stream);
 
 /* Device-side inspector (the paper's future work, "move the scheduler to device"): one
  * kernel builds, from DEVICE BSR arrays, the same plan image bsra_plan builds on the host (bit for

@@ -48,11 +48,12 @@ FLAG_RAGGED_KV = 2  # BSRA_FLAG_RAGGED_KV: contiguous (ragged) K/V, no page tabl
 FLAG_BALANCE_CTAS = 4  # BSRA_FLAG_BALANCE_CTAS: plan with the queue count that minimises the makespan
 FLAG_CP_GATHER = 8  # BSRA_FLAG_CP_GATHER: decode kernel gathers K/V rows (TMA gather4 or cp.async)
 FLAG_CP_ASYNC = 16  # BSRA_FLAG_CP_ASYNC: ... with 16-byte cp.async
+FLAG_DEFER_CONTRACTION = 32  # BSRA_FLAG_DEFER_CONTRACTION: run() leaves split rows to bsra_contract
 
 
 _lib = None
 EXPORTS = ["bsra_version", "bsra_num_sms", "bsra_workspace_bytes", "bsra_engine_create", "bsra_engine_destroy",
-           "bsra_plan", "bsra_run", "bsra_graph_release", "bsra_plan_device", "bsra_plan_device_status", "bsra_set_kv_scales", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
+           "bsra_plan", "bsra_run", "bsra_contract", "bsra_graph_release", "bsra_plan_device", "bsra_plan_device_status", "bsra_set_kv_scales", "bsra_plan_ragged", "bsra_run_ragged", "bsra_merge_states", "bsra_merge_many",
            "bsra_plan_host", "bsra_plan_export",
            "bsra_plan_stats", "bsra_last_run_launches", "bsra_selected_kernel", "bsra_last_error",
            "bsra_dist_unique_id", "bsra_dist_create", "bsra_dist_destroy", "bsra_dist_scratch_bytes",
@@ -77,6 +78,7 @@ def lib():
             "bsra_engine_destroy": (None, [P]),
             "bsra_plan": (I32, [P, I32, P, P, P, ctypes.c_float, P]),
             "bsra_run": (I32, [P, P, P, P, P, P, P, P, P, P, P, P]),
+            "bsra_contract": (I32, [P, P, P, P, I32, P, P]),
             "bsra_set_kv_scales": (I32, [P, ctypes.c_float, ctypes.c_float]),
             "bsra_graph_release": (I32, [P]),
             "bsra_plan_device": (I32, [P, I32, P, P, P, ctypes.c_float, P]),
@@ -123,7 +125,8 @@ def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="n
                 max_total_qo_rows=1, num_ctas=0, tile_set=(16, 64, 128, 256), tile_q=0, alpha=1, beta=1,
                 kv_chunk_align=0, kv_chunk_min=0, kernel="auto", pdl=False, ragged_kv=False, window=0,
                 soft_cap=0.0, kv_dtype=None, k_scale=0.0, v_scale=0.0, alibi=False, balance_ctas=False,
-                max_total_kv_tokens=0, max_qo_len=0, rope_theta=0.0, rope_scale=0.0, cp_gather=False, cp_async=False) -> Config:
+                max_total_kv_tokens=0, max_qo_len=0, rope_theta=0.0, rope_scale=0.0, cp_gather=False, cp_async=False,
+                defer_contraction=False) -> Config:
     """window: sliding window W (0 = off, DESIGN.md R26); soft_cap: logits soft-cap c (0 = off, R27);
     kv_dtype "e4m3": fp8 KV cache with per-tensor scales k_scale / v_scale (0 = 1; R28);
     max_total_kv_tokens / max_qo_len: engine bounds (include/bsra.h)."""
@@ -136,7 +139,8 @@ def make_config(*, H_qo, H_kv, D, page_size, dtype="bf16", o_dtype=None, mask="n
     c.alibi = 1 if alibi else 0
     c.sliding_window, c.logits_soft_cap = int(window), float(soft_cap)
     c.flags = ((FLAG_PDL if pdl else 0) | (FLAG_RAGGED_KV if ragged_kv else 0) | (FLAG_BALANCE_CTAS if balance_ctas else 0)
-               | (FLAG_CP_GATHER if cp_gather else 0) | (FLAG_CP_ASYNC if cp_async else 0))
+               | (FLAG_CP_GATHER if cp_gather else 0) | (FLAG_CP_ASYNC if cp_async else 0)
+               | (FLAG_DEFER_CONTRACTION if defer_contraction else 0))
     c.num_qo_heads, c.num_kv_heads, c.head_dim, c.page_size = H_qo, H_kv, D, page_size
     c.dtype = DTYPE[dtype] if isinstance(dtype, str) else dtype
     od = o_dtype if o_dtype is not None else dtype
@@ -247,6 +251,13 @@ class Engine:
         _check(lib().bsra_run_ragged(self._h, _p(q), _p(k), _p(v), ctypes.cast(ks, ctypes.c_void_p),
                                      ctypes.cast(vs, ctypes.c_void_p), _p(custom_mask), _p(mask_bit_indptr), _p(o),
                                      _p(lse), self._stream(stream)))
+
+    def contract(self, o, lse=None, o_extra=None, lse_extra=None, stream=None):
+        """bsra_contract: fold the deferred run's merge lists into o / lse, each row ⊕ the extra
+        state (o_extra fp32 [rows, H_qo, D], lse_extra [rows, H_qo]) when given."""
+        inv = {v: k for k, v in TORCH_DTYPE.items()}
+        _check(lib().bsra_contract(self._h, _p(o_extra), _p(lse_extra), _p(o), inv[o.dtype], _p(lse),
+                                   self._stream(stream)))
 
     def export_plan(self, from_device=False, stream=None) -> np.ndarray:
         L = lib()
@@ -398,7 +409,10 @@ class ComposableDecode:
     query rows (large B_r: one "request" with l_qo = n, tensor-core tile; with g = 4 and n = 64
     the 256 fused rows are one paired 256-row tile, so every prefix K/V tile staged in shared
     memory serves all branches) and per-branch suffix blocks (B_r = 1) — one engine ("wrapper")
-    each; the two attention states are combined with ⊕ (bsra_merge_states).
+    each; the two attention states are combined with ⊕. The prefix engine defers its contraction
+    (BSRA_FLAG_DEFER_CONTRACTION): when every prefix item is split, one bsra_contract launch folds
+    the prefix's partial states AND the suffix state into o (prefix ⊕ suffix in one pass);
+    otherwise its contraction writes the prefix state and bsra_merge_states combines the two.
 
     concurrent: the two engines run at the same time on disjoint SM sets — the prefix engine's
     persistent grid takes `prefix_ctas` SMs (tensor-bound tiles), the suffix engine the other
@@ -413,7 +427,8 @@ class ComposableDecode:
         self.concurrent = concurrent
         self.prefix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
                                          max_batch=1, max_total_qo_rows=n_branch, num_ctas=prefix_ctas,
-                                         tile_set=prefix_tiles, kernel=kernel, balance_ctas=balance, pdl=pdl), device)
+                                         tile_set=prefix_tiles, kernel=kernel, balance_ctas=balance, pdl=pdl,
+                                         defer_contraction=True), device)
         self.suffix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
                                          max_batch=n_branch, max_total_qo_rows=n_branch, num_ctas=suffix_ctas,
                                          tile_q=16, kernel=kernel, max_qo_len=1,
@@ -424,10 +439,13 @@ class ComposableDecode:
         self.o_s = torch.empty((n_branch, H_qo, D), device=dev)
         self.l_s = torch.empty((n_branch, H_qo), device=dev)
         self.side = torch.cuda.Stream(device=dev) if concurrent else None
+        self.fold_suffix = False
 
     def plan(self, prefix: dict, suffix: dict, sm_scale=0.0, stream=None):
         self.prefix.plan(prefix["qo_indptr"], prefix["kv_page_indptr"], prefix["kv_last_page_len"], sm_scale, stream)
         self.suffix.plan(suffix["qo_indptr"], suffix["kv_page_indptr"], suffix["kv_last_page_len"], sm_scale, stream)
+        img = self.prefix.export_plan()
+        self.fold_suffix = bool(img.size) and int(img[5]) == int(img[7])  # every prefix item split
 
     def run(self, q, k_pool, v_pool, strides, prefix_indices, suffix_indices, o, lse=None, stream=None):
         st = stream if stream is not None else torch.cuda.current_stream()
@@ -439,8 +457,12 @@ class ComposableDecode:
         else:
             self.prefix.run(q, k_pool, v_pool, strides, strides, prefix_indices, self.o_p, self.l_p, stream=st)
             self.suffix.run(q, k_pool, v_pool, strides, strides, suffix_indices, self.o_s, self.l_s, stream=st)
-        merge_states(self.o_p, self.l_p, self.o_s, self.l_s, o_out=o, lse_out=lse, stream=st)
+        if self.fold_suffix:  # one pass: prefix slots ⊕ suffix state -> o
+            self.prefix.contract(o, lse, o_extra=self.o_s, lse_extra=self.l_s, stream=st)
+        else:
+            self.prefix.contract(self.o_p, self.l_p, stream=st)
+            merge_states(self.o_p, self.l_p, self.o_s, self.l_s, o_out=o, lse_out=lse, stream=st)
         return o, lse
 
     def launches(self) -> int:
-        return self.prefix.last_launches() + self.suffix.last_launches() + 1
+        return self.prefix.last_launches() + 1 + self.suffix.last_launches() + (0 if self.fold_suffix else 1)

@@ -52,6 +52,9 @@ struct AttnParams {
   // angle's fraction of a turn, exact for every position
   int32_t rope;
   uint64_t rope_f[64];
+  // contraction kernel only (bsra_contract): an extra state ⊕-combined into every folded row
+  const float* x_o;    // [rows, H_qo, D] fp32, the layout of o; NULL = none
+  const float* x_lse;  // [rows, H_qo]
 };
 
 // sin / cos of the RoPE angle pos * theta (frequency f = theta / 2pi in 2^-64 turns): the 64-bit

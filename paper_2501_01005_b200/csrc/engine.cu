@@ -75,8 +75,10 @@ bsra_status validate_config(const bsra_config& c) {
   if (c.kv_chunk_align < 0 || c.kv_chunk_min < 0) return fail(BSRA_EINVAL, "negative chunk parameters");
   if (c.kernel < BSRA_KERNEL_AUTO || c.kernel > BSRA_KERNEL_TC) return fail(BSRA_EINVAL, "bad kernel selector");
   if (c.flags & ~(BSRA_FLAG_PDL | BSRA_FLAG_RAGGED_KV | BSRA_FLAG_BALANCE_CTAS | BSRA_FLAG_CP_GATHER |
-                  BSRA_FLAG_CP_ASYNC))
+                  BSRA_FLAG_CP_ASYNC | BSRA_FLAG_DEFER_CONTRACTION))
     return fail(BSRA_EINVAL, "unknown flag bits");
+  if ((c.flags & BSRA_FLAG_DEFER_CONTRACTION) && (tm & 14) == 0)
+    return fail(BSRA_EINVAL, "BSRA_FLAG_DEFER_CONTRACTION: decode-only engines merge in-kernel (no contraction stage)");
   if ((c.flags & BSRA_FLAG_RAGGED_KV) && c.page_size != 128)
     return fail(BSRA_EINVAL, "BSRA_FLAG_RAGGED_KV engines take page_size = 128 (the KV tile)");
   if (c.sliding_window < 0) return fail(BSRA_EINVAL, "sliding_window < 0");
@@ -184,6 +186,8 @@ struct bsra_engine {
   bool captured = false;     // a run() was captured into a CUDA graph since the last release
   LaunchSig cap_sig;         // launch choices of that captured run()
   long long* trace = nullptr;  // BSRA_EXPERIMENTS builds: device buffer for kernel pipeline traces
+  bsra::AttnParams deferred{};  // BSRA_FLAG_DEFER_CONTRACTION: the last run's parameters (bsra_contract)
+  bool have_deferred = false;
   int32_t last_launches = 0;
   const char* selected = "none";
 };
@@ -598,6 +602,14 @@ bsra_status launch_contraction_t(const bsra::AttnParams& p, int grid, cudaStream
   return BSRA_OK;
 }
 
+// Contraction grid: one warp per (list, row) up to a full GPU of 256-thread blocks (the stage is
+// latency-bound: each warp's slot loads are one dependent round trip). Fixed per engine (lists <=
+// num_ctas, rows <= T_max), so captured graphs stay valid across re-plans.
+int contraction_grid(const bsra_engine* e) {
+  const int64_t warps = (int64_t)e->cfg.num_ctas * e->lay.T_max;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 8 * (int64_t)e->sms));
+}
+
 template <typename TO>
 bsra_status launch_contraction_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st) {
   return D == 64 ? launch_contraction_t<TO, 64>(p, grid, st) : launch_contraction_t<TO, 128>(p, grid, st);
@@ -771,8 +783,11 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     if (s) return s;
   }
   e->last_launches = 1 + gather_launches;
-  if (!p.fused_merge) {  // contraction stage: fixed grid, exits at once if nothing split
-    const int cgrid = std::max(1, std::min(grid, 2 * e->sms));
+  if (!p.fused_merge && (c.flags & BSRA_FLAG_DEFER_CONTRACTION)) {  // bsra_contract runs the stage
+    e->deferred = p;
+    e->have_deferred = true;
+  } else if (!p.fused_merge) {  // contraction stage: fixed grid, exits at once if nothing split
+    const int cgrid = contraction_grid(e);
     if (c.o_dtype == BSRA_F32 || c.dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
     else if (c.dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
     else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
@@ -897,6 +912,33 @@ bsra_status bsra_merge_states(const void* o_a, const float* lse_a, const void* o
       return merge_states_o<__nv_bfloat16>(out_dtype, head_dim, o_a, lse_a, o_b, lse_b, n, o_out, lse_out, st);
   }
   return fail(BSRA_EINVAL, "bad dtype");
+}
+
+bsra_status bsra_contract(bsra_engine* e, const float* o_extra, const float* lse_extra, void* o, int32_t o_dtype,
+                          float* lse, void* stream) {
+  if (!e) return fail(BSRA_EINVAL, "NULL engine");
+  const bsra_config& c = e->cfg;
+  if (!(c.flags & BSRA_FLAG_DEFER_CONTRACTION)) return fail(BSRA_EINVAL, "engine without BSRA_FLAG_DEFER_CONTRACTION");
+  if (!e->have_deferred) return fail(BSRA_EINVAL, "no deferred run to contract");
+  if (!o) return fail(BSRA_EINVAL, "NULL o");
+  if ((o_extra == nullptr) != (lse_extra == nullptr)) return fail(BSRA_EINVAL, "o_extra and lse_extra: both or neither");
+  if (o_extra && e->device_planned) return fail(BSRA_EUNSUPPORTED, "an extra state needs a host-built plan");
+  if (o_extra && e->summary.n_slots != e->summary.n_items)
+    return fail(BSRA_EUNSUPPORTED, "an extra state needs every item split (rows written through are final)");
+  if (o_dtype != BSRA_F32 && o_dtype != BSRA_F16 && o_dtype != BSRA_BF16) return fail(BSRA_EINVAL, "bad o_dtype");
+  bsra::AttnParams p = e->deferred;
+  p.o = o;
+  p.o_f32 = o_dtype == BSRA_F32;
+  p.lse = lse;
+  p.x_o = o_extra;
+  p.x_lse = lse_extra;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int cgrid = contraction_grid(e);
+  bsra_status s;
+  if (o_dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
+  else if (o_dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
+  else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
+  return s;
 }
 
 bsra_status bsra_merge_many(const float* o_parts, const float* lse_parts, int32_t P, int64_t rows, int32_t heads,

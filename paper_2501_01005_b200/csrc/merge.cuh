@@ -57,14 +57,36 @@ __device__ __forceinline__ int list_of_slot(const PlanView& pv, int slot) {
   return lo;
 }
 
+// A merge list's metadata (everything the merging CTA needs besides the partials). The decode
+// kernels resolve it for their staged items while the K/V stream runs, so the tail of a launch
+// does not pay the slot -> list binary search and the plan reads (dependent global loads) after
+// the arrival.
+struct ListMeta {
+  int l, s0, s1, kvh, qt, nrows;
+  int64_t qo_begin;
+};
+
+__device__ __forceinline__ ListMeta list_meta(const PlanView& pv, int l, int g) {
+  ListMeta m;
+  m.l = l;
+  m.s0 = pv.list_indptr[l];
+  m.s1 = pv.list_indptr[l + 1];
+  const int req = pv.list_req[l];
+  m.kvh = pv.list_kvh[l];
+  m.qt = pv.list_qtile[l];
+  m.nrows = min(pv.T_q, pv.req_qo_len[req] * g - m.qt * pv.T_q);
+  m.qo_begin = pv.req_qo_begin[req];
+  return m;
+}
+
 template <typename TO, int D>
-__device__ __forceinline__ void fused_contraction(const AttnParams& p, const PlanView& pv, int slot, int tid, int nthr,
-                                                  int bar_id, volatile int* s_flag) {
+__device__ __forceinline__ void fused_contraction_meta(const AttnParams& p, const PlanView& pv, const ListMeta* pre,
+                                                       int slot, int tid, int nthr, int bar_id, volatile int* s_flag) {
   __threadfence();  // this thread's partial writes are visible device-wide
   asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");
   if (tid == 0) {
-    const int l = list_of_slot(pv, slot);
-    const int len = pv.list_indptr[l + 1] - pv.list_indptr[l];
+    const int l = pre ? pre->l : list_of_slot(pv, slot);
+    const int len = pre ? pre->s1 - pre->s0 : pv.list_indptr[l + 1] - pv.list_indptr[l];
     const int old = atomicAdd(p.counters + l, 1);
     const bool last = old == len - 1;
     if (last) p.counters[l] = 0;  // every other arrival of this launch has happened
@@ -74,10 +96,8 @@ __device__ __forceinline__ void fused_contraction(const AttnParams& p, const Pla
   const int l = *s_flag;
   if (l >= 0) {
     __threadfence();  // acquire: the other CTAs' partials are visible
-    const int req = pv.list_req[l], kvh = pv.list_kvh[l], qt = pv.list_qtile[l];
-    const int lq = pv.req_qo_len[req];
-    const int nrows = min(pv.T_q, lq * p.g - qt * pv.T_q);
-    const int s0 = pv.list_indptr[l], s1 = pv.list_indptr[l + 1];
+    const ListMeta lm = pre ? *pre : list_meta(pv, l, p.g);
+    const int kvh = lm.kvh, qt = lm.qt, nrows = lm.nrows, s0 = lm.s0, s1 = lm.s1;
     // ⊕ over the list in closed form (max-shifted): per row one warp forms the slot weights
     // w_s = e^{lse_s - m} once, then lanes accumulate D/32 contiguous dims per slot in slot order.
     constexpr int kPer = D / 32;
@@ -122,7 +142,7 @@ __device__ __forceinline__ void fused_contraction(const AttnParams& p, const Pla
       const float lse = tot > 0.f ? m + __logf(tot) : -INFINITY;
       const int f = qt * pv.T_q + r;
       const int tok = f / p.g, head = kvh * p.g + f % p.g;
-      const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
+      const int64_t orow = (lm.qo_begin + tok) * (int64_t)p.H_qo + head;
       if (p.o_f32) {
         float* dst = reinterpret_cast<float*>(p.o) + orow * D + lane * kPer;
 #pragma unroll
@@ -136,6 +156,12 @@ __device__ __forceinline__ void fused_contraction(const AttnParams& p, const Pla
     }
   }
   asm volatile("bar.sync %0, %1;\n" ::"r"(bar_id), "r"(nthr) : "memory");  // s_flag reuse
+}
+
+template <typename TO, int D>
+__device__ __forceinline__ void fused_contraction(const AttnParams& p, const PlanView& pv, int slot, int tid, int nthr,
+                                                  int bar_id, volatile int* s_flag) {
+  fused_contraction_meta<TO, D>(p, pv, nullptr, slot, tid, nthr, bar_id, s_flag);
 }
 
 // Standalone contraction (engines whose tiles can be 64/128/256 rows, where a merge list is too
@@ -159,9 +185,18 @@ __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant_
     if (f >= lq * p.g) continue;
     const int tok = f / p.g, head = kvh * p.g + f % p.g;
     const int s0 = pv.list_indptr[li], s1 = pv.list_indptr[li + 1];
+    const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
+    // bsra_contract's extra state: one more term of the closed form, after the slots
+    float xl = -INFINITY, xo[kPer];
+    if (p.x_o) {
+      xl = p.x_lse[orow];
+      const float* src = p.x_o + orow * D + lane * kPer;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) xo[j] = src[j];
+    }
     float m = -INFINITY;
     for (int s = s0 + lane; s < s1; s += 32) m = fmaxf(m, p.part_lse[(int64_t)pv.list_slot[s] * p.T_slot + r]);
-    m = warp_max(m);
+    m = fmaxf(warp_max(m), xl);
     float acc[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) acc[j] = 0.f;
@@ -190,12 +225,17 @@ __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant_
           }
         }
       }
+      if (xl != -INFINITY) {
+        const float wx = __expf(xl - m);
+        tot += wx;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) acc[j] = fmaf(wx, xo[j], acc[j]);
+      }
     }
     const float inv = tot > 0.f ? 1.f / tot : 0.f;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) acc[j] *= inv;
     const float lse = tot > 0.f ? m + __logf(tot) : -INFINITY;
-    const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
     store_row<TO, D>(p.o, orow, lane, acc, p.o_f32);
     if (p.lse && lane == 0) p.lse[orow] = lse;
   }

@@ -89,7 +89,8 @@ constexpr int kOffRed = kOffBar + 512;
 // red [4][kN], vote flags [2][4], epilogue hand-off sums [2][4][kN] and max [2][kN]
 constexpr int kOffItems = kOffRed + 1024;
 constexpr int kStagedItems = 64;  // the CTA's first queue entries, decoded once into shared memory
-constexpr int kSmemBytes = kOffItems + kStagedItems * 80 + 1024;  // + alignment slack
+constexpr int kOffMeta = kOffItems + kStagedItems * 80;  // merge-list metadata of staged split items
+constexpr int kSmemBytes = kOffMeta + kStagedItems * 32 + 1024;  // + alignment slack
 constexpr int kThreads = 320;  // producer, 4 softmax warps, MMA warp, 4 epilogue warps
 constexpr int kThreadsRope = 576;  // + 8 RoPE warps (two per SM sub-partition) in the fused-RoPE variant
 constexpr int threads_for(bool rope) { return rope ? kThreadsRope : kThreads; }
@@ -104,6 +105,7 @@ struct DecItem {
 };
 
 static_assert(sizeof(DecItem) <= 80, "staged item slot");
+static_assert(sizeof(ListMeta) <= 32, "staged list metadata slot");
 
 __device__ __forceinline__ DecItem dec_item(const PlanView& pv, int it, int g) {
   DecItem d;
@@ -144,6 +146,13 @@ __device__ __forceinline__ void rope_chunk(uint8_t* lo, uint8_t* hi, int64_t pos
   *reinterpret_cast<uint4*>(hi) = b;
 }
 
+// Pipeline trace points (BSRA_EXPERIMENTS builds only; scripts/trace_decode.py)
+#ifdef BSRA_EXPERIMENTS
+#define DEC_TRACE(e) do { if (p.trace) p.trace[(e) * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns(); } while (0)
+#else
+#define DEC_TRACE(e) do { } while (0)
+#endif
+
 // kF16: fp16 q / o (else bf16) at compile time: one code path per instantiation (instruction
 // fetch stalls measured on the fp8 kernel when both were inlined). kRope: fused RoPE (R31) —
 // eight more warps rotate each landed K tile in shared memory and each item's Q tile before the
@@ -181,6 +190,14 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
   float* hmax = hsum + 2 * 4 * kN;                          // [2][kN] running max
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) DEC_TRACE(7);
+#ifdef BSRA_EXPERIMENTS
+  if (p.trace && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[15 * 1024 + blockIdx.x] = smid + 1;
+  }
+#endif
   const PlanView pv = load_plan(p.plan);
   const int g = p.g;
   const int it0 = pv.cta_indptr[blockIdx.x], it1 = pv.cta_indptr[blockIdx.x + 1];
@@ -192,6 +209,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
   auto item_at = [&](int it) { return it - it0 < kStagedItems ? staged[it - it0] : dec_item(pv, it, g); };
 
   if (threadIdx.x == 0) {
+    DEC_TRACE(0);
     for (int s = 0; s < kStages; ++s) {
       ptx::mbar_init(&full[s], kRow && tp.cp == 1 ? 32 : 1);  // cp.async gather: one arrival per lane
       ptx::mbar_init(&empty[s], 1);
@@ -224,6 +242,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) DEC_TRACE(6);
   pdl_launch_dependents();  // PDL: the next kernel's CTAs may take SMs this grid releases
   // debug (p.trace set): per-CTA start / end time, globaltimer ns (scripts/cta_balance.py)
 #ifdef BSRA_EXPERIMENTS
@@ -242,6 +261,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     uint32_t ephase = 1;  // fresh barriers: waiting on parity 1 passes
     uint32_t qphase[2] = {1, 1};
     int qb = 0;
+    if (lane == 0) DEC_TRACE(11);
     for (int it = it0; it < it1; ++it) {
       const DecItem d = item_at(it);
       // ---- Q tile: 16 fused rows = q_tb tokens x q_hb heads, two 64-column halves
@@ -340,6 +360,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
             ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * (kD * 4));
           }
           __syncwarp();
+          if (lane == 0 && it == it0 && ti == 0) DEC_TRACE(8);
           if (lane < nsub) {
             uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
             uint8_t* vd = kd + kKVBytes;
@@ -399,6 +420,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       const DecItem d = item_at(it);
       ptx::mbar_wait(kRope ? &qrot[qb] : &full_q[qb], qphase[qb]);
       qphase[qb] ^= 1;
+      if (lane == 0 && it == it0) DEC_TRACE(9);
       if (d.ntiles == 0) {
         ptx::mbar_arrive_warp(&empty_q[qb]);
         qb ^= 1;
@@ -407,6 +429,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       const uint64_t bq = ptx::smem_desc_sw128(sbase + kOffQ + qb * kQBytes, 16, 1024);
       for (int ti = 0; ti < d.ntiles; ++ti) {
         ptx::mbar_wait(kRope ? &krot[stage] : &full[stage], fphase);
+        if (lane == 0 && it == it0 && ti == 0) DEC_TRACE(10);
         ptx::mbar_wait(&s_free[sb], sfph[sb]);
         sfph[sb] ^= 1;
         if (kRow && tp.cp == 1) ptx::fence_proxy_async();  // cp.async (generic-proxy) writes -> tensor core
@@ -475,6 +498,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         const int n = (int)imin64(kTile, d.ke - t0);
         ptx::mbar_wait(&bar_s[sbuf], sph[sbuf]);
         sph[sbuf] ^= 1;
+        if (ct == 0 && it == it0 && ti == 0) DEC_TRACE(1);
         ptx::tc_fence_after();
         float s[kC];
         ptx::tmem_ld<kC>(tmem + lane_addr + sbuf * 16, s);
@@ -627,6 +651,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       if (lane == 0) ptx::mbar_arrive(&epi_full[ob]);
       ob ^= 1;
     }
+    if (ct == 0) DEC_TRACE(2);
   } else if (kRope && warp >= 10) {
     // ====== RoPE warps (10..17): rotate Q (per item) and K (per tile) in shared memory (R31) ======
     const int rt = threadIdx.x - dec::kThreads;  // 0..255
@@ -708,7 +733,16 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
     int ob = 0;
     uint32_t efph[2] = {0, 0};
+    // merge-list metadata of the staged split items, resolved while the first tiles stream in
+    ListMeta* smeta = reinterpret_cast<ListMeta*>(smem + kOffMeta);
+    const int nstaged = min(kStagedItems, it1 - it0);
+    if (p.fused_merge) {
+      for (int k = et; k < nstaged; k += 128)
+        if (staged[k].slot >= 0) smeta[k] = list_meta(pv, list_of_slot(pv, staged[k].slot), g);
+      ptx::named_bar_sync(2, 128);
+    }
     pdl_wait();  // PDL: the previous kernel on the stream has completed before we write
+    if (et == 0) DEC_TRACE(3);
     for (int it = it0; it < it1; ++it) {
       const DecItem d = item_at(it);
       float ov[kC], l[kC], mm[kC];
@@ -761,12 +795,15 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           }
         }
       }
+      if (et == 0 && it + 1 == it1) DEC_TRACE(4);
       if (d.slot >= 0 && p.fused_merge) {  // split item: the CTA completing its merge list folds it
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
-        if constexpr (kF16) fused_contraction<__half, kD>(p, pv, d.slot, et, 128, 2, s_flag);
-        else fused_contraction<__nv_bfloat16, kD>(p, pv, d.slot, et, 128, 2, s_flag);
+        const ListMeta* pre = it - it0 < kStagedItems ? smeta + (it - it0) : nullptr;
+        if constexpr (kF16) fused_contraction_meta<__half, kD>(p, pv, pre, d.slot, et, 128, 2, s_flag);
+        else fused_contraction_meta<__nv_bfloat16, kD>(p, pv, pre, d.slot, et, 128, 2, s_flag);
       }
     }
+    if (et == 0) DEC_TRACE(5);
   }
   ptx::tc_fence_before();
   __syncthreads();

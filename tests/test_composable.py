@@ -63,3 +63,92 @@ def test_gpu_composable_c4_full(cuda_device):
     ci = synth.c4_composable(device=cuda_device)
     gpu = _gpu_composable(ci, cuda_device, prefix_ctas=148, suffix_ctas=148)
     assert_close(gpu, _oracle(ci, "single"), "bf16", what="c4 full")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pc,sc,conc,fold", [(148, 148, False, True), (64, 84, True, True), (8, 148, False, False),
+                                             (8, 140, True, False)])
+def test_gpu_composable_fold_paths(cuda_device, pc, sc, conc, fold):
+    """bsra_contract with the suffix as extra state (every prefix item split: one launch folds the
+    prefix slots and the suffix) and the fallback (prefix rows written through: contraction, then
+    merge_states), sequential and on concurrent grids."""
+    from tests.helpers import assert_close
+    ci = synth.c4_composable(n_branch=16, prefix_len=2048, suffix_len=100, device=cuda_device)
+    gpu = _gpu_composable(ci, cuda_device, prefix_ctas=pc, suffix_ctas=sc, concurrent=conc)
+    assert gpu[2].fold_suffix == fold
+    assert gpu[2].launches() == (3 if fold else 4)
+    assert_close(gpu, _oracle(ci, "single"), "bf16", what=f"fold={fold} conc={conc}")
+
+
+@pytest.mark.gpu
+def test_gpu_composable_c4_bench_graph(cuda_device):
+    """configs[3] at full size in the bench's launch configuration: prefix on 64 SMs and suffix on
+    84 concurrently, captured in a CUDA graph over two layers (two pools) and replayed."""
+    import paper_2501_01005_b200 as bsra
+    from tests.helpers import assert_close
+    cis = [synth.c4_composable(device=cuda_device, seed_base=100 * r) for r in range(2)]
+    c0 = cis[0]
+    n = c0.q.shape[0]
+    comp = bsra.ComposableDecode(H_qo=32, H_kv=8, D=128, page_size=16, n_branch=n, prefix_ctas=64, suffix_ctas=84,
+                                 concurrent=True)
+    comp.plan(c0.prefix, c0.suffix, c0.sm_scale)
+    assert comp.fold_suffix
+    # each layer its own page tables (same shapes: the plan is shared)
+    idx = [(torch.from_numpy(ci.prefix["kv_page_indices"]).to(cuda_device),
+            torch.from_numpy(ci.suffix["kv_page_indices"]).to(cuda_device)) for ci in cis]
+    outs = [(torch.full((n, 32, 128), float("nan"), device=cuda_device, dtype=torch.bfloat16),
+             torch.full((n, 32), float("nan"), device=cuda_device)) for _ in cis]
+    s = torch.cuda.Stream(device=cuda_device)
+
+    def step():
+        for ci, (pi, si), (o, l) in zip(cis, idx, outs):
+            comp.run(ci.q, ci.k_pool, ci.v_pool, ci.strides, pi, si, o, l, stream=s)
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        step()
+    for o, l in outs:
+        o.fill_(float("nan"))
+        l.fill_(float("nan"))
+    with torch.cuda.stream(s):
+        g.replay()
+        g.replay()
+    torch.cuda.synchronize()
+    for ci, (o, l) in zip(cis, outs):
+        assert_close((o.float().cpu().numpy(), l.cpu().numpy()), _oracle(ci, "single"), "bf16", what="c4 bench graph")
+
+
+@pytest.mark.gpu
+def test_gpu_contract_errors(cuda_device):
+    """bsra_contract: EINVAL without BSRA_FLAG_DEFER_CONTRACTION or before a deferred run;
+    EUNSUPPORTED for an extra state when rows were written through; decode-only engines cannot
+    take the flag."""
+    import paper_2501_01005_b200 as bsra
+    wl = synth.Workload("ce", 8, 2, 128, 16, "bf16", "none", np.array([4, 4], np.int32), np.array([64, 64], np.int32))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    with pytest.raises(bsra.BsraError, match="decode-only"):
+        bsra.Engine(bsra.make_config(H_qo=8, H_kv=2, D=128, page_size=16, tile_set=(16,), defer_contraction=True), 0)
+    o = torch.empty((8, 8, 128), device=cuda_device, dtype=torch.bfloat16)
+    lse = torch.empty((8, 8), device=cuda_device)
+    plain = bsra.Engine(bsra.make_config(H_qo=8, H_kv=2, D=128, page_size=16, max_batch=2, max_total_qo_rows=8,
+                                         tile_q=64, num_ctas=2), 0)
+    with pytest.raises(bsra.BsraError, match="DEFER"):
+        plain.contract(o, lse)
+    eng = bsra.Engine(bsra.make_config(H_qo=8, H_kv=2, D=128, page_size=16, max_batch=2, max_total_qo_rows=8,
+                                       tile_q=64, num_ctas=2, defer_contraction=True), 0)
+    with pytest.raises(bsra.BsraError, match="no deferred run"):
+        eng.contract(o, lse)
+    eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+    eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse)
+    assert eng.last_launches() == 1
+    xo = torch.zeros((8, 8, 128), device=cuda_device)
+    xl = torch.full((8, 8), float("-inf"), device=cuda_device)
+    with pytest.raises(bsra.BsraError, match="every item split"):  # 2 CTAs, 4 rows: nothing split
+        eng.contract(o, lse, o_extra=xo, lse_extra=xl)
+    eng.contract(o, lse)  # no extra: nothing to fold, rows written through stay
+    torch.cuda.synchronize()
+    from tests.helpers import assert_close
+    assert_close((o.float().cpu().numpy(), lse.cpu().numpy()), oracle.attention_from_inputs(inp), "bf16",
+                 what="deferred, unsplit")
