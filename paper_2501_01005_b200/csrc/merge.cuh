@@ -172,7 +172,13 @@ __device__ __forceinline__ void fused_contraction(const AttnParams& p, const Pla
 // warp (a dependent ⊕ chain would leave one load in flight and make the stage latency-bound).
 template <typename TO, int D>
 __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant__ AttnParams p) {
+  // Latency-bound stage: the dependent global round trips per warp are plan header -> list
+  // metadata -> (request, slot ids) -> every slot's lse AND o row (and the extra state) in one
+  // round -> store. The o rows do not depend on the max, so groups of 8 slot rows are loaded
+  // before m is known; the fold itself is the closed form in slot order (bitwise the same as
+  // fused_contraction).
   constexpr int kPer = D / 32;
+  constexpr int kGrp = 8;
   const PlanView pv = load_plan(p.plan);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -180,13 +186,28 @@ __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant_
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += nwarps) {
     const int li = (int)(w / pv.T_q), r = (int)(w % pv.T_q);
     const int req = pv.list_req[li], kvh = pv.list_kvh[li], qt = pv.list_qtile[li];
+    const int s0 = pv.list_indptr[li], s1 = pv.list_indptr[li + 1];
+    const int slot_l = s0 + lane < s1 ? pv.list_slot[s0 + lane] : 0;  // lane s: slot id of list entry s
     const int lq = pv.req_qo_len[req];
+    const int64_t qo_begin = pv.req_qo_begin[req];
     const int f = qt * pv.T_q + r;
     if (f >= lq * p.g) continue;
     const int tok = f / p.g, head = kvh * p.g + f % p.g;
-    const int s0 = pv.list_indptr[li], s1 = pv.list_indptr[li + 1];
-    const int64_t orow = (pv.req_qo_begin[req] + tok) * (int64_t)p.H_qo + head;
-    // bsra_contract's extra state: one more term of the closed form, after the slots
+    const int64_t orow = (qo_begin + tok) * (int64_t)p.H_qo + head;
+    const int ns = s1 - s0;
+    // ---- one round of loads: lse of up to 32 slots (lane-parallel), o rows of the first group,
+    // the extra state
+    const float lse_l = lane < ns ? p.part_lse[(int64_t)slot_l * p.T_slot + r] : -INFINITY;
+    float v[kGrp][kPer];
+#pragma unroll
+    for (int u = 0; u < kGrp; ++u) {
+      const int sl = __shfl_sync(0xffffffffu, slot_l, u);
+      if (u < ns) {
+        const float* src = p.part_o + ((int64_t)sl * p.T_slot + r) * D + lane * kPer;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) v[u][j] = src[j];
+      }
+    }
     float xl = -INFINITY, xo[kPer];
     if (p.x_o) {
       xl = p.x_lse[orow];
@@ -194,31 +215,38 @@ __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant_
 #pragma unroll
       for (int j = 0; j < kPer; ++j) xo[j] = src[j];
     }
-    float m = -INFINITY;
-    for (int s = s0 + lane; s < s1; s += 32) m = fmaxf(m, p.part_lse[(int64_t)pv.list_slot[s] * p.T_slot + r]);
+    float m = lse_l;
+    for (int s = s0 + 32 + lane; s < s1; s += 32)  // lists longer than a warp
+      m = fmaxf(m, p.part_lse[(int64_t)pv.list_slot[s] * p.T_slot + r]);
     m = fmaxf(warp_max(m), xl);
     float acc[kPer];
 #pragma unroll
     for (int j = 0; j < kPer; ++j) acc[j] = 0.f;
     float tot = 0.f;
     if (m != -INFINITY) {
-      for (int sb = s0; sb < s1; sb += 8) {
-        float v[8][kPer], wt[8];
+      for (int sb = 0; sb < ns; sb += kGrp) {
+        float wt[kGrp];
+        if (sb > 0) {  // later groups: their rows (the first group's are already in flight)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {  // issue the group's loads first
-          const int s = sb + u;
-          wt[u] = 0.f;
-          if (s < s1) {
-            const int64_t prow = (int64_t)pv.list_slot[s] * p.T_slot + r;
-            wt[u] = __expf(p.part_lse[prow] - m);  // 0 for an empty partial
-            const float* src = p.part_o + prow * D + lane * kPer;
+          for (int u = 0; u < kGrp; ++u) {
+            if (sb + u < ns) {
+              const int sl = pv.list_slot[s0 + sb + u];
+              const float* src = p.part_o + ((int64_t)sl * p.T_slot + r) * D + lane * kPer;
 #pragma unroll
-            for (int j = 0; j < kPer; ++j) v[u][j] = src[j];
+              for (int j = 0; j < kPer; ++j) v[u][j] = src[j];
+            }
           }
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {  // then accumulate in slot order
-          if (sb + u < s1) {
+        for (int u = 0; u < kGrp; ++u) {
+          const int e = sb + u;
+          float l = __shfl_sync(0xffffffffu, lse_l, e & 31);
+          if (e >= 32 && e < ns) l = p.part_lse[(int64_t)pv.list_slot[s0 + e] * p.T_slot + r];
+          wt[u] = e < ns ? __expf(l - m) : 0.f;  // 0 for an empty partial
+        }
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {  // the fold in slot order
+          if (sb + u < ns) {
             tot += wt[u];
 #pragma unroll
             for (int j = 0; j < kPer; ++j) acc[j] = fmaf(wt[u], v[u][j], acc[j]);

@@ -149,8 +149,11 @@ __device__ __forceinline__ void rope_chunk(uint8_t* lo, uint8_t* hi, int64_t pos
 // Pipeline trace points (BSRA_EXPERIMENTS builds only; scripts/trace_decode.py)
 #ifdef BSRA_EXPERIMENTS
 #define DEC_TRACE(e) do { if (p.trace) p.trace[(e) * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns(); } while (0)
+// per-tile clock64 events of CTA 0 (index k < 1024): rows 20.. of the trace buffer
+#define DEC_TTRACE(e, k) do { if (p.trace && blockIdx.x == 0 && (k) < 1024) p.trace[(20 + (e)) * 1024 + (k)] = clock64(); } while (0)
 #else
 #define DEC_TRACE(e) do { } while (0)
+#define DEC_TTRACE(e, k) do { } while (0)
 #endif
 
 // kF16: fp16 q / o (else bf16) at compile time: one code path per instantiation (instruction
@@ -258,6 +261,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     }
     const int B = tp.box_tok;
     int stage = 0;
+    int tcount = 0;  // trace index
     uint32_t ephase = 1;  // fresh barriers: waiting on parity 1 passes
     uint32_t qphase[2] = {1, 1};
     int qb = 0;
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           }
           if (lane == 0) {
             ptx::mbar_wait(&empty[stage], ephase);
+            DEC_TTRACE(0, tcount);
             ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * (kD * 4));
           }
           __syncwarp();
@@ -371,6 +376,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           }
           __syncwarp();
         }
+        ++tcount;
         if (++stage == kStages) {
           stage = 0;
           ephase ^= 1;
@@ -388,6 +394,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     const uint32_t idO = ptx::idesc_f16(fmt, 128, kN, 1, 0);  // A = V^T (MN-major), B = P^T (K-major)
     const uint32_t sbase = ptx::smem_u32(smem);
     int stage = 0, sb = 0, pb = 0, qb = 0, ob = 0;
+    int tcount = 0;
     uint32_t fphase = 0;
     uint32_t ofph[2] = {1, 1};
     uint32_t sfph[2] = {1, 1}, pfph[2] = {0, 0}, qphase[2] = {0, 0};
@@ -430,8 +437,11 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
       for (int ti = 0; ti < d.ntiles; ++ti) {
         ptx::mbar_wait(kRope ? &krot[stage] : &full[stage], fphase);
         if (lane == 0 && it == it0 && ti == 0) DEC_TRACE(10);
+        if (lane == 0) DEC_TTRACE(1, tcount);
         ptx::mbar_wait(&s_free[sb], sfph[sb]);
         sfph[sb] ^= 1;
+        if (lane == 0) DEC_TTRACE(2, tcount);
+        ++tcount;
         if (kRow && tp.cp == 1) ptx::fence_proxy_async();  // cp.async (generic-proxy) writes -> tensor core
         ptx::tc_fence_after();
         const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes, 16, 1024);
@@ -499,6 +509,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ptx::mbar_wait(&bar_s[sbuf], sph[sbuf]);
         sph[sbuf] ^= 1;
         if (ct == 0 && it == it0 && ti == 0) DEC_TRACE(1);
+        if (ct == 0) DEC_TTRACE(3, tpar);
         ptx::tc_fence_after();
         float s[kC];
         ptx::tmem_ld<kC>(tmem + lane_addr + sbuf * 16, s);
@@ -618,6 +629,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
 #pragma unroll
         for (int c = 0; c < kC; ++c) lp[c] += pr[c];
         if (ct == 0) ptx::mbar_arrive(&p_full[pbuf]);  // the MMA warp issues PV(t)
+        if (ct == 0) DEC_TTRACE(4, tpar);
         ++tpar;
         pv_pending[pbuf] = true;
         pbuf ^= 1;
@@ -750,6 +762,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ptx::mbar_wait(&epi_full[ob], efph[ob]);
         ptx::mbar_wait(&o_full[ob], efph[ob]);  // the item's last PV completed
         efph[ob] ^= 1;
+        if (et == 0) DEC_TTRACE(5, it - it0);
         ptx::tc_fence_after();
         ptx::tmem_ld<kC>(tmem + lane_addr + 32 + ob * 16, ov);
         ptx::tmem_ld_wait();
@@ -796,6 +809,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         }
       }
       if (et == 0 && it + 1 == it1) DEC_TRACE(4);
+      if (et == 0) DEC_TTRACE(6, it - it0);
       if (d.slot >= 0 && p.fused_merge) {  // split item: the CTA completing its merge list folds it
         volatile int* s_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
         const ListMeta* pre = it - it0 < kStagedItems ? smeta + (it - it0) : nullptr;

@@ -72,8 +72,15 @@ def main():
         def suf():
             for ci in cis:
                 comp.suffix.run(ci.q, ci.k_pool, ci.v_pool, ci.strides, ci.strides, si, comp.o_s, comp.l_s, stream=s)
+        def con():
+            for (o, l) in outs:
+                if comp.fold_suffix:
+                    comp.prefix.contract(o, l, o_extra=comp.o_s, lse_extra=comp.l_s, stream=s)
+                else:
+                    comp.prefix.contract(comp.o_p, comp.l_p, stream=s)
         r = {"us_per_layer": ms * 1e3, "TB/s": unique / (ms * 1e-3) / 1e12,
              "prefix_us": graph_ms(pre, s) / layers * 1e3, "suffix_us": graph_ms(suf, s) / layers * 1e3,
+             "contract_us": graph_ms(con, s) / layers * 1e3,
              "prefix_T_q": int(comp.prefix.export_plan()[3]), "prefix_items": int(comp.prefix.export_plan()[5]),
              "prefix_slots": int(comp.prefix.export_plan()[7])}
         res[name] = r
