@@ -49,6 +49,8 @@ struct TcParams {
   int32_t pdl;      // launched with programmatic dependent launch (host-side launch choice)
   int32_t cp;       // decode K/V gather: 0 = TMA boxes per page, 1 = 16-byte cp.async rows, 2 = TMA gather4 rows
   int64_t row_s0, row_s1, row_s2;  // gather4: (page, slot, head) strides in rows of the 2-D [rows, D] view
+  int32_t grp;      // 1: page boxes of the 5-D pool view (both 64-column halves per box), group-major tiles
+  int32_t cs;       // grp: pool page stride / head stride (the 5-D view's (page, head) coordinate = page * cs + head)
   int32_t dbg;      // BSRA_EXPERIMENTS builds only ($BSRA_DEBUG_PREFILL timing modes); 0 otherwise
 };
 
@@ -164,9 +166,18 @@ __device__ __forceinline__ void rope_chunk(uint8_t* lo, uint8_t* hi, int64_t pos
 // instantiation, so the box kernel carries none of that code.
 // kD: head_dim 128 (two 64-column SW128 halves per row) or 64 (one half: the S MMA takes K = 64,
 // the PV MMA keeps M = 128 with O^T rows 64..127 unused and never stored).
-template <int kC, int kMask, bool kF16, bool kRope, bool kRow = false, int kD = 128>
+// kGrp: K/V tiles group-major — [16 groups of 8 tokens][64-column half][8 rows][128 B] — so ONE TMA
+// box of the 5-D pool view (d_lo, token_lo, half, token_hi, page*cs + head) brings a whole page
+// (both halves, 4 KB at B_c = 16) where the half-major layout [half][128 rows][128 B] needs one box
+// per half: the decode producer is TMA-issue-bound at ~80-90 cycles per small box
+// (scripts/tma_issue_bench.cu), so half the boxes per tile. Paged pools only (the 8-token groups
+// need page-aligned tiles); the MMA descriptors take SBO = 2048 and the half offset 1024.
+template <int kC, int kMask, bool kF16, bool kRope, bool kRow = false, int kD = 128, bool kGrp = false>
 __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
   static_assert(kD == 128 || (kD == 64 && !kRope && !kRow), "head_dim 64: box gather, no RoPE");
+  static_assert(!kGrp || (kD == 128 && !kRope && !kRow), "group-major tiles: plain box gather, head_dim 128");
+  constexpr int kRowG = kGrp ? 2048 : 1024;                // bytes between 8-row groups of a K/V tile (SBO)
+  constexpr int kHalfOff = kGrp ? 1024 : dec::kHalfBytes;  // bytes between the two 64-column halves
   using namespace dec;
   const AttnParams& p = tp.p;
   extern __shared__ uint8_t smem_raw[];
@@ -366,7 +377,13 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           }
           __syncwarp();
           if (lane == 0 && it == it0 && ti == 0) DEC_TRACE(8);
-          if (lane < nsub) {
+          if (kGrp && lane < nsub) {  // one box per page: 8-token groups [lane*B/8, (lane+1)*B/8) of the tile
+            uint8_t* kd = smem + stage * kStageBytes + (lane * B >> 3) * 2048;
+            uint8_t* vd = kd + kKVBytes;
+            const int c4 = page * tp.cs + d.kvh;
+            ptx::tma_load_5d(kd, &tp.tk, &full[stage], 0, 0, 0, off >> 3, c4);
+            ptx::tma_load_5d(vd, &tp.tv, &full[stage], 0, 0, 0, off >> 3, c4);
+          } else if (lane < nsub) {
             uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
             uint8_t* vd = kd + kKVBytes;
             ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
@@ -410,12 +427,12 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ofph[x.ob] ^= 1;
       }
       ptx::tc_fence_after();
-      const uint64_t a0 = ptx::smem_desc_sw128(sbase + x.st * kStageBytes + kKVBytes, kHalfBytes, 1024);
+      const uint64_t a0 = ptx::smem_desc_sw128(sbase + x.st * kStageBytes + kKVBytes, kHalfOff, kRowG);
       const uint64_t b0 = ptx::smem_desc_sw128(sbase + kOffP + pb * kPBytes, 16, 1024);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t sbo = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
-        ptx::mma_f16_ss_warp(tmem + 32 + x.ob * 16, a0 + (uint64_t)(kk * 128), b0 + sbo, idO,
+        ptx::mma_f16_ss_warp(tmem + 32 + x.ob * 16, a0 + (uint64_t)(kk * (2 * kRowG >> 4)), b0 + sbo, idO,
                              (x.ti > 0 || kk > 0) ? 1u : 0u);
       }
       ptx::mma_commit_warp(&empty[x.st]);  // K/V stage free once these MMAs complete
@@ -444,10 +461,10 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         ++tcount;
         if (kRow && tp.cp == 1) ptx::fence_proxy_async();  // cp.async (generic-proxy) writes -> tensor core
         ptx::tc_fence_after();
-        const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes, 16, 1024);
+        const uint64_t a0 = ptx::smem_desc_sw128(sbase + stage * kStageBytes, 16, kRowG);
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
-          const uint64_t sa = (uint64_t)((kk >> 2) * (kHalfBytes >> 4) + (kk & 3) * 2);
+          const uint64_t sa = (uint64_t)((kk >> 2) * (kHalfOff >> 4) + (kk & 3) * 2);
           const uint64_t sbo = (uint64_t)((kk >> 2) * (kN * 128 >> 4) + (kk & 3) * 2);
           ptx::mma_f16_ss_warp(tmem + sb * 16, a0 + sa, bq + sbo, idS, kk > 0);
         }
@@ -523,8 +540,9 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           ptx::mbar_wait(&full[stage], fphase);  // (already complete) orders the TMA writes before ours
           uint8_t* vS = smem + stage * kStageBytes + kKVBytes;
           uint4 z = make_uint4(0, 0, 0, 0);
-          uint4* v0 = reinterpret_cast<uint4*>(vS + row * 128);
-          uint4* v1 = reinterpret_cast<uint4*>(vS + kHalfBytes + row * 128);
+          const int roff = kGrp ? (row >> 3) * 2048 + (row & 7) * 128 : row * 128;
+          uint4* v0 = reinterpret_cast<uint4*>(vS + roff);
+          uint4* v1 = reinterpret_cast<uint4*>(vS + kHalfOff + roff);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             v0[j] = z;

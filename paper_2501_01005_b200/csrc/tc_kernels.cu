@@ -63,6 +63,27 @@ bool make_pool_map(CUtensorMap* m, const void* pool, bool f16, int H_kv, int64_t
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// paged pool as the 5-D view of the group-major decode tiles (tc_decode kGrp): dims (d_lo 64,
+// token_lo 8, half 2, token_hi page_size/8, c = page * cs + head), strides (-, s1, 64, 8 s1, s2)
+// elements with cs = s0 / s2 (so c * s2 = page * s0 + head * s2); box (64, 8, 2, B/8, 1) lands as
+// [B/8 groups][half][8 rows][128 B] — a whole page (both halves) per box. Needs s0 % s2 == 0 and
+// page_size % 8 == 0; the caller falls back to the 4-D map otherwise.
+bool make_pool_map5(CUtensorMap* m, const void* pool, bool f16, int64_t page_size, int64_t s0, int64_t s1, int64_t s2,
+                    int B, int* cs_out) {
+  auto enc = get_encode();
+  if (!enc || s2 <= 0 || s0 % s2 || page_size % 8 || B % 8) return false;
+  const int64_t cs = s0 / s2;
+  if (cs <= 0 || cs > (1 << 20)) return false;
+  cuuint64_t dims[5] = {64, 8, 2, (cuuint64_t)(page_size / 8), 0x7fffffffull};  // 2^32 - 1 encodes but traps at run time
+  cuuint64_t strides[4] = {(cuuint64_t)s1 * 2, 128, (cuuint64_t)s1 * 16, (cuuint64_t)s2 * 2};
+  cuuint32_t box[5] = {64, 8, 2, (cuuint32_t)(B / 8), 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  *cs_out = (int)cs;
+  return enc(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(pool),
+             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // pool as a 2-D tensor [rows, 128] (a row = one (page, slot, head) of D = 128 contiguous elements)
 // for TMA gather4: box {64 columns, 1 row}, 128B swizzle; 4 rows per instruction
 bool make_row_map(CUtensorMap* m, const void* pool, bool f16) {
@@ -77,7 +98,7 @@ bool make_row_map(CUtensorMap* m, const void* pool, bool f16) {
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int kC, int kMask, bool kF8, bool kRope = false, bool kRow = false, int kD = 128>
+template <int kC, int kMask, bool kF8, bool kRope = false, bool kRow = false, int kD = 128, bool kGrp = false>
 cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
   static bool attr = false;
   if constexpr (kF8) {  // fp8 KV cache: K in TMEM, converter warps (tc_decode_f8.cuh)
@@ -94,17 +115,17 @@ cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
     return launch_tc(tc_decode_f8_kernel<kC, kMask, false>, grid, f8d::threads_for(kC), f8d::kSmemBytes, st, tp);
   } else {
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false, kRope, kRow, kD>,
+    cudaError_t e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, false, kRope, kRow, kD, kGrp>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true, kRope, kRow, kD>,
+    e = cudaFuncSetAttribute(tc_decode_kernel<kC, kMask, true, kRope, kRow, kD, kGrp>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, dec::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   const int nt = dec::threads_for(kRope);
-  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true, kRope, kRow, kD>, grid, nt, dec::kSmemBytes, st, tp);
-  return launch_tc(tc_decode_kernel<kC, kMask, false, kRope, kRow, kD>, grid, nt, dec::kSmemBytes, st, tp);
+  if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true, kRope, kRow, kD, kGrp>, grid, nt, dec::kSmemBytes, st, tp);
+  return launch_tc(tc_decode_kernel<kC, kMask, false, kRope, kRow, kD, kGrp>, grid, nt, dec::kSmemBytes, st, tp);
   }
 }
 
@@ -130,6 +151,13 @@ cudaError_t launch_decode_m(int mask, const TcParams& tp, int grid, cudaStream_t
         case 0: return launch_decode_t<kC, 0, false, true>(tp, grid, st);
         case 1: return launch_decode_t<kC, 1, false, true>(tp, grid, st);
         default: return launch_decode_t<kC, 2, false, true>(tp, grid, st);
+      }
+    }
+    if (tp.grp) {  // group-major tiles: one 5-D box per page (paged pools)
+      switch (mask) {
+        case 0: return launch_decode_t<kC, 0, false, false, false, 128, true>(tp, grid, st);
+        case 1: return launch_decode_t<kC, 1, false, false, false, 128, true>(tp, grid, st);
+        default: return launch_decode_t<kC, 2, false, false, false, 128, true>(tp, grid, st);
       }
     }
   }
@@ -201,7 +229,21 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     tp.pdl = L.pdl;
     tp.cp = cp_gather ? (rows_ok && !L.force_cp_async ? 2 : 1) : 0;
     bool maps_ok = make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb, p.D);
-    if (tp.cp == 0) maps_ok = maps_ok && make_kv_maps(tp, p, L, B);
+    // group-major tiles (one box per page) where the pool strides allow the 5-D view
+    int cs_k = 0, cs_v = 0;
+#ifdef BSRA_NO_GRP  // A/B builds (scripts/build_variant.sh): the half-major 4-D page boxes everywhere
+    const bool try_grp = false;
+#else
+    const bool try_grp = true;
+#endif
+    if (try_grp && tp.cp == 0 && !L.ragged && !L.f8kv && !L.rope && p.D == 128 &&
+        make_pool_map5(&tp.tk, p.k, L.f16, ps, p.ks0, p.ks1, p.ks2, B, &cs_k) &&
+        make_pool_map5(&tp.tv, p.v, L.f16, ps, p.vs0, p.vs1, p.vs2, B, &cs_v) && cs_k == cs_v) {
+      tp.grp = 1;
+      tp.cs = cs_k;
+    } else if (tp.cp == 0) {
+      maps_ok = maps_ok && make_kv_maps(tp, p, L, B);
+    }
     if (tp.cp == 2) {
       tp.row_s0 = p.ks0 / 128;
       tp.row_s1 = p.ks1 / 128;
