@@ -629,14 +629,24 @@ def bench_prefill(dev, pk, args, world, rank):
     full = synth.c3_prefill_llama70b()
     wl, _ = head_sharded_wl(full, world, rank) if world > 1 else (full, (0, full.H_kv))
     L3 = Layered(wl, 2, dev, seed_base=1000 * rank)
-    e3 = L3.engine(num_ctas=args.num_ctas, kernel=args.kernel, tile_q=args.prefill_tile)
-    mine = per_launch_ms(L3, e3, reps=3)
+    e3 = L3.engine(num_ctas=args.num_ctas, kernel=args.kernel, tile_q=args.prefill_tile, pdl=True)
+    iso_ms = max(gather_over_ranks(per_launch_ms(L3, e3, reps=3), world))
+    # as the decode headline: layers back to back in a CUDA graph with PDL (a layer's prologue and
+    # K/V streaming overlap the previous layer's tail); 4 runs (2 layers x 2) per replay
+    s = torch.cuda.Stream()
+
+    def four():
+        for r in (0, 1, 0, 1):
+            L3.run_layer(e3, r, s)
+    mine = time_graph(four, s, 5) / 4
     per_rank = gather_over_ranks(mine, world)
     p_ms = max(per_rank)
     fl = causal_flops(full)
     tf = fl / (p_ms * 1e-3) / 1e12
     out = {"value": tf, "unit": "TFLOP/s", "workload": "c3_prefill_llama70b (configs[2])", "n_gpus": world,
            "scaling": "strong" if world > 1 else None, "ms_per_layer": p_ms, "per_rank_ms": per_rank,
+           "how": "ms per layer in a CUDA graph of 4 PDL runs over 2 layers (attention + contraction launches)",
+           "ms_per_layer_isolated": iso_ms, "value_isolated": fl / (iso_ms * 1e-3) / 1e12,
            "frac": tf / world / pk["bf16_tflops"], "peak": pk["bf16_tflops"], "peak_kind": "burst (measured)",
            "frac_of_sustained": tf / world / pk.get("bf16_tflops_sustained", pk["bf16_tflops"]),
            "kernel": e3.selected_kernel(), "tile_q": int(e3.export_plan()[3]), "flops_per_layer": fl}

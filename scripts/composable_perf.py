@@ -55,7 +55,7 @@ def main():
     variants.append(("base_pdl", dict(prefix_tiles=(64, 128), balance=False, prefix_ctas=148, suffix_ctas=148,
                                       pdl=True)))
     variants.append(("pair_pdl", dict(prefix_ctas=148, suffix_ctas=148, pdl=True)))
-    for pc, sc in ((64, 84), (84, 64), (20, 128), (44, 104), (64, 64)):
+    for pc, sc in ((56, 92), (64, 84), (72, 76), (80, 68), (88, 60)):
         variants.append((f"conc_{pc}_{sc}", dict(prefix_ctas=pc, suffix_ctas=sc, concurrent=True)))
     for name, kw in variants:
         comp = bsra.ComposableDecode(H_qo=32, H_kv=8, D=128, page_size=16, n_branch=n, **kw)
