@@ -186,6 +186,23 @@ cudaError_t launch_decode(bool f8, int kc, int mask, const TcParams& tp, int gri
 bool make_q_map_ext(CUtensorMap* m, const void* q, bool f16, int H_qo, int64_t N, int hb, int tb) {
   return make_q_map(m, q, f16, H_qo, N, hb, tb);
 }
+// Group-major K/V tiles (one 5-D box per page, tp.grp = 1) where the pool strides allow it:
+// paged 16-bit pools with head_dim 128 (not for contiguous KV, fp8 or RoPE launches; A/B builds
+// with -DBSRA_NO_GRP keep the half-major 4-D boxes). Returns false (tp untouched) otherwise.
+bool make_kv_maps5(TcParams& tp, const AttnParams& p, const TcLaunch& L, int B) {
+#ifdef BSRA_NO_GRP
+  return false;
+#endif
+  if (L.ragged || L.f8kv || L.rope || p.D != 128) return false;
+  int cs_k = 0, cs_v = 0;
+  if (!make_pool_map5(&tp.tk, p.k, L.f16, L.page_size, p.ks0, p.ks1, p.ks2, B, &cs_k) ||
+      !make_pool_map5(&tp.tv, p.v, L.f16, L.page_size, p.vs0, p.vs1, p.vs2, B, &cs_v) || cs_k != cs_v)
+    return false;
+  tp.grp = 1;
+  tp.cs = cs_k;
+  return true;
+}
+
 // K and V maps for a launch: paged pools, or contiguous KV (token extent L.total_kv, one page)
 bool make_kv_maps(TcParams& tp, const AttnParams& p, const TcLaunch& L, int B) {
   if (L.ragged)
@@ -230,20 +247,7 @@ int tc_launch(const AttnParams& p, const TcLaunch& L, cudaStream_t st, const cha
     tp.cp = cp_gather ? (rows_ok && !L.force_cp_async ? 2 : 1) : 0;
     bool maps_ok = make_q_map(&tp.tq, p.q, L.f16, p.H_qo, L.total_qo, tp.q_hb, tp.q_tb, p.D);
     // group-major tiles (one box per page) where the pool strides allow the 5-D view
-    int cs_k = 0, cs_v = 0;
-#ifdef BSRA_NO_GRP  // A/B builds (scripts/build_variant.sh): the half-major 4-D page boxes everywhere
-    const bool try_grp = false;
-#else
-    const bool try_grp = true;
-#endif
-    if (try_grp && tp.cp == 0 && !L.ragged && !L.f8kv && !L.rope && p.D == 128 &&
-        make_pool_map5(&tp.tk, p.k, L.f16, ps, p.ks0, p.ks1, p.ks2, B, &cs_k) &&
-        make_pool_map5(&tp.tv, p.v, L.f16, ps, p.vs0, p.vs1, p.vs2, B, &cs_v) && cs_k == cs_v) {
-      tp.grp = 1;
-      tp.cs = cs_k;
-    } else if (tp.cp == 0) {
-      maps_ok = maps_ok && make_kv_maps(tp, p, L, B);
-    }
+    if (tp.cp == 0 && !make_kv_maps5(tp, p, L, B)) maps_ok = maps_ok && make_kv_maps(tp, p, L, B);
     if (tp.cp == 2) {
       tp.row_s0 = p.ks0 / 128;
       tp.row_s1 = p.ks1 / 128;
