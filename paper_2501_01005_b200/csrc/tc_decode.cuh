@@ -95,7 +95,12 @@ constexpr int kOffMeta = kOffItems + kStagedItems * 80;  // merge-list metadata 
 constexpr int kSmemBytes = kOffMeta + kStagedItems * 32 + 1024;  // + alignment slack
 constexpr int kThreads = 320;  // producer, 4 softmax warps, MMA warp, 4 epilogue warps
 constexpr int kThreadsRope = 576;  // + 8 RoPE warps (two per SM sub-partition) in the fused-RoPE variant
-constexpr int threads_for(bool rope) { return rope ? kThreadsRope : kThreads; }
+// Plain variant: + 3 producer warps (10..12). TMA issue is per-warp serialised (~65-160 cycles per
+// instruction whatever the box size, and it scales with the number of issuing warps:
+// scripts/tma_issue_bench.cu), so K and V boxes (and the four gather4 quarters) come from
+// different warps.
+constexpr int kThreadsPlain = kThreads + 96;
+constexpr int threads_for(bool rope) { return rope ? kThreadsRope : kThreadsPlain; }
 constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T double buffer at 32 / 48
 constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
 }  // namespace dec
@@ -222,10 +227,15 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
   for (int k = threadIdx.x; k < min(kStagedItems, it1 - it0); k += blockDim.x) staged[k] = dec_item(pv, it0 + k, g);
   auto item_at = [&](int it) { return it - it0 < kStagedItems ? staged[it - it0] : dec_item(pv, it, g); };
 
+  // producer warps: warp 0 (Q and K), 10 (V), 11 / 12 (gather4: the V halves; 0 / 10 the K halves)
+#ifndef BSRA_BOX_PRODUCERS
+#define BSRA_BOX_PRODUCERS 2
+#endif
+  const int nprod = kRope || (kRow && tp.cp == 1) ? 1 : (kRow && tp.cp == 2 ? 4 : BSRA_BOX_PRODUCERS);
   if (threadIdx.x == 0) {
     DEC_TRACE(0);
     for (int s = 0; s < kStages; ++s) {
-      ptx::mbar_init(&full[s], kRow && tp.cp == 1 ? 32 : 1);  // cp.async gather: one arrival per lane
+      ptx::mbar_init(&full[s], kRow && tp.cp == 1 ? 32 : nprod);  // cp.async gather: one arrival per lane
       ptx::mbar_init(&empty[s], 1);
       ptx::mbar_init(&krot[s], 1);
     }
@@ -263,10 +273,14 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
   if (p.trace && threadIdx.x == 0) p.trace[16 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
 #endif
 
-  if (warp == 0) {
-    // ============================ TMA producer ============================
+  const int prole = warp == 0 ? 0 : (!kRope && warp >= 10 ? warp - 9 : -1);  // producer role
+  if (prole >= 0) {
+    // ============================ TMA producers ============================
+    // role 0: Q + K (box path) / K half 0 (gather4) / everything (cp.async, RoPE variant); role 1:
+    // V / K half 1; roles 2, 3: V halves 0 / 1 (gather4). Every role walks the same tile sequence.
+    if (prole < nprod) {
     if (lane == 0) {
-      ptx::tma_prefetch_desc(&tp.tq);
+      if (prole == 0) ptx::tma_prefetch_desc(&tp.tq);
       ptx::tma_prefetch_desc(&tp.tk);
       ptx::tma_prefetch_desc(&tp.tv);
     }
@@ -280,7 +294,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     for (int it = it0; it < it1; ++it) {
       const DecItem d = item_at(it);
       // ---- Q tile: 16 fused rows = q_tb tokens x q_hb heads, two 64-column halves
-      if (lane == 0) {
+      if (lane == 0 && prole == 0) {
         ptx::mbar_wait(&empty_q[qb], qphase[qb]);
         ptx::mbar_arrive_expect_tx(&full_q[qb], kD == 128 ? kQBytes : kQBytes / 2);
         const int head0 = d.kvh * g + (g > kN ? d.row0 % g : 0);
@@ -308,15 +322,13 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           }
           if (lane == 0) {
             ptx::mbar_wait(&empty[stage], ephase);
-            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)kStageBytes);
+            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)kStageBytes / 4);
           }
           __syncwarp();
-          uint8_t* kd = smem + stage * kStageBytes + lane * 4 * 128;
-          uint8_t* vd = kd + kKVBytes;
-          ptx::tma_gather4(kd, &tp.tk, &full[stage], 0, rows[0], rows[1], rows[2], rows[3]);
-          ptx::tma_gather4(kd + kHalfBytes, &tp.tk, &full[stage], 64, rows[0], rows[1], rows[2], rows[3]);
-          ptx::tma_gather4(vd, &tp.tv, &full[stage], 0, rows[0], rows[1], rows[2], rows[3]);
-          ptx::tma_gather4(vd + kHalfBytes, &tp.tv, &full[stage], 64, rows[0], rows[1], rows[2], rows[3]);
+          // role r: K or V = r >> 1, column half = r & 1
+          uint8_t* dst = smem + stage * kStageBytes + lane * 4 * 128 + (prole >> 1) * kKVBytes + (prole & 1) * kHalfBytes;
+          ptx::tma_gather4(dst, (prole >> 1) ? &tp.tv : &tp.tk, &full[stage], (prole & 1) * 64, rows[0], rows[1],
+                           rows[2], rows[3]);
           __syncwarp();
         } else if (kRow) {
           // 16-byte cp.async gather, any page size (small pages, B_c not dividing 128): per
@@ -370,26 +382,32 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
               off = (int)(tok % p.page_size);
             }
           }
+          // role 0 loads K, role 1 V (a single role in the RoPE variant: both)
           if (lane == 0) {
             ptx::mbar_wait(&empty[stage], ephase);
-            DEC_TTRACE(0, tcount);
-            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * (kD * 4));
+            if (prole == 0) DEC_TTRACE(0, tcount);
+            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * (kD * 4) / nprod);
           }
           __syncwarp();
-          if (lane == 0 && it == it0 && ti == 0) DEC_TRACE(8);
+          if (lane == 0 && it == it0 && ti == 0 && prole == 0) DEC_TRACE(8);
+          const bool doK = prole == 0, doV = prole == 1 || nprod == 1;
           if (kGrp && lane < nsub) {  // one box per page: 8-token groups [lane*B/8, (lane+1)*B/8) of the tile
             uint8_t* kd = smem + stage * kStageBytes + (lane * B >> 3) * 2048;
             uint8_t* vd = kd + kKVBytes;
             const int c4 = page * tp.cs + d.kvh;
-            ptx::tma_load_5d(kd, &tp.tk, &full[stage], 0, 0, 0, off >> 3, c4);
-            ptx::tma_load_5d(vd, &tp.tv, &full[stage], 0, 0, 0, off >> 3, c4);
+            if (doK) ptx::tma_load_5d(kd, &tp.tk, &full[stage], 0, 0, 0, off >> 3, c4);
+            if (doV) ptx::tma_load_5d(vd, &tp.tv, &full[stage], 0, 0, 0, off >> 3, c4);
           } else if (lane < nsub) {
             uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
             uint8_t* vd = kd + kKVBytes;
-            ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
-            if (kD == 128) ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
-            ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
-            if (kD == 128) ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
+            if (doK) {
+              ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
+              if (kD == 128) ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
+            }
+            if (doV) {
+              ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
+              if (kD == 128) ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
+            }
           }
           __syncwarp();
         }
@@ -400,6 +418,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
         }
       }
     }
+    }  // prole < nprod
   } else if (warp == 5) {
     // ================================ MMA issuer ================================
     // One flat stream of tiles across the CTA's items: S(k) as soon as K(k) landed and the softmax
