@@ -279,18 +279,6 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     // role 0: Q + K (box path) / K half 0 (gather4) / everything (cp.async, RoPE variant); role 1:
     // V / K half 1; roles 2, 3: V halves 0 / 1 (gather4). Every role walks the same tile sequence.
     if (prole < nprod) {
-    // gather4 path: this lane's 4 token rows of tile ti of item d (rows past the chunk repeat its last)
-    auto g4_rows = [&](const DecItem& d, int ti, int* rows) {
-      const int64_t t0 = d.kb + (int64_t)ti * kTile;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t t = imin64(t0 + 4 * lane + j, d.ke - 1);
-        const int64_t pg = __ldg(p.page_indices + d.page_begin + t / p.page_size);
-        rows[j] = (int)(pg * tp.row_s0 + (t % p.page_size) * tp.row_s1 + d.kvh * tp.row_s2);
-      }
-    };
-    int g4_pre[4] = {0, 0, 0, 0};
-    bool g4_have = false;
     if (lane == 0) {
       if (prole == 0) ptx::tma_prefetch_desc(&tp.tq);
       ptx::tma_prefetch_desc(&tp.tk);
@@ -325,24 +313,12 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
           // is D contiguous elements); lane l loads token rows 4l .. 4l+3 of the tile, both
           // 64-column halves of K and V: 4 instructions per lane, 128 per 64 KB tile, any page
           // size. Rows past the chunk repeat its last row (masked in S, zeroed in V).
-          // The tile's page ids were loaded one tile ahead (g4_pre, below): the gather4 issue does
-          // not wait for the page table.
           int rows[4];
-          if (g4_have) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) rows[j] = g4_pre[j];
-          } else {
-            g4_rows(d, ti, rows);
-          }
-          {  // the next tile's ids: this item's next tile, or the first tile of the next item with tiles
-            int itn = it, tin = ti + 1;
-            DecItem dn = d;
-            while (tin >= dn.ntiles && ++itn < it1) {
-              dn = item_at(itn);
-              tin = 0;
-            }
-            g4_have = itn < it1;
-            if (g4_have) g4_rows(dn, tin, g4_pre);
+          for (int j = 0; j < 4; ++j) {
+            const int64_t t = imin64(t0 + 4 * lane + j, d.ke - 1);
+            const int64_t pg = __ldg(p.page_indices + d.page_begin + t / p.page_size);
+            rows[j] = (int)(pg * tp.row_s0 + (t % p.page_size) * tp.row_s1 + d.kvh * tp.row_s2);
           }
           if (lane == 0) {
             ptx::mbar_wait(&empty[stage], ephase);
