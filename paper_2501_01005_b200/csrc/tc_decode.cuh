@@ -279,145 +279,145 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
     // role 0: Q + K (box path) / K half 0 (gather4) / everything (cp.async, RoPE variant); role 1:
     // V / K half 1; roles 2, 3: V halves 0 / 1 (gather4). Every role walks the same tile sequence.
     if (prole < nprod) {
-    if (lane == 0) {
-      if (prole == 0) ptx::tma_prefetch_desc(&tp.tq);
-      ptx::tma_prefetch_desc(&tp.tk);
-      ptx::tma_prefetch_desc(&tp.tv);
-    }
-    const int B = tp.box_tok;
-    int stage = 0;
-    int tcount = 0;  // trace index
-    uint32_t ephase = 1;  // fresh barriers: waiting on parity 1 passes
-    uint32_t qphase[2] = {1, 1};
-    int qb = 0;
-    if (lane == 0) DEC_TRACE(11);
-    for (int it = it0; it < it1; ++it) {
-      const DecItem d = item_at(it);
-      // ---- Q tile: 16 fused rows = q_tb tokens x q_hb heads, two 64-column halves
-      if (lane == 0 && prole == 0) {
-        ptx::mbar_wait(&empty_q[qb], qphase[qb]);
-        ptx::mbar_arrive_expect_tx(&full_q[qb], kD == 128 ? kQBytes : kQBytes / 2);
-        const int head0 = d.kvh * g + (g > kN ? d.row0 % g : 0);
-        const int tok0 = (int)d.qo_begin + d.row0 / g;
-        uint8_t* qdst = smem + kOffQ + qb * kQBytes;
-        ptx::tma_load_3d(qdst, &tp.tq, &full_q[qb], 0, head0, tok0);
-        if (kD == 128) ptx::tma_load_3d(qdst + kN * 128, &tp.tq, &full_q[qb], 64, head0, tok0);
+      if (lane == 0) {
+        if (prole == 0) ptx::tma_prefetch_desc(&tp.tq);
+        ptx::tma_prefetch_desc(&tp.tk);
+        ptx::tma_prefetch_desc(&tp.tv);
       }
-      qphase[qb] ^= 1;
-      qb ^= 1;
-      // ---- K/V tiles
-      for (int ti = 0; ti < d.ntiles; ++ti) {
-        const int64_t t0 = d.kb + (int64_t)ti * kTile;
-        if (kRow && tp.cp == 2) {
-          // TMA gather4 (sm_100): the K/V pools as 2-D [rows, D] tensors (a (page, slot, head) row
-          // is D contiguous elements); lane l loads token rows 4l .. 4l+3 of the tile, both
-          // 64-column halves of K and V: 4 instructions per lane, 128 per 64 KB tile, any page
-          // size. Rows past the chunk repeat its last row (masked in S, zeroed in V).
-          int rows[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int64_t t = imin64(t0 + 4 * lane + j, d.ke - 1);
-            const int64_t pg = __ldg(p.page_indices + d.page_begin + t / p.page_size);
-            rows[j] = (int)(pg * tp.row_s0 + (t % p.page_size) * tp.row_s1 + d.kvh * tp.row_s2);
-          }
-          if (lane == 0) {
+      const int B = tp.box_tok;
+      int stage = 0;
+      int tcount = 0;  // trace index
+      uint32_t ephase = 1;  // fresh barriers: waiting on parity 1 passes
+      uint32_t qphase[2] = {1, 1};
+      int qb = 0;
+      if (lane == 0) DEC_TRACE(11);
+      for (int it = it0; it < it1; ++it) {
+        const DecItem d = item_at(it);
+        // ---- Q tile: 16 fused rows = q_tb tokens x q_hb heads, two 64-column halves
+        if (lane == 0 && prole == 0) {
+          ptx::mbar_wait(&empty_q[qb], qphase[qb]);
+          ptx::mbar_arrive_expect_tx(&full_q[qb], kD == 128 ? kQBytes : kQBytes / 2);
+          const int head0 = d.kvh * g + (g > kN ? d.row0 % g : 0);
+          const int tok0 = (int)d.qo_begin + d.row0 / g;
+          uint8_t* qdst = smem + kOffQ + qb * kQBytes;
+          ptx::tma_load_3d(qdst, &tp.tq, &full_q[qb], 0, head0, tok0);
+          if (kD == 128) ptx::tma_load_3d(qdst + kN * 128, &tp.tq, &full_q[qb], 64, head0, tok0);
+        }
+        qphase[qb] ^= 1;
+        qb ^= 1;
+        // ---- K/V tiles
+        for (int ti = 0; ti < d.ntiles; ++ti) {
+          const int64_t t0 = d.kb + (int64_t)ti * kTile;
+          if (kRow && tp.cp == 2) {
+            // TMA gather4 (sm_100): the K/V pools as 2-D [rows, D] tensors (a (page, slot, head) row
+            // is D contiguous elements); lane l loads token rows 4l .. 4l+3 of the tile, both
+            // 64-column halves of K and V: 4 instructions per lane, 128 per 64 KB tile, any page
+            // size. Rows past the chunk repeat its last row (masked in S, zeroed in V).
+            int rows[4];
+  #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int64_t t = imin64(t0 + 4 * lane + j, d.ke - 1);
+              const int64_t pg = __ldg(p.page_indices + d.page_begin + t / p.page_size);
+              rows[j] = (int)(pg * tp.row_s0 + (t % p.page_size) * tp.row_s1 + d.kvh * tp.row_s2);
+            }
+            if (lane == 0) {
+              ptx::mbar_wait(&empty[stage], ephase);
+              ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)kStageBytes / 4);
+            }
+            __syncwarp();
+            // role r: K or V = r >> 1, column half = r & 1
+            uint8_t* dst = smem + stage * kStageBytes + lane * 4 * 128 + (prole >> 1) * kKVBytes + (prole & 1) * kHalfBytes;
+            ptx::tma_gather4(dst, (prole >> 1) ? &tp.tv : &tp.tk, &full[stage], (prole & 1) * 64, rows[0], rows[1],
+                             rows[2], rows[3]);
+            __syncwarp();
+          } else if (kRow) {
+            // 16-byte cp.async gather, any page size (small pages, B_c not dividing 128): per
+            // instruction the warp moves 4 token rows x 128 B (lane = chunk c of row sub), written
+            // at the SW128 position TMA would use; rows past the chunk are zero-filled (no read).
+            const int c8 = lane & 7, sub = lane >> 3;
             ptx::mbar_wait(&empty[stage], ephase);
-            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)kStageBytes / 4);
-          }
-          __syncwarp();
-          // role r: K or V = r >> 1, column half = r & 1
-          uint8_t* dst = smem + stage * kStageBytes + lane * 4 * 128 + (prole >> 1) * kKVBytes + (prole & 1) * kHalfBytes;
-          ptx::tma_gather4(dst, (prole >> 1) ? &tp.tv : &tp.tk, &full[stage], (prole & 1) * 64, rows[0], rows[1],
-                           rows[2], rows[3]);
-          __syncwarp();
-        } else if (kRow) {
-          // 16-byte cp.async gather, any page size (small pages, B_c not dividing 128): per
-          // instruction the warp moves 4 token rows x 128 B (lane = chunk c of row sub), written
-          // at the SW128 position TMA would use; rows past the chunk are zero-filled (no read).
-          const int c8 = lane & 7, sub = lane >> 3;
-          ptx::mbar_wait(&empty[stage], ephase);
-          const uint32_t sK = ptx::smem_u32(smem + stage * kStageBytes), sV = sK + kKVBytes;
-          const uint16_t* kg = reinterpret_cast<const uint16_t*>(p.k);
-          const uint16_t* vg = reinterpret_cast<const uint16_t*>(p.v);
-#pragma unroll 1
-          for (int rb0 = 0; rb0 < kTile / 4; rb0 += 8) {
-            int64_t ko[8], vo[8];
-            bool ok[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {  // the 8 rows' page ids first (independent loads)
-              const int64_t t = t0 + 4 * (rb0 + u) + sub;
-              ok[u] = t < d.ke;
-              int64_t pg = 0, sl;
-              if (p.kv_ragged) {
-                sl = d.page_begin + t;
-              } else {
-                pg = ok[u] ? __ldg(p.page_indices + d.page_begin + t / p.page_size) : 0;
-                sl = t % p.page_size;
+            const uint32_t sK = ptx::smem_u32(smem + stage * kStageBytes), sV = sK + kKVBytes;
+            const uint16_t* kg = reinterpret_cast<const uint16_t*>(p.k);
+            const uint16_t* vg = reinterpret_cast<const uint16_t*>(p.v);
+  #pragma unroll 1
+            for (int rb0 = 0; rb0 < kTile / 4; rb0 += 8) {
+              int64_t ko[8], vo[8];
+              bool ok[8];
+  #pragma unroll
+              for (int u = 0; u < 8; ++u) {  // the 8 rows' page ids first (independent loads)
+                const int64_t t = t0 + 4 * (rb0 + u) + sub;
+                ok[u] = t < d.ke;
+                int64_t pg = 0, sl;
+                if (p.kv_ragged) {
+                  sl = d.page_begin + t;
+                } else {
+                  pg = ok[u] ? __ldg(p.page_indices + d.page_begin + t / p.page_size) : 0;
+                  sl = t % p.page_size;
+                }
+                ko[u] = ok[u] ? pg * p.ks0 + sl * p.ks1 + (int64_t)d.kvh * p.ks2 + c8 * 8 : 0;
+                vo[u] = ok[u] ? pg * p.vs0 + sl * p.vs1 + (int64_t)d.kvh * p.vs2 + c8 * 8 : 0;
               }
-              ko[u] = ok[u] ? pg * p.ks0 + sl * p.ks1 + (int64_t)d.kvh * p.ks2 + c8 * 8 : 0;
-              vo[u] = ok[u] ? pg * p.vs0 + sl * p.vs1 + (int64_t)d.kvh * p.vs2 + c8 * 8 : 0;
+  #pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const int r = 4 * (rb0 + u) + sub;
+                const uint32_t sw = (uint32_t)(r * 128 + ((c8 ^ (r & 7)) << 4));
+                cp_async16_zfill(sK + sw, kg + ko[u], ok[u]);
+                cp_async16_zfill(sK + kHalfBytes + sw, kg + ko[u] + 64, ok[u]);
+                cp_async16_zfill(sV + sw, vg + vo[u], ok[u]);
+                cp_async16_zfill(sV + kHalfBytes + sw, vg + vo[u] + 64, ok[u]);
+              }
             }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const int r = 4 * (rb0 + u) + sub;
-              const uint32_t sw = (uint32_t)(r * 128 + ((c8 ^ (r & 7)) << 4));
-              cp_async16_zfill(sK + sw, kg + ko[u], ok[u]);
-              cp_async16_zfill(sK + kHalfBytes + sw, kg + ko[u] + 64, ok[u]);
-              cp_async16_zfill(sV + sw, vg + vo[u], ok[u]);
-              cp_async16_zfill(sV + kHalfBytes + sw, vg + vo[u] + 64, ok[u]);
+            cp_async_mbar_arrive_noinc(&full[stage]);
+          } else {
+            // TMA: lane j handles sub-block j (one page, or 128 tokens of a big page)
+            const int n = (int)imin64(kTile, d.ke - t0);
+            const int nsub = (n + B - 1) / B;
+            int page = 0, off = 0;
+            if (lane < nsub) {
+              const int64_t tok = t0 + (int64_t)lane * B;
+              if (p.kv_ragged) {  // contiguous KV: token coordinate, no page table
+                off = (int)(d.page_begin + tok);
+              } else {
+                page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
+                off = (int)(tok % p.page_size);
+              }
             }
+            // role 0 loads K, role 1 V (a single role in the RoPE variant: both)
+            if (lane == 0) {
+              ptx::mbar_wait(&empty[stage], ephase);
+              if (prole == 0) DEC_TTRACE(0, tcount);
+              ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * (kD * 4) / nprod);
+            }
+            __syncwarp();
+            if (lane == 0 && it == it0 && ti == 0 && prole == 0) DEC_TRACE(8);
+            const bool doK = prole == 0, doV = prole == 1 || nprod == 1;
+            if (kGrp && lane < nsub) {  // one box per page: 8-token groups [lane*B/8, (lane+1)*B/8) of the tile
+              uint8_t* kd = smem + stage * kStageBytes + (lane * B >> 3) * 2048;
+              uint8_t* vd = kd + kKVBytes;
+              const int c4 = page * tp.cs + d.kvh;
+              if (doK) ptx::tma_load_5d(kd, &tp.tk, &full[stage], 0, 0, 0, off >> 3, c4);
+              if (doV) ptx::tma_load_5d(vd, &tp.tv, &full[stage], 0, 0, 0, off >> 3, c4);
+            } else if (lane < nsub) {
+              uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
+              uint8_t* vd = kd + kKVBytes;
+              if (doK) {
+                ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
+                if (kD == 128) ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
+              }
+              if (doV) {
+                ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
+                if (kD == 128) ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
+              }
+            }
+            __syncwarp();
           }
-          cp_async_mbar_arrive_noinc(&full[stage]);
-        } else {
-          // TMA: lane j handles sub-block j (one page, or 128 tokens of a big page)
-          const int n = (int)imin64(kTile, d.ke - t0);
-          const int nsub = (n + B - 1) / B;
-          int page = 0, off = 0;
-          if (lane < nsub) {
-            const int64_t tok = t0 + (int64_t)lane * B;
-            if (p.kv_ragged) {  // contiguous KV: token coordinate, no page table
-              off = (int)(d.page_begin + tok);
-            } else {
-              page = __ldg(p.page_indices + d.page_begin + tok / p.page_size);
-              off = (int)(tok % p.page_size);
-            }
+          ++tcount;
+          if (++stage == kStages) {
+            stage = 0;
+            ephase ^= 1;
           }
-          // role 0 loads K, role 1 V (a single role in the RoPE variant: both)
-          if (lane == 0) {
-            ptx::mbar_wait(&empty[stage], ephase);
-            if (prole == 0) DEC_TTRACE(0, tcount);
-            ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)nsub * B * (kD * 4) / nprod);
-          }
-          __syncwarp();
-          if (lane == 0 && it == it0 && ti == 0 && prole == 0) DEC_TRACE(8);
-          const bool doK = prole == 0, doV = prole == 1 || nprod == 1;
-          if (kGrp && lane < nsub) {  // one box per page: 8-token groups [lane*B/8, (lane+1)*B/8) of the tile
-            uint8_t* kd = smem + stage * kStageBytes + (lane * B >> 3) * 2048;
-            uint8_t* vd = kd + kKVBytes;
-            const int c4 = page * tp.cs + d.kvh;
-            if (doK) ptx::tma_load_5d(kd, &tp.tk, &full[stage], 0, 0, 0, off >> 3, c4);
-            if (doV) ptx::tma_load_5d(vd, &tp.tv, &full[stage], 0, 0, 0, off >> 3, c4);
-          } else if (lane < nsub) {
-            uint8_t* kd = smem + stage * kStageBytes + lane * B * 128;
-            uint8_t* vd = kd + kKVBytes;
-            if (doK) {
-              ptx::tma_load_4d(kd, &tp.tk, &full[stage], 0, d.kvh, off, page);
-              if (kD == 128) ptx::tma_load_4d(kd + kHalfBytes, &tp.tk, &full[stage], 64, d.kvh, off, page);
-            }
-            if (doV) {
-              ptx::tma_load_4d(vd, &tp.tv, &full[stage], 0, d.kvh, off, page);
-              if (kD == 128) ptx::tma_load_4d(vd + kHalfBytes, &tp.tv, &full[stage], 64, d.kvh, off, page);
-            }
-          }
-          __syncwarp();
-        }
-        ++tcount;
-        if (++stage == kStages) {
-          stage = 0;
-          ephase ^= 1;
         }
       }
-    }
     }  // prole < nprod
   } else if (warp == 5) {
     // ================================ MMA issuer ================================
