@@ -64,7 +64,14 @@ constexpr int kSmemBytes = kOffItems + dec::kStagedItems * 80 + 1024;  // + alig
 // 128 registers: fewer spills of the 16-column softmax state; each V converter thread takes 2
 // rows). Measured g = 16: 248 vs 264 us; g = 8 with 2 V warps was slower (147 vs 126 us).
 __host__ __device__ constexpr int v_warps(int kC) { return kC >= 16 ? 2 : 4; }
-__host__ __device__ constexpr int threads_for(int kC) { return 32 * (1 + 4 + v_warps(kC) + 4 + 1 + 4); }
+#ifndef BSRA_F8_PRODUCERS
+#define BSRA_F8_PRODUCERS 2
+#endif
+// + one V producer warp (the last warp) for kC <= 8: TMA issue is per-warp serialised
+// (scripts/tma_issue_bench.cu), so K and V page boxes come from two warps; kC = 16 keeps one
+// producer (its 128-register budget at 512 threads)
+__host__ __device__ constexpr int producers(int kC) { return kC >= 16 ? 1 : BSRA_F8_PRODUCERS; }
+__host__ __device__ constexpr int threads_for(int kC) { return 32 * (1 + 4 + v_warps(kC) + 4 + 1 + 4 + producers(kC) - 1); }
 constexpr uint32_t kTmemCols = 256;             // S^T 0 / 16, O^T 32 / 48 (item parity), K stages 64 + 64 k
 constexpr uint32_t kColO = 32, kColK = 64;
 constexpr float kRescaleThresh = 8.f;
@@ -119,6 +126,8 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
   constexpr int kWM = kWS0 + 4;        // MMA issuer
   constexpr int kWE0 = kWM + 1;        // first epilogue warp
   constexpr int kVR = 128 / (32 * kVW);  // token rows per V converter thread
+  constexpr int kNP = producers(kC);     // TMA producer warps: 0 (Q + K) and, if 2, the last (V)
+  constexpr int kWP1 = kWE0 + 4;         // the V producer warp
   const AttnParams& p = tp.p;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -157,7 +166,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kF8St; ++s) {
-      ptx::mbar_init(&f8full[s], 1);
+      ptx::mbar_init(&f8full[s], kNP);
       ptx::mbar_init(&f8empty[s], 128 + 32 * kVW);
     }
     for (int s = 0; s < kKSt; ++s) {
@@ -207,8 +216,11 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
   if (threadIdx.x == 0) F8T(9, 0);
   int tpos = 0;  // tiles seen by this role (trace index)
 
-  if (warp == 0) {
-    // ============================ TMA producer ============================
+  if (warp == 0 || (kNP == 2 && warp == kWP1)) {
+    // ============================ TMA producers ============================
+    // role 0 (warp 0): Q and the K page boxes; role 1 (the last warp): the V page boxes
+    const int role = warp == 0 ? 0 : 1;
+    const bool doK = role == 0, doV = role == 1 || kNP == 1;
     if (lane == 0) {
       ptx::tma_prefetch_desc(&tp.tq);
       ptx::tma_prefetch_desc(&tp.tk);
@@ -221,7 +233,7 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
     int qb = 0;
     for (int it = it0; it < it1; ++it) {
       const DecItem d = item_at(it);
-      if (lane == 0) {
+      if (lane == 0 && role == 0) {
         ptx::mbar_wait(&empty_q[qb], qphase[qb]);
         ptx::mbar_arrive_expect_tx(&full_q[qb], kQBytes);
         const int head0 = d.kvh * g + (g > kN ? d.row0 % g : 0);
@@ -248,15 +260,15 @@ __global__ void __launch_bounds__(f8d::threads_for(kC), 1) tc_decode_f8_kernel(c
         }
         if (lane == 0) {
           ptx::mbar_wait(&f8empty[stage], ephase);
-          ptx::mbar_arrive_expect_tx(&f8full[stage], (uint32_t)nsub * B * 256);
+          ptx::mbar_arrive_expect_tx(&f8full[stage], (uint32_t)nsub * B * 256 / kNP);
         }
         __syncwarp();
         if (lane < nsub) {
           uint8_t* kd = smem + stage * kF8StageBytes + lane * B * 128;
-          ptx::tma_load_4d(kd, &tp.tk, &f8full[stage], 0, d.kvh, off, page);
-          ptx::tma_load_4d(kd + kF8Half, &tp.tv, &f8full[stage], 0, d.kvh, off, page);
+          if (doK) ptx::tma_load_4d(kd, &tp.tk, &f8full[stage], 0, d.kvh, off, page);
+          if (doV) ptx::tma_load_4d(kd + kF8Half, &tp.tv, &f8full[stage], 0, d.kvh, off, page);
         }
-        if (lane == 0) F8T(0, tpos);
+        if (lane == 0 && role == 0) F8T(0, tpos);
         ++tpos;
         __syncwarp();
         if (++stage == kF8St) {
