@@ -9,10 +9,15 @@
 // streams HBM (decode is HBM-bound, fig:varlen).
 //
 // Warp roles (one CTA per SM, persistent over the CTA's plan queue; warp 5 issues the MMAs):
-//   warp 0      TMA producer: per page and 64-column half, one box {64 d, B_c tokens} of the
-//               4-D pool view (d, kv head, slot, page) — the BSR `indices` give the page coordinate
-//               (the sparse gather of §3.2.1, done by TMA). Runs ahead across items
-//               through a kStages-deep smem ring.
+//   warp 0      TMA producer (Q, K): per page one box of the 5-D pool view (d_lo, token_lo, half,
+//               token_hi, page * cs + head) — both 64-column halves, group-major tiles (kGrp) —
+//               or, half-major, one box {64 d, B_c tokens} per page and half of the 4-D view
+//               (d, kv head, slot, page); the BSR `indices` give the page coordinate (the sparse
+//               gather of §3.2.1, done by TMA). Runs ahead across items through a
+//               kStages-deep smem ring.
+//   warps 10-12 more TMA producers (plain variant): warp 10 issues the V boxes; for the row
+//               gather (gather4) warps 0 / 10 / 11 / 12 issue the K / V x column-half quarters —
+//               TMA issue is serialised per warp (scripts/tma_issue_bench.cu).
 //   warps 1..4  128 threads: thread = TMEM lane = token (softmax) = head-dim row d (output).
 //   warps 6..9  epilogue: O^T is double-buffered in TMEM (cols 32 / 48 by item parity); the
 //               softmax warps hand each finished item over (row-sum partials + running max in
