@@ -596,9 +596,20 @@ bsra_status launch_simt_d(const bsra::AttnParams& p, int D, int grid, cudaStream
 }
 
 template <typename TO, int D>
-bsra_status launch_contraction_t(const bsra::AttnParams& p, int grid, cudaStream_t st) {
-  bsra::contraction_kernel<TO, D><<<grid, 256, 0, st>>>(p);
-  CUDA_TRY(cudaGetLastError());
+bsra_status launch_contraction_t(const bsra::AttnParams& p, int grid, cudaStream_t st, bool pdl) {
+  // pdl: programmatic dependent launch — the kernel's blocks start (plan and list reads) while
+  // the attention kernel before it drains, and wait (griddepcontrol.wait) before the partials
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = pdl ? attr : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, bsra::contraction_kernel<TO, D>, p));
   return BSRA_OK;
 }
 
@@ -611,8 +622,8 @@ int contraction_grid(const bsra_engine* e) {
 }
 
 template <typename TO>
-bsra_status launch_contraction_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st) {
-  return D == 64 ? launch_contraction_t<TO, 64>(p, grid, st) : launch_contraction_t<TO, 128>(p, grid, st);
+bsra_status launch_contraction_d(const bsra::AttnParams& p, int D, int grid, cudaStream_t st, bool pdl) {
+  return D == 64 ? launch_contraction_t<TO, 64>(p, grid, st, pdl) : launch_contraction_t<TO, 128>(p, grid, st, pdl);
 }
 
 }  // namespace
@@ -788,9 +799,10 @@ bsra_status run_core(bsra_engine* e, const void* q, const void* k_pool, const vo
     e->have_deferred = true;
   } else if (!p.fused_merge) {  // contraction stage: fixed grid, exits at once if nothing split
     const int cgrid = contraction_grid(e);
-    if (c.o_dtype == BSRA_F32 || c.dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
-    else if (c.dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
-    else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
+    const bool pdl = (c.flags & BSRA_FLAG_PDL) != 0;
+    if (c.o_dtype == BSRA_F32 || c.dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st, pdl);
+    else if (c.dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st, pdl);
+    else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st, pdl);
     if (s) return s;
     e->last_launches = 2 + gather_launches;
   }
@@ -935,9 +947,10 @@ bsra_status bsra_contract(bsra_engine* e, const float* o_extra, const float* lse
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int cgrid = contraction_grid(e);
   bsra_status s;
-  if (o_dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st);
-  else if (o_dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st);
-  else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st);
+  const bool pdl = (c.flags & BSRA_FLAG_PDL) != 0;
+  if (o_dtype == BSRA_F32) s = launch_contraction_d<float>(p, c.head_dim, cgrid, st, pdl);
+  else if (o_dtype == BSRA_F16) s = launch_contraction_d<__half>(p, c.head_dim, cgrid, st, pdl);
+  else s = launch_contraction_d<__nv_bfloat16>(p, c.head_dim, cgrid, st, pdl);
   return s;
 }
 

@@ -179,10 +179,12 @@ __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant_
   // fused_contraction).
   constexpr int kPer = D / 32;
   constexpr int kGrp = 8;
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const PlanView pv = load_plan(p.plan);
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t total = (int64_t)pv.n_lists * pv.T_q;
+  bool waited = false;  // PDL: the partials (and o) belong to the kernel before: wait once, late
   for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < total; w += nwarps) {
     const int li = (int)(w / pv.T_q), r = (int)(w % pv.T_q);
     const int req = pv.list_req[li], kvh = pv.list_kvh[li], qt = pv.list_qtile[li];
@@ -195,6 +197,10 @@ __global__ void __launch_bounds__(256) contraction_kernel(const __grid_constant_
     const int tok = f / p.g, head = kvh * p.g + f % p.g;
     const int64_t orow = (qo_begin + tok) * (int64_t)p.H_qo + head;
     const int ns = s1 - s0;
+    if (!waited) {  // (a no-op without PDL) the plan / list reads above overlap the predecessor
+      asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      waited = true;
+    }
     // ---- one round of loads: lse of up to 32 slots (lane-parallel), o rows of the first group,
     // the extra state
     const float lse_l = lane < ns ? p.part_lse[(int64_t)slot_l * p.T_slot + r] : -INFINITY;

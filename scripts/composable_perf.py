@@ -55,8 +55,11 @@ def main():
     variants.append(("base_pdl", dict(prefix_tiles=(64, 128), balance=False, prefix_ctas=148, suffix_ctas=148,
                                       pdl=True)))
     variants.append(("pair_pdl", dict(prefix_ctas=148, suffix_ctas=148, pdl=True)))
-    for pc, sc in ((56, 92), (64, 84), (72, 76), (80, 68), (88, 60)):
+    for pc, sc in ((56, 92), (64, 84), (72, 76)):
         variants.append((f"conc_{pc}_{sc}", dict(prefix_ctas=pc, suffix_ctas=sc, concurrent=True)))
+    variants.append(("conc_64_84_nopdl", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=False)))
+    variants.append(("conc_64_84_prefix_pdl", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=True,
+                                                   suffix_pdl=False)))
     for name, kw in variants:
         comp = bsra.ComposableDecode(H_qo=32, H_kv=8, D=128, page_size=16, n_branch=n, **kw)
         comp.plan(c0.prefix, c0.suffix, c0.sm_scale)
