@@ -123,9 +123,11 @@ typedef struct {
   int32_t reserved[2];       /* must be zero                                                    */
 } bsra_config;
 
-/* flags: BSRA_FLAG_PDL launches the tcgen05 kernels with programmatic dependent launch: a run()
- * may start streaming K/V while the previous kernel on the stream drains, and waits for it
- * (griddepcontrol.wait) before writing o / lse / workspace. Only valid when the inputs of a
+/* flags: BSRA_FLAG_PDL launches the tcgen05 kernels and the contraction kernel (bsra_run of
+ * 64/128/256-row engines, bsra_contract) with programmatic dependent launch: a run() may start
+ * streaming K/V while the previous kernel on the stream drains, and waits for it
+ * (griddepcontrol.wait) before writing o / lse / workspace; the contraction kernel reads the
+ * plan early and waits before reading the partial states. Only valid when the inputs of a
  * run() (q, pools, indices, mask) are NOT produced by the kernel immediately preceding it on
  * the stream — e.g. consecutive layers' attention captured back to back. */
 #define BSRA_FLAG_PDL 1
