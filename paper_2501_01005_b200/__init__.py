@@ -422,9 +422,10 @@ class ComposableDecode:
 
     def __init__(self, *, H_qo, H_kv, D, page_size, n_branch, dtype="bf16", device=0, prefix_ctas=0,
                  suffix_ctas=0, kernel="auto", prefix_tiles=(64, 128, 256), balance=True, concurrent=False,
-                 pdl=False, suffix_pdl=None):
+                 pdl=False, suffix_pdl=None, suffix_first=False):
         self.n, self.H_qo, self.D = n_branch, H_qo, D
         self.concurrent = concurrent
+        self.suffix_first = suffix_first  # sequential order: suffix kernel, then prefix kernel
         self.prefix = Engine(make_config(H_qo=H_qo, H_kv=H_kv, D=D, page_size=page_size, dtype=dtype, o_dtype="f32",
                                          max_batch=1, max_total_qo_rows=n_branch, num_ctas=prefix_ctas,
                                          tile_set=prefix_tiles, kernel=kernel, balance_ctas=balance, pdl=pdl,
@@ -454,6 +455,9 @@ class ComposableDecode:
             self.prefix.run(q, k_pool, v_pool, strides, strides, prefix_indices, self.o_p, self.l_p, stream=self.side)
             self.suffix.run(q, k_pool, v_pool, strides, strides, suffix_indices, self.o_s, self.l_s, stream=st)
             st.wait_stream(self.side)
+        elif self.suffix_first:
+            self.suffix.run(q, k_pool, v_pool, strides, strides, suffix_indices, self.o_s, self.l_s, stream=st)
+            self.prefix.run(q, k_pool, v_pool, strides, strides, prefix_indices, self.o_p, self.l_p, stream=st)
         else:
             self.prefix.run(q, k_pool, v_pool, strides, strides, prefix_indices, self.o_p, self.l_p, stream=st)
             self.suffix.run(q, k_pool, v_pool, strides, strides, suffix_indices, self.o_s, self.l_s, stream=st)
