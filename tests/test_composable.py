@@ -152,3 +152,13 @@ def test_gpu_contract_errors(cuda_device):
     from tests.helpers import assert_close
     assert_close((o.float().cpu().numpy(), lse.cpu().numpy()), oracle.attention_from_inputs(inp), "bf16",
                  what="deferred, unsplit")
+
+
+@pytest.mark.gpu
+def test_gpu_composable_suffix_first_pdl(cuda_device):
+    """Sequential order suffix -> prefix -> bsra_contract with PDL between the launches."""
+    from tests.helpers import assert_close
+    ci = synth.c4_composable(n_branch=32, prefix_len=4096, suffix_len=200, device=cuda_device)
+    gpu = _gpu_composable(ci, cuda_device, prefix_ctas=148, suffix_ctas=148, pdl=True, suffix_first=True)
+    assert gpu[2].fold_suffix
+    assert_close(gpu, _oracle(ci, "single"), "bf16", what="suffix first, PDL")
