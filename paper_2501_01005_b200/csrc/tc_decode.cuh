@@ -15,9 +15,10 @@
 //               (d, kv head, slot, page); the BSR `indices` give the page coordinate (the sparse
 //               gather of §3.2.1, done by TMA). Runs ahead across items through a
 //               kStages-deep smem ring.
-//   warps 10-12 more TMA producers (plain variant): warp 10 issues the V boxes; for the row
-//               gather (gather4) warps 0 / 10 / 11 / 12 issue the K / V x column-half quarters —
-//               TMA issue is serialised per warp (scripts/tma_issue_bench.cu).
+//   warps 10-12 more TMA producers (plain variant): warp 10 issues the V boxes; the row-gather
+//   (10-16)     variant has 8 producer warps (0, 10..16), each issuing one K / V x column-half
+//               quarter of half the tile's rows — TMA issue is serialised per warp
+//               (scripts/tma_issue_bench.cu).
 //   warps 1..4  128 threads: thread = TMEM lane = token (softmax) = head-dim row d (output).
 //   warps 6..9  epilogue: O^T is double-buffered in TMEM (cols 32 / 48 by item parity); the
 //               softmax warps hand each finished item over (row-sum partials + running max in
@@ -105,7 +106,8 @@ constexpr int kThreadsRope = 576;  // + 8 RoPE warps (two per SM sub-partition) 
 // scripts/tma_issue_bench.cu), so K and V boxes (and the four gather4 quarters) come from
 // different warps.
 constexpr int kThreadsPlain = kThreads + 96;
-constexpr int threads_for(bool rope) { return rope ? kThreadsRope : kThreadsPlain; }
+constexpr int kThreadsRow = kThreads + 224;  // row gather: 8 producer warps (0, 10..16)
+constexpr int threads_for(bool rope, bool row = false) { return rope ? kThreadsRope : row ? kThreadsRow : kThreadsPlain; }
 constexpr uint32_t kTmemCols = 64;  // S^T buffers at cols 0 / 16, O^T double buffer at 32 / 48
 constexpr float kRescaleThresh = 8.f;  // log2 units: rescale O only when the max grows by > 2^8
 }  // namespace dec
@@ -183,7 +185,7 @@ __device__ __forceinline__ void rope_chunk(uint8_t* lo, uint8_t* hi, int64_t pos
 // (scripts/tma_issue_bench.cu), so half the boxes per tile. Paged pools only (the 8-token groups
 // need page-aligned tiles); the MMA descriptors take SBO = 2048 and the half offset 1024.
 template <int kC, int kMask, bool kF16, bool kRope, bool kRow = false, int kD = 128, bool kGrp = false>
-__global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
+__global__ void __launch_bounds__(dec::threads_for(kRope, kRow), 1) tc_decode_kernel(const __grid_constant__ TcParams tp) {
   static_assert(kD == 128 || (kD == 64 && !kRope && !kRow), "head_dim 64: box gather, no RoPE");
   static_assert(!kGrp || (kD == 128 && !kRope && !kRow), "group-major tiles: plain box gather, head_dim 128");
   constexpr int kRowG = kGrp ? 2048 : 1024;                // bytes between 8-row groups of a K/V tile (SBO)
@@ -232,11 +234,11 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
   for (int k = threadIdx.x; k < min(kStagedItems, it1 - it0); k += blockDim.x) staged[k] = dec_item(pv, it0 + k, g);
   auto item_at = [&](int it) { return it - it0 < kStagedItems ? staged[it - it0] : dec_item(pv, it, g); };
 
-  // producer warps: warp 0 (Q and K), 10 (V), 11 / 12 (gather4: the V halves; 0 / 10 the K halves)
+  // producer warps: warp 0 (Q and K), 10 (V); gather4: warps 0, 10..16 (quarter x half of the rows)
 #ifndef BSRA_BOX_PRODUCERS
 #define BSRA_BOX_PRODUCERS 2
 #endif
-  const int nprod = kRope || (kRow && tp.cp == 1) ? 1 : (kRow && tp.cp == 2 ? 4 : BSRA_BOX_PRODUCERS);
+  const int nprod = kRope || (kRow && tp.cp == 1) ? 1 : (kRow && tp.cp == 2 ? 8 : BSRA_BOX_PRODUCERS);
   if (threadIdx.x == 0) {
     DEC_TRACE(0);
     for (int s = 0; s < kStages; ++s) {
@@ -278,7 +280,7 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
   if (p.trace && threadIdx.x == 0) p.trace[16 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
 #endif
 
-  const int prole = warp == 0 ? 0 : (!kRope && warp >= 10 ? warp - 9 : -1);  // producer role
+  const int prole = warp == 0 ? 0 : (!kRope && warp >= 10 ? warp - 9 : -1);  // producer role (warps 10..)
   if (prole >= 0) {
     // ============================ TMA producers ============================
     // role 0: Q + K (box path) / K half 0 (gather4) / everything (cp.async, RoPE variant); role 1:
@@ -327,13 +329,16 @@ __global__ void __launch_bounds__(dec::threads_for(kRope), 1) tc_decode_kernel(c
             }
             if (lane == 0) {
               ptx::mbar_wait(&empty[stage], ephase);
-              ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)kStageBytes / 4);
+              ptx::mbar_arrive_expect_tx(&full[stage], (uint32_t)kStageBytes / 8);
             }
             __syncwarp();
-            // role r: K or V = r >> 1, column half = r & 1
-            uint8_t* dst = smem + stage * kStageBytes + lane * 4 * 128 + (prole >> 1) * kKVBytes + (prole & 1) * kHalfBytes;
-            ptx::tma_gather4(dst, (prole >> 1) ? &tp.tv : &tp.tk, &full[stage], (prole & 1) * 64, rows[0], rows[1],
-                             rows[2], rows[3]);
+            // role r: quarter q = r & 3 (K or V = q >> 1, column half = q & 1), lanes 16 (r >> 2) .. +15
+            const int q = prole & 3;
+            if ((lane >> 4) == (prole >> 2)) {
+              uint8_t* dst = smem + stage * kStageBytes + lane * 4 * 128 + (q >> 1) * kKVBytes + (q & 1) * kHalfBytes;
+              ptx::tma_gather4(dst, (q >> 1) ? &tp.tv : &tp.tk, &full[stage], (q & 1) * 64, rows[0], rows[1], rows[2],
+                               rows[3]);
+            }
             __syncwarp();
           } else if (kRow) {
             // 16-byte cp.async gather, any page size (small pages, B_c not dividing 128): per

@@ -123,7 +123,7 @@ cudaError_t launch_decode_t(const TcParams& tp, int grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int nt = dec::threads_for(kRope);
+  const int nt = dec::threads_for(kRope, kRow);
   if (tp.f16) return launch_tc(tc_decode_kernel<kC, kMask, true, kRope, kRow, kD, kGrp>, grid, nt, dec::kSmemBytes, st, tp);
   return launch_tc(tc_decode_kernel<kC, kMask, false, kRope, kRow, kD, kGrp>, grid, nt, dec::kSmemBytes, st, tp);
   }
