@@ -962,7 +962,7 @@ def main():
     achieved = by["total"] / (region_launch_ms * 1e-3) / 1e9
     traffic = None
     traffic_src = None
-    for fn, key in (("r02c_ncu_traffic.json", "tc_decode"), ("r02b_ncu_traffic.json", "tc_decode")):
+    for fn, key in (("r02d_ncu_traffic.json", "tc_decode"), ("r02c_ncu_traffic.json", "tc_decode")):
         try:  # DRAM read+write per launch from the committed ncu --set full capture of this kernel
             with open(os.path.join(ROOT, "profiles", fn)) as f:
                 traffic = json.load(f)[key]["traffic_bytes"]
