@@ -162,3 +162,13 @@ def test_gpu_composable_suffix_first_pdl(cuda_device):
     gpu = _gpu_composable(ci, cuda_device, prefix_ctas=148, suffix_ctas=148, pdl=True, suffix_first=True)
     assert gpu[2].fold_suffix
     assert_close(gpu, _oracle(ci, "single"), "bf16", what="suffix first, PDL")
+
+
+@pytest.mark.gpu
+def test_gpu_composable_deterministic(cuda_device):
+    """The bench's concurrent step (64 + 84 SMs, one bsra_contract) is bitwise reproducible: the
+    prefix chunks, the suffix rows and the fold run in a fixed order whatever the timing."""
+    ci = synth.c4_composable(n_branch=64, prefix_len=4096, suffix_len=256, device=cuda_device)
+    a = _gpu_composable(ci, cuda_device, prefix_ctas=64, suffix_ctas=84, concurrent=True)
+    b = _gpu_composable(ci, cuda_device, prefix_ctas=64, suffix_ctas=84, concurrent=True)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
