@@ -232,7 +232,8 @@ bsra_status bsra_run(bsra_engine* e, const void* q, const void* k_pool, const vo
  * in the same closed form (the composable formats' prefix ⊕ suffix). Rows the run
  * wrote through (unsplit items, App. D.2) are not touched, so an extra state requires a plan in
  * which every item is split (bsra_plan_stats / the image: n_slots == n_items): BSRA_EUNSUPPORTED
- * otherwise. o_extra / lse_extra: both or neither. May be captured in a CUDA graph with the run.
+ * otherwise. o_extra / lse_extra: both or neither. A new plan cancels the pending contraction (the
+ * next bsra_contract needs a run of that plan first). May be captured in a CUDA graph with the run.
  * Errors: EINVAL (no deferred run, flag not set, NULL o, bad o_dtype), EUNSUPPORTED. */
 bsra_status bsra_contract(bsra_engine* e, const float* o_extra, const float* lse_extra, void* o, int32_t o_dtype,
                           float* lse, void* stream);

@@ -444,6 +444,7 @@ bsra_status plan_core(bsra_engine* e, const int32_t* qo_indptr, const int32_t* p
   e->image.swap(im);
   e->summary = sum;
   e->planned = true;
+  e->have_deferred = false;  // bsra_contract needs a run of this plan
   e->device_planned = false;
   e->f8_prefill = f8_prefill;
   e->f8_rows = f8_rows;
@@ -528,6 +529,7 @@ bsra_status bsra_plan_device(bsra_engine* e, int32_t batch, const int32_t* d_qo_
   e->summary.T_q = c.tile_q;
   e->summary.n_items = 1;  // unknown on the host: run() validates its pointers
   e->planned = true;
+  e->have_deferred = false;  // bsra_contract needs a run of this plan
   e->device_planned = true;
   e->f8_prefill = false;
   e->f8_rows = 0;

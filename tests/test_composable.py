@@ -172,3 +172,25 @@ def test_gpu_composable_deterministic(cuda_device):
     a = _gpu_composable(ci, cuda_device, prefix_ctas=64, suffix_ctas=84, concurrent=True)
     b = _gpu_composable(ci, cuda_device, prefix_ctas=64, suffix_ctas=84, concurrent=True)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.gpu
+def test_gpu_contract_after_replan_needs_a_run(cuda_device):
+    """A new plan cancels the pending contraction: bsra_contract between plan() and run() is EINVAL."""
+    import paper_2501_01005_b200 as bsra
+    wl = synth.Workload("cr", 8, 2, 128, 16, "bf16", "none", np.array([4, 4], np.int32), np.array([640, 64], np.int32))
+    inp = synth.make_inputs(wl, device=cuda_device)
+    eng = bsra.Engine(bsra.make_config(H_qo=8, H_kv=2, D=128, page_size=16, max_batch=2, max_total_qo_rows=8,
+                                       tile_q=64, num_ctas=8, defer_contraction=True), 0)
+    o = torch.empty((8, 8, 128), device=cuda_device, dtype=torch.bfloat16)
+    lse = torch.empty((8, 8), device=cuda_device)
+    eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+    eng.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse)
+    eng.contract(o, lse)
+    torch.cuda.synchronize()
+    from tests.helpers import assert_close
+    assert_close((o.float().cpu().numpy(), lse.cpu().numpy()), oracle.attention_from_inputs(inp), "bf16",
+                 what="deferred, split rows")
+    eng.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+    with pytest.raises(bsra.BsraError, match="no deferred run"):
+        eng.contract(o, lse)
