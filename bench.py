@@ -722,7 +722,8 @@ def bench_quest(dev, pk):
     block 16, 32/32 heads, d 128, batch 1; each head keeps `page_budget` pages of its seq_len/16
     (synth.quest_decode). Per-launch latency (median of 9, CUDA events) through the decode
     kernel; the paper's H100 latencies quoted as context, not as a target. Timed as a CUDA graph of
-    20 back-to-back launches (PDL) ÷ 20, so host enqueue cost is out of the figure."""
+    20 back-to-back launches (PDL) ÷ 20, so host enqueue cost is out of the figure; `us_serialised`
+    is the same without PDL (no overlap between consecutive launches)."""
     paper_h100_us = {(4096, 64): 20.299, (4096, 256): 44.383, (32768, 64): 22.371, (32768, 512): 68.478}
     out = {"unit": "us per launch", "paper": "FlashInfer on H100 SXM5, Table eval-sparsity-flashinfer"}
     for (S, P), ref in paper_h100_us.items():
@@ -742,10 +743,21 @@ def bench_quest(dev, pk):
                 e.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse,
                       stream=s)
         us = time_graph(twenty, s, 10) / 20 * 1e3
+        # the same 20 launches without PDL: fully serialised, so no overlap of one launch's
+        # prologue / loads with the previous one's tail (the per-kernel latency the paper quotes)
+        cfg.flags &= ~bsra.FLAG_PDL
+        e2 = bsra.Engine(cfg, torch.cuda.current_device())
+        e2.plan(inp.qo_indptr, inp.kv_page_indptr, inp.kv_last_page_len, inp.sm_scale)
+
+        def twenty_serial():
+            for _ in range(20):
+                e2.run(inp.q, inp.k_pool, inp.v_pool, inp.k_strides, inp.v_strides, inp.kv_page_indices, o, lse,
+                       stream=s)
+        us_serial = time_graph(twenty_serial, s, 10) / 20 * 1e3
         by = decode_bytes(wl)["total"]
-        out[f"seq{S}_budget{P}"] = {"us": us, "TB/s": by / (us * 1e-6) / 1e12, "bytes": by,
-                                    "paper_h100_us": ref, "kernel": e.selected_kernel()}
-        del inp, e
+        out[f"seq{S}_budget{P}"] = {"us": us, "TB/s": by / (us * 1e-6) / 1e12, "us_serialised": us_serial,
+                                    "bytes": by, "paper_h100_us": ref, "kernel": e.selected_kernel()}
+        del inp, e, e2
         torch.cuda.empty_cache()
     return out
 
