@@ -60,6 +60,8 @@ def main():
     variants.append(("pair_pdl_suffix_first", dict(prefix_ctas=148, suffix_ctas=148, pdl=True, suffix_first=True)))
     variants.append(("pair_suffix_first", dict(prefix_ctas=148, suffix_ctas=148, suffix_first=True)))
     variants.append(("conc_64_84_nopdl", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=False)))
+    variants.append(("conc_64_84_suffix_pdl", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=False,
+                                                   suffix_pdl=True)))
     variants.append(("conc_64_84_prefix_pdl", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=True,
                                                    suffix_pdl=False)))
     for name, kw in variants:
