@@ -42,8 +42,14 @@ namespace bsra {
 namespace f8d {
 constexpr int kTile = 128;
 constexpr int kN = 16;
-constexpr int kF8St = 4;                        // fp8 landing ring
-constexpr int kVSt = 2;                         // 16-bit V ring
+#ifndef BSRA_F8_ST
+#define BSRA_F8_ST 4
+#endif
+#ifndef BSRA_F8_VST
+#define BSRA_F8_VST 2
+#endif
+constexpr int kF8St = BSRA_F8_ST;               // fp8 landing ring
+constexpr int kVSt = BSRA_F8_VST;               // 16-bit V ring
 constexpr int kKSt = 3;                         // K stages in TMEM (64 columns each)
 constexpr int kF8Half = kTile * 128;            // K or V of one tile in fp8: 16 KB
 constexpr int kF8StageBytes = 2 * kF8Half;
