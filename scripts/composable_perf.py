@@ -60,6 +60,9 @@ def main():
     variants.append(("pair_pdl_suffix_first", dict(prefix_ctas=148, suffix_ctas=148, pdl=True, suffix_first=True)))
     variants.append(("pair_suffix_first", dict(prefix_ctas=148, suffix_ctas=148, suffix_first=True)))
     variants.append(("conc_64_84_nopdl", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=False)))
+    variants.append(("conc_64_84_tq128", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, prefix_tiles=(64, 128))))
+    variants.append(("conc_56_92_tq128", dict(prefix_ctas=56, suffix_ctas=92, concurrent=True, prefix_tiles=(64, 128))))
+    variants.append(("conc_72_76_tq128", dict(prefix_ctas=72, suffix_ctas=76, concurrent=True, prefix_tiles=(64, 128))))
     variants.append(("conc_64_84_suffix_pdl", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=False,
                                                    suffix_pdl=True)))
     variants.append(("conc_64_84_prefix_pdl", dict(prefix_ctas=64, suffix_ctas=84, concurrent=True, pdl=True,
