@@ -15,6 +15,7 @@
 //               (d, kv head, slot, page); the BSR `indices` give the page coordinate (the sparse
 //               gather of §3.2.1, done by TMA). Runs ahead across items through a
 //               kStages-deep smem ring.
+//   warp 18     (fused-RoPE variant) the V producer
 //   warps 10-12 more TMA producers (plain variant): warp 10 issues the V boxes; the row-gather
 //   (10-16)     variant has 8 producer warps (0, 10..16), each issuing one K / V x column-half
 //               quarter of half the tile's rows — TMA issue is serialised per warp
@@ -100,7 +101,12 @@ constexpr int kStagedItems = 64;  // the CTA's first queue entries, decoded once
 constexpr int kOffMeta = kOffItems + kStagedItems * 80;  // merge-list metadata of staged split items
 constexpr int kSmemBytes = kOffMeta + kStagedItems * 32 + 1024;  // + alignment slack
 constexpr int kThreads = 320;  // producer, 4 softmax warps, MMA warp, 4 epilogue warps
-constexpr int kThreadsRope = 576;  // + 8 RoPE warps (two per SM sub-partition) in the fused-RoPE variant
+#ifndef BSRA_ROPE_PRODUCERS
+#define BSRA_ROPE_PRODUCERS 2
+#endif
+// + 8 RoPE warps (two per SM sub-partition) in the fused-RoPE variant, and (2 producers) warp 18
+// issuing the V boxes
+constexpr int kThreadsRope = 576 + 32 * (BSRA_ROPE_PRODUCERS - 1);
 // Plain variant: + 3 producer warps (10..12). TMA issue is per-warp serialised (~65-160 cycles per
 // instruction whatever the box size, and it scales with the number of issuing warps:
 // scripts/tma_issue_bench.cu), so K and V boxes (and the four gather4 quarters) come from
@@ -238,7 +244,8 @@ __global__ void __launch_bounds__(dec::threads_for(kRope, kRow), 1) tc_decode_ke
 #ifndef BSRA_BOX_PRODUCERS
 #define BSRA_BOX_PRODUCERS 2
 #endif
-  const int nprod = kRope || (kRow && tp.cp == 1) ? 1 : (kRow && tp.cp == 2 ? 8 : BSRA_BOX_PRODUCERS);
+  const int nprod = kRope ? BSRA_ROPE_PRODUCERS
+                          : (kRow && tp.cp == 1) ? 1 : (kRow && tp.cp == 2 ? 8 : BSRA_BOX_PRODUCERS);
   if (threadIdx.x == 0) {
     DEC_TRACE(0);
     for (int s = 0; s < kStages; ++s) {
@@ -280,7 +287,8 @@ __global__ void __launch_bounds__(dec::threads_for(kRope, kRow), 1) tc_decode_ke
   if (p.trace && threadIdx.x == 0) p.trace[16 * 1024 + blockIdx.x] = (long long)ptx::globaltimer_ns();
 #endif
 
-  const int prole = warp == 0 ? 0 : (!kRope && warp >= 10 ? warp - 9 : -1);  // producer role (warps 10..)
+  // producer role: warp 0, then warps 10.. (plain / row variants) or warp 18 (RoPE variant)
+  const int prole = warp == 0 ? 0 : (!kRope && warp >= 10 ? warp - 9 : (kRope && warp == 18 ? 1 : -1));
   if (prole >= 0) {
     // ============================ TMA producers ============================
     // role 0: Q + K (box path) / K half 0 (gather4) / everything (cp.async, RoPE variant); role 1:
